@@ -1,0 +1,21 @@
+"""fp64 CPU oracle for fused attention forward/backward (HipKittens, arXiv 2511.08083).
+
+TEST INFRASTRUCTURE ONLY. Only `tests/`, `__graft_entry__.smoke()` and the
+`cpu_baseline` / `--impl reference` legs of `bench.py` may import this package.
+The product path (`paper_2511_08083_b200`) never imports it and shares no code
+with it: no kernels, headers, helpers, constants or pre/post-processing.
+
+Pinned by `tests/test_oracle_*.py` (closed forms, invariants, finite
+differences, a library special case and the paper's printed constants).
+No function here is "parity unpinned".
+"""
+from .attention import (  # noqa: F401
+    LN2,
+    LOG2E,
+    attn_fwd,
+    attn_fwd_bwd,
+    attn_naive,
+    attn_rows,
+    attn_key_rows,
+    softmax_scale,
+)

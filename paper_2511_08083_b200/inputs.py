@@ -1,0 +1,80 @@
+"""Seeded synthetic inputs (shared by the oracle tests and the CUDA path).
+
+Holds none of the method's arithmetic: only random-number generation.
+
+Recipe (reading #15): Q, K, V and
+dO are i.i.d. N(0, std^2) drawn in fp32 and rounded to bf16 (RNE), BNHD
+contiguous, the paper's N(0,1) inputs. Every (tensor, b, kvh)
+block is drawn from its own generator seeded with splitmix64(seed, t, b, kvh),
+so a rank that owns only some batches produces exactly the values the 1-GPU
+run would have for those batches.
+"""
+from __future__ import annotations
+
+import torch
+
+_M64 = (1 << 64) - 1
+TENSOR_IDS = {"Q": 1, "K": 2, "V": 3, "dO": 4}
+
+
+def splitmix64(*xs: int) -> int:
+    """Fold integers through splitmix64; returns a 63-bit seed."""
+    z = 0x9E3779B97F4A7C15
+    for x in xs:
+        z = (z + (int(x) & _M64) + 0x9E3779B97F4A7C15) & _M64
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+        z = z ^ (z >> 31)
+    return z & ((1 << 63) - 1)
+
+
+def _block(shape, seed, device, std):
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    x = torch.randn(shape, generator=g, device=device, dtype=torch.float32)
+    if std != 1.0:
+        x.mul_(std)
+    return x.to(torch.bfloat16)
+
+
+def make_inputs(B, N, Hq, Hkv, d, seed=0, device="cpu", std=1.0, batches=None,
+                tensors=("Q", "K", "V", "dO")):
+    """Return dict name -> bf16 tensor. Q/dO [B', N, Hq, d], K/V [B', N, Hkv, d].
+
+    `batches` (default all of range(B)) selects which global batch indices to
+    generate, in order; the values for batch b do not depend on which other
+    batches are generated. `std` scales Q/K/V/dO (stress tests use 4.0).
+    """
+    if Hq % Hkv:
+        raise ValueError("Hq must be a multiple of Hkv")
+    G = Hq // Hkv
+    batches = list(range(B)) if batches is None else list(batches)
+    out = {}
+    for name in tensors:
+        t = TENSOR_IDS[name]
+        heads = Hq if name in ("Q", "dO") else Hkv
+        x = torch.empty((len(batches), N, heads, d), dtype=torch.bfloat16, device=device)
+        for bi, b in enumerate(batches):
+            for kvh in range(Hkv):
+                if name in ("Q", "dO"):
+                    blk = _block((N, G, d), splitmix64(seed, t, b, kvh), device, std)
+                    x[bi, :, kvh * G:(kvh + 1) * G, :] = blk
+                else:
+                    blk = _block((N, d), splitmix64(seed, t, b, kvh), device, std)
+                    x[bi, :, kvh, :] = blk
+        out[name] = x
+    return out
+
+
+def sample_rows(N: int, count: int, seed: int, diag_tile: int = 128):
+    """Row sample for ROW-mode checks: first 8, last 8, tile
+    edges (multiples of 128 +- 1) and random rows; sorted, unique."""
+    g = torch.Generator().manual_seed(splitmix64(seed, 99))
+    rows = set(range(min(8, N))) | set(range(max(0, N - 8), N))
+    for t in range(diag_tile, N, diag_tile):
+        for r in (t - 1, t, t + 1):
+            if 0 <= r < N and len(rows) < count // 2 + 16:
+                rows.add(r)
+    while len(rows) < min(count, N):
+        rows.add(int(torch.randint(0, N, (1,), generator=g)))
+    return sorted(rows)
