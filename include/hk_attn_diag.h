@@ -1,0 +1,25 @@
+/* hk_attn_diag.h — diagnostic entry points of libhkattn.so (not the hot path).
+ *
+ * hk_diag_umma: one 128 x N output tile through tcgen05, to pin the
+ * UMMA instruction/shared-memory descriptor encodings the attention kernels
+ * rely on, in isolation.
+ *   A : device bf16 [128][K] row-major.
+ *   B : device bf16; b_mn == 0: [N][K] row-major and D = A * B^T (B K-major);
+ *                    b_mn != 0: [K][N] row-major and D = A * B   (B MN-major).
+ *   D : device fp32 [128][N] row-major, overwritten.
+ *   a_tmem != 0 stages A in tensor memory (the P*V / dS*K operand form),
+ *   otherwise A is read from shared memory (K-major).
+ * Supported: N in {64, 128}, K in {64, 128}. Same error conventions as hk_attn.h.
+ */
+#ifndef HK_ATTN_DIAG_H_
+#define HK_ATTN_DIAG_H_
+#include "hk_attn.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+hk_status hk_diag_umma(const void* A, const void* B, float* D, int N, int K, int a_tmem, int b_mn,
+                       cudaStream_t stream);
+#ifdef __cplusplus
+}
+#endif
+#endif

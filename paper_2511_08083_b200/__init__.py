@@ -1,0 +1,6 @@
+"""B200-native (sm_100a) fused bf16 attention forward/backward.
+
+The data-parallel hot path of HipKittens (arXiv 2511.08083): MHA/GQA,
+causal and non-causal, head dim 64/128, behind the C ABI in include/hk_attn.h.
+"""
+from .api import Attention, HKError, attn_bwd, attn_fwd, bwd_workspace_bytes  # noqa: F401

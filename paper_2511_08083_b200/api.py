@@ -1,0 +1,103 @@
+"""Python binding of the C ABI (include/hk_attn.h): argument marshalling only.
+
+Every step of the computation runs in libhkattn.so's sm_100a kernels; torch is
+used for device memory and the current stream. There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from ._lib import HKError, check, lib  # noqa: F401
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _check_tensor(name, t, dtype=torch.bfloat16):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (BNHD)")
+    if t.device != torch.device("cuda", torch.cuda.current_device()):
+        raise ValueError(f"{name} must live on the current CUDA device")
+
+
+def _shapes(q, k, v):
+    if q.dim() != 4 or k.dim() != 4 or v.shape != k.shape:
+        raise ValueError("q must be [B,N,Hq,d]; k, v [B,N,Hkv,d]")
+    B, N, Hq, d = q.shape
+    if k.shape[0] != B or k.shape[1] != N or k.shape[3] != d:
+        raise ValueError("k/v shape mismatch with q")
+    return B, N, Hq, k.shape[2], d
+
+
+def attn_fwd(q, k, v, causal: bool = False, out=None, lse=None):
+    """O, LSE = attention(q, k, v). q [B,N,Hq,d], k/v [B,N,Hkv,d] bf16 CUDA.
+    Returns (o [B,N,Hq,d] bf16, lse [B,Hq,N] fp32, natural log)."""
+    for n, t in (("q", q), ("k", k), ("v", v)):
+        _check_tensor(n, t)
+    B, N, Hq, Hkv, d = _shapes(q, k, v)
+    o = torch.empty_like(q) if out is None else out
+    L = torch.empty((B, Hq, N), dtype=torch.float32, device=q.device) if lse is None else lse
+    _check_tensor("out", o)
+    _check_tensor("lse", L, torch.float32)
+    check(lib().hk_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, Hq, Hkv, N, d, int(bool(causal)),
+                            _stream()))
+    return o, L
+
+
+def bwd_workspace_bytes(B, Hq, Hkv, N, d) -> int:
+    return int(lib().hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d))
+
+
+def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None, dk=None, dv=None):
+    """dQ, dK, dV of L = sum(O * dO) for O = attention(q, k, v).
+    Returns (dq, dk, dv) bf16, plus the workspace holds D = rowsum(dO*O) then LSE*log2e."""
+    for n, t in (("q", q), ("k", k), ("v", v), ("o", o), ("do", do)):
+        _check_tensor(n, t)
+    _check_tensor("lse", lse, torch.float32)
+    B, N, Hq, Hkv, d = _shapes(q, k, v)
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    nbytes = bwd_workspace_bytes(B, Hq, Hkv, N, d)
+    ws = torch.empty(nbytes // 4, dtype=torch.float32, device=q.device) if workspace is None else workspace
+    check(lib().hk_attn_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
+                            _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), B, Hq, Hkv, N, d,
+                            int(bool(causal)), _stream()))
+    return dq, dk, dv
+
+
+class Attention(torch.autograd.Function):
+    """autograd wrapper: Attention.apply(q, k, v, causal) -> o."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, causal=False):
+        o, lse = attn_fwd(q, k, v, causal)
+        ctx.save_for_backward(q, k, v, o, lse)
+        ctx.causal = causal
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, o, lse = ctx.saved_tensors
+        dq, dk, dv = attn_bwd(q, k, v, o, lse, do.contiguous(), ctx.causal)
+        return dq, dk, dv, None
+
+
+def diag_umma(a, b, n, k, a_tmem: bool, b_mn: bool):
+    """Diagnostic single-tile tcgen05 GEMM (include/hk_attn_diag.h)."""
+    _check_tensor("a", a)
+    _check_tensor("b", b)
+    d = torch.empty((128, n), dtype=torch.float32, device=a.device)
+    check(lib().hk_diag_umma(_ptr(a), _ptr(b), _ptr(d), n, k, int(a_tmem), int(b_mn), _stream()))
+    return d

@@ -1,0 +1,223 @@
+// libhkattn.so: C ABI (include/hk_attn.h) over the sm_100a attention kernels.
+// Host side only validates, encodes TMA maps and launches; every step of the
+// computation runs in the kernels below.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <utility>
+
+#include "../../include/hk_attn.h"
+#include "../../include/hk_attn_diag.h"
+#include "bwd.cuh"
+#include "fwd.cuh"
+#include "tma_host.h"
+#include "umma_diag.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+hk_status fail(hk_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+hk_status fail(hk_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + nb && y < x + na;
+}
+
+hk_status check_device(int* num_sms) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(HK_ERR_DEVICE, "cudaGetDevice failed");
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(HK_ERR_DEVICE, "device %d is sm_%d%d; libhkattn is built for sm_100a only", dev, major, minor);
+  if (num_sms) cudaDeviceGetAttribute(num_sms, cudaDevAttrMultiProcessorCount, dev);
+  return HK_OK;
+}
+
+// cudaFuncSetAttribute(max dynamic smem) once per (kernel, device).
+hk_status ensure_smem_impl(const void* fn, uint32_t bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({fn, dev})) return HK_OK;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return fail(HK_ERR_DEVICE, "cudaFuncSetAttribute(max dynamic smem = %u) failed", bytes);
+  done.insert({fn, dev});
+  return HK_OK;
+}
+template <typename F>
+hk_status ensure_smem(F* fn, uint32_t bytes) {
+  return ensure_smem_impl(reinterpret_cast<const void*>(fn), bytes);
+}
+
+hk_status launched(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(HK_ERR_LAUNCH, "%s launch failed: %s", what, cudaGetErrorString(e));
+  return HK_OK;
+}
+
+hk_status validate_common(int B, int Hq, int Hkv, int N, int d) {
+  if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0)
+    return fail(HK_ERR_INVALID_ARGUMENT, "B, Hq, Hkv, N must be positive (got %d, %d, %d, %d)", B, Hq, Hkv, N);
+  if (Hq % Hkv != 0) return fail(HK_ERR_INVALID_ARGUMENT, "Hq (%d) must be a multiple of Hkv (%d)", Hq, Hkv);
+  if (d != 64 && d != 128) return fail(HK_ERR_UNSUPPORTED, "head dim d=%d unsupported (need 64 or 128)", d);
+  if (N % 128 != 0) return fail(HK_ERR_UNSUPPORTED, "N=%d must be a multiple of 128", N);
+  if (Hq > 65535 || B > 65535) return fail(HK_ERR_UNSUPPORTED, "Hq and B must be <= 65535");
+  return HK_OK;
+}
+
+template <int D, bool CAUSAL>
+hk_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const hk::FwdParams& p,
+                     cudaStream_t stream) {
+  using C = hk::FwdCfg<D>;
+  auto* fn = hk::fwd_kernel<D, CAUSAL>;
+  hk_status s = ensure_smem(fn, C::SMEM);
+  if (s != HK_OK) return s;
+  dim3 grid(p.num_pairs, p.Hq, p.B);
+  fn<<<grid, C::THREADS, C::SMEM, stream>>>(mq, mk, mv, p);
+  return launched("hk_attn_fwd");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hk_attn_last_error(void) { return g_err; }
+
+const char* hk_status_string(hk_status s) {
+  switch (s) {
+    case HK_OK: return "HK_OK";
+    case HK_ERR_INVALID_ARGUMENT: return "HK_ERR_INVALID_ARGUMENT";
+    case HK_ERR_UNSUPPORTED: return "HK_ERR_UNSUPPORTED";
+    case HK_ERR_DEVICE: return "HK_ERR_DEVICE";
+    case HK_ERR_LAUNCH: return "HK_ERR_LAUNCH";
+  }
+  return "HK_ERR_UNKNOWN";
+}
+
+int hk_attn_abi_version(void) { return 1; }
+
+hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, float* LSE, int B, int Hq, int Hkv,
+                      int N, int d, int causal, cudaStream_t stream) {
+  g_err[0] = 0;
+  hk_status s = validate_common(B, Hq, Hkv, N, d);
+  if (s != HK_OK) return s;
+  if (!Q || !K || !V || !O || !LSE) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(LSE))
+    return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  const size_t q_bytes = (size_t)B * N * Hq * d * 2, kv_bytes = (size_t)B * N * Hkv * d * 2;
+  const size_t lse_bytes = (size_t)B * Hq * N * 4;
+  if (overlaps(O, q_bytes, Q, q_bytes) || overlaps(O, q_bytes, K, kv_bytes) || overlaps(O, q_bytes, V, kv_bytes) ||
+      overlaps(LSE, lse_bytes, O, q_bytes) || overlaps(LSE, lse_bytes, Q, q_bytes) ||
+      overlaps(LSE, lse_bytes, K, kv_bytes) || overlaps(LSE, lse_bytes, V, kv_bytes))
+    return fail(HK_ERR_INVALID_ARGUMENT, "outputs O/LSE must not alias inputs or each other");
+  s = check_device(nullptr);
+  if (s != HK_OK) return s;
+
+  CUtensorMap mq, mk, mv;
+  if (!hk::encode_bnhd(&mq, Q, B, N, Hq, d, 128) || !hk::encode_bnhd(&mk, K, B, N, Hkv, d, 128) ||
+      !hk::encode_bnhd(&mv, V, B, N, Hkv, d, 128))
+    return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed");
+  hk::FwdParams p;
+  p.lse = LSE;
+  p.o = reinterpret_cast<__nv_bfloat16*>(O);
+  p.B = B;
+  p.Hq = Hq;
+  p.Hkv = Hkv;
+  p.N = N;
+  p.num_pairs = (N / 128 + 1) / 2;
+  if (d == 64) return causal ? launch_fwd<64, true>(mq, mk, mv, p, stream) : launch_fwd<64, false>(mq, mk, mv, p, stream);
+  return causal ? launch_fwd<128, true>(mq, mk, mv, p, stream) : launch_fwd<128, false>(mq, mk, mv, p, stream);
+}
+
+size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d) {
+  (void)Hkv;
+  (void)d;
+  if (B <= 0 || Hq <= 0 || N <= 0) return 0;
+  return (size_t)2 * B * Hq * N * sizeof(float);
+}
+
+hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,
+                      void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes, int B, int Hq, int Hkv,
+                      int N, int d, int causal, cudaStream_t stream) {
+  g_err[0] = 0;
+  hk_status s = validate_common(B, Hq, Hkv, N, d);
+  if (s != HK_OK) return s;
+  if (!Q || !K || !V || !O || !LSE || !dO || !dQ || !dK || !dV || !workspace)
+    return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  const void* ptrs[] = {Q, K, V, O, LSE, dO, dQ, dK, dV, workspace};
+  for (const void* ptr : ptrs)
+    if (!aligned16(ptr)) return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  if (workspace_bytes < hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d))
+    return fail(HK_ERR_INVALID_ARGUMENT, "workspace too small: %zu < %zu bytes", workspace_bytes,
+                hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d));
+  const size_t q_bytes = (size_t)B * N * Hq * d * 2, kv_bytes = (size_t)B * N * Hkv * d * 2;
+  const size_t lse_bytes = (size_t)B * Hq * N * 4;
+  const void* ins[] = {Q, K, V, O, LSE, dO};
+  const size_t in_sz[] = {q_bytes, kv_bytes, kv_bytes, q_bytes, lse_bytes, q_bytes};
+  void* outs[] = {dQ, dK, dV, workspace};
+  const size_t out_sz[] = {q_bytes, kv_bytes, kv_bytes, workspace_bytes};
+  for (int i = 0; i < 4; ++i) {
+    for (int k = 0; k < 6; ++k)
+      if (overlaps(outs[i], out_sz[i], ins[k], in_sz[k]))
+        return fail(HK_ERR_INVALID_ARGUMENT, "outputs/workspace must not alias inputs");
+    for (int k = i + 1; k < 4; ++k)
+      if (overlaps(outs[i], out_sz[i], outs[k], out_sz[k]))
+        return fail(HK_ERR_INVALID_ARGUMENT, "outputs/workspace must not alias each other");
+  }
+  s = check_device(nullptr);
+  if (s != HK_OK) return s;
+  return hk::launch_bwd(Q, K, V, O, LSE, dO, dQ, dK, dV, reinterpret_cast<float*>(workspace), B, Hq, Hkv, N, d,
+                        causal != 0, stream, g_err, sizeof(g_err));
+}
+
+hk_status hk_diag_umma(const void* A, const void* Bm, float* D, int N, int K, int a_tmem, int b_mn,
+                       cudaStream_t stream) {
+  g_err[0] = 0;
+  if (!A || !Bm || !D) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if ((N != 64 && N != 128) || (K != 64 && K != 128)) return fail(HK_ERR_UNSUPPORTED, "N, K must be 64 or 128");
+  hk_status s = check_device(nullptr);
+  if (s != HK_OK) return s;
+  CUtensorMap ma, mb;
+  // A: [128][K] as (d=K, H=1, N=128, B=1); B: [N][K] (K-major) or [K][N] (MN-major).
+  bool ok = hk::encode_bnhd(&ma, A, 1, 128, 1, K, 128);
+  ok = ok && (b_mn ? hk::encode_bnhd(&mb, Bm, 1, K, 1, N, K) : hk::encode_bnhd(&mb, Bm, 1, N, 1, K, N));
+  if (!ok) return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed");
+  const uint32_t smem = 128 * K * 2 + N * K * 2 + 1024;
+  auto* A16 = reinterpret_cast<const __nv_bfloat16*>(A);
+#define HK_DIAG(NN, KK, AT, BMN)                                                   \
+  if (N == NN && K == KK && (a_tmem != 0) == AT && (b_mn != 0) == BMN) {           \
+    auto* fn = hk::umma_diag_kernel<NN, KK, AT, BMN>;                              \
+    if ((s = ensure_smem(fn, smem)) != HK_OK) return s;                            \
+    fn<<<1, 128, smem, stream>>>(ma, mb, A16, D);                                  \
+    return launched("hk_diag_umma");                                               \
+  }
+  HK_DIAG(64, 64, false, false) HK_DIAG(64, 64, false, true) HK_DIAG(64, 64, true, false) HK_DIAG(64, 64, true, true)
+  HK_DIAG(64, 128, false, false) HK_DIAG(64, 128, false, true) HK_DIAG(64, 128, true, false)
+  HK_DIAG(64, 128, true, true) HK_DIAG(128, 64, false, false) HK_DIAG(128, 64, false, true)
+  HK_DIAG(128, 64, true, false) HK_DIAG(128, 64, true, true) HK_DIAG(128, 128, false, false)
+  HK_DIAG(128, 128, false, true) HK_DIAG(128, 128, true, false) HK_DIAG(128, 128, true, true)
+#undef HK_DIAG
+  return fail(HK_ERR_UNSUPPORTED, "unsupported diag configuration");
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+"""CPU-side checks of the C ABI boundary: the library loads and exports every
+symbol declared in include/*.h; the Python binding has a signature for each;
+host-only validation paths return the documented statuses."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_2511_08083_b200", "libhkattn.so")
+
+
+def declared_symbols():
+    names = set()
+    inc = os.path.join(ROOT, "include")
+    for f in os.listdir(inc):
+        if f.endswith(".h"):
+            src = open(os.path.join(inc, f)).read()
+            src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+            names |= set(re.findall(r"\b(hk_\w+)\s*\(", src))
+    return names
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2511_08083_b200 import build
+    build.build()
+    return ctypes.CDLL(LIB)
+
+
+def test_exports_every_declared_symbol(lib):
+    names = declared_symbols()
+    assert {"hk_attn_fwd", "hk_attn_bwd", "hk_attn_bwd_workspace_bytes", "hk_attn_last_error"} <= names
+    for n in names:
+        assert hasattr(lib, n), f"{n} not exported"
+
+
+def test_binding_covers_header():
+    from paper_2511_08083_b200._lib import SIGNATURES
+    assert declared_symbols() == set(SIGNATURES)
+
+
+def test_host_only_validation(lib):
+    """Host-only paths (no GPU touched): version, status strings, workspace
+    size, and argument validation that fails before any CUDA call."""
+    from paper_2511_08083_b200 import _lib
+    L = _lib.lib()
+    assert L.hk_attn_abi_version() == 1
+    assert L.hk_status_string(2) == b"HK_ERR_UNSUPPORTED"
+    assert L.hk_attn_bwd_workspace_bytes(2, 4, 2, 256, 64) == 2 * 2 * 4 * 256 * 4
+    p = ctypes.c_void_p(16)
+    assert L.hk_attn_fwd(p, p, p, p, p, 1, 2, 2, 128, 96, 0, None) == 2   # d = 96
+    assert L.hk_attn_fwd(p, p, p, p, p, 1, 2, 2, 100, 64, 0, None) == 2   # N % 128
+    assert L.hk_attn_fwd(p, p, p, p, p, 1, 3, 2, 128, 64, 0, None) == 1   # Hq % Hkv
+    assert b"multiple" in L.hk_attn_last_error()
+    assert L.hk_attn_fwd(p, p, p, p, p, 0, 2, 2, 128, 64, 0, None) == 1   # B = 0
+    assert L.hk_attn_fwd(None, p, p, p, p, 1, 2, 2, 128, 64, 0, None) == 1
+    assert L.hk_attn_fwd(ctypes.c_void_p(8), p, p, p, p, 1, 2, 2, 128, 64, 0, None) == 1
+    # outputs aliasing inputs
+    assert L.hk_attn_fwd(p, p, p, p, p, 1, 2, 2, 128, 64, 0, None) == 1
+    assert b"alias" in L.hk_attn_last_error()
+    # bwd: workspace too small
+    a = [ctypes.c_void_p(16 * (i + 1) << 30) for i in range(10)]
+    assert L.hk_attn_bwd(*a, 0, 1, 2, 2, 128, 64, 0, None) == 1
+    assert b"workspace" in L.hk_attn_last_error()
