@@ -1,14 +1,529 @@
-// Backward kernels (placeholder until the dK/dV and dQ passes land).
+// Backward fused attention for sm_100a: three stream-ordered kernels.
+//
+// The paper gives no backward algorithm (PAPER.md: "notoriously
+// register heavy", multiple MFMA shapes, row+col loads of one shared tile);
+// BASELINE.json prescribes the structure implemented here:
+//   B0  bwd_pre_kernel   D = rowsum(dO * O) and LSE2 = LSE * log2(e)   (HBM-bound)
+//   B1  bwd_dkdv_kernel  per (key tile j, kvh, b): loop h in the GQA group and
+//       query blocks i; S^T = K_j Q_i^T, dP^T = V_j dO_i^T (tcgen05, TMEM),
+//       P^T = exp2(c S^T - LSE2_i), dS^T = P^T (dP^T - D_i) in registers,
+//       dV += P^T dO_i, dK += dS^T Q_i with bf16 P^T / dS^T read from TMEM.
+//       The GQA group reduction is this in-kernel h-loop (no atomics).
+//   B2  bwd_dq_kernel    per (query tile i, h, b): loop key blocks j;
+//       S = Q_i K_j^T, dP = dO_i V_j^T, dS = P (dP - D_i), dQ += dS K_j.
+// Both B1 and B2 double-buffer the score/dP accumulators in TMEM so the
+// elementwise work of block i overlaps the tensor-core work of block i+1.
 #pragma once
 #include <cstddef>
 #include <cstdio>
+
 #include "../../include/hk_attn.h"
+#include "ptx.cuh"
+#include "tma_host.h"
 
 namespace hk {
-inline hk_status launch_bwd(const void*, const void*, const void*, const void*, const float*, const void*, void*,
-                            void*, void*, float*, int, int, int, int, int, bool, cudaStream_t, char* err,
-                            size_t errlen) {
-  snprintf(err, errlen, "hk_attn_bwd not built yet");
-  return HK_ERR_UNSUPPORTED;
+
+// ---------------------------------------------------------------- B0
+// One group of d/8 lanes per (b, n, h) row (16-B loads), rows in memory order.
+template <int D>
+__global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ O,
+                                                      const __nv_bfloat16* __restrict__ dO,
+                                                      const float* __restrict__ lse, float* __restrict__ Dout,
+                                                      float* __restrict__ lse2, int B, int N, int H) {
+  constexpr int LPR = D / 8;  // lanes per row
+  constexpr int RPW = 32 / LPR;
+  const size_t rows = (size_t)B * N * H;
+  const int sub = threadIdx.x % LPR;
+  const size_t gwarp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const size_t nwarps = (size_t)gridDim.x * blockDim.x / 32;
+  const int lrow = (threadIdx.x % 32) / LPR;
+  for (size_t base = gwarp * RPW; base < rows; base += nwarps * RPW) {
+    const size_t row = base + lrow;
+    float acc = 0.f;
+    if (row < rows) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(O + row * D) + sub);
+      const uint4 g = __ldg(reinterpret_cast<const uint4*>(dO + row * D) + sub);
+      const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&g);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 x = __bfloat1622float2(ap[k]), y = __bfloat1622float2(gp[k]);
+        acc = fmaf(x.x, y.x, acc);
+        acc = fmaf(x.y, y.y, acc);
+      }
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (row < rows && sub == 0) {
+      const size_t h = row % H, n = (row / H) % N, b = row / ((size_t)H * N);
+      const size_t idx = (b * H + h) * N + n;
+      Dout[idx] = acc;
+      lse2[idx] = lse[idx] * 1.4426950408889634f;
+    }
+  }
 }
+
+struct BwdParams {
+  const float* Dv;    // [B][Hq][N]
+  const float* lse2;  // [B][Hq][N]
+  __nv_bfloat16* dq;  // [B][N][Hq][D]
+  __nv_bfloat16* dk;  // [B][N][Hkv][D]
+  __nv_bfloat16* dv;  // [B][N][Hkv][D]
+  int B, Hq, Hkv, N;
+};
+
+template <int D>
+struct BwdCfg {
+  static constexpr int PANELS = D / 64;
+  static constexpr uint32_t T128 = 128 * D * 2;  // a 128-row tile
+  static constexpr uint32_t T64 = 64 * D * 2;    // a 64-row block
+  static constexpr int NS = 4;                   // ring depth (64-row blocks)
+  // B1: K_j, V_j (128 rows each) + NS x {Q_i, dO_i (64 rows), lse2, D (64 fp32)}
+  static constexpr uint32_t STAGE1 = 2 * T64 + 512;
+  static constexpr uint32_t SMEM1 = 2 * T128 + NS * STAGE1 + 1024;
+  // B2: Q_i, dO_i (128 rows) + NS x {K_j, V_j (64 rows)}
+  static constexpr uint32_t STAGE2 = 2 * T64;
+  static constexpr uint32_t SMEM2 = 2 * T128 + NS * STAGE2 + 1024;
+  static constexpr int THREADS = 320;  // 8 compute warps + TMA warp + MMA warp
+};
+
+// SMEM descriptor helpers for [rows][D] bf16 tiles stored as D/64 panels of rows x 128 B.
+// K-major use (rows are M or N, D is the contraction): k-step kk of 16 elements.
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int rows, int kk) {
+  return sdesc_sw128(base + (kk / 4) * rows * 128 + (kk % 4) * 32, 16, 1024);
+}
+// MN-major use (rows are the contraction, D is N): k-step kk of 16 rows.
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int rows, int kk) {
+  return sdesc_sw128(base + kk * 16 * 128, rows * 128, 1024);
+}
+
+// ---------------------------------------------------------------- B1: dK, dV
+// TMEM: dV [0,D)  dK [D,2D)  buffer b: S^T [2D+128b, +64)  dP^T [2D+128b+64, +64)
+template <int D, bool CAUSAL>
+__global__ void __launch_bounds__(320, 1)
+    bwd_dkdv_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapdO,
+                    const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
+                    const BwdParams p) {
+  using C = BwdCfg<D>;
+  constexpr int NS = C::NS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + C::T128;
+  uint8_t* sStage = smem + 2 * C::T128;  // stage s: Q [T64] dO [T64] lse2 [256 B] D [256 B]
+
+  __shared__ uint64_t bar_kv, bar_full[NS], bar_empty[NS], bar_sp[2], bar_ds[2], bar_acc;
+  __shared__ uint32_t tmem_base_s;
+
+  const int warp = warp_id(), lane = lane_id();
+  const int T = p.N / 128;
+  const int jt = CAUSAL ? (T - 1 - (int)blockIdx.x) : (int)blockIdx.x;  // key tile (heaviest first)
+  const int kvh = blockIdx.y, b = blockIdx.z;
+  const int G = p.Hq / p.Hkv;
+  const int nq = p.N / 64;               // 64-row query blocks
+  const int i0 = CAUSAL ? 2 * jt : 0;    // first query block that sees key tile jt
+  const int per_h = nq - i0;
+  const int n_it = G * per_h;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_kv, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar_sp[s], 1);
+      mbar_init(&bar_ds[s], 8);
+    }
+    mbar_init(&bar_acc, 1);
+    fence_barrier_init();
+  }
+  if (warp == 8) {
+    tma_prefetch(&mapQ);
+    tma_prefetch(&mapdO);
+    tma_prefetch(&mapK);
+    tma_prefetch(&mapV);
+  }
+  if (warp == 9) tmem_alloc<512>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tmem_base_s;
+  const uint32_t tdV = tb, tdK = tb + D;
+  auto tS = [&](int s) { return tb + 2 * D + 128 * s; };
+  auto tP = [&](int s) { return tb + 2 * D + 128 * s + 64; };
+
+  if (warp == 8) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      const uint64_t pol_keep = policy_evict_last();
+      const uint64_t pol_stream = policy_evict_normal();
+      mbar_arrive_expect_tx(&bar_kv, 2 * C::T128);
+      for (int pn = 0; pn < C::PANELS; ++pn) {
+        tma_load_4d(&mapK, &bar_kv, sK + pn * 128 * 128, pn * 64, kvh, jt * 128, b, pol_stream);
+        tma_load_4d(&mapV, &bar_kv, sV + pn * 128 * 128, pn * 64, kvh, jt * 128, b, pol_stream);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it % NS;
+        const uint32_t ph = (it / NS) & 1;
+        const int h = kvh * G + it / per_h;
+        const int qi = i0 + it % per_h;
+        uint8_t* st = sStage + s * C::STAGE1;
+        mbar_wait(&bar_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&bar_full[s], 2 * C::T64 + 512);
+        for (int pn = 0; pn < C::PANELS; ++pn) {
+          tma_load_4d(&mapQ, &bar_full[s], st + pn * 64 * 128, pn * 64, h, qi * 64, b, pol_keep);
+          tma_load_4d(&mapdO, &bar_full[s], st + C::T64 + pn * 64 * 128, pn * 64, h, qi * 64, b, pol_keep);
+        }
+        const size_t off = ((size_t)b * p.Hq + h) * p.N + (size_t)qi * 64;
+        bulk_load(st + 2 * C::T64, p.lse2 + off, 256, &bar_full[s]);
+        bulk_load(st + 2 * C::T64 + 256, p.Dv + off, 256, &bar_full[s]);
+      }
+    }
+  } else if (warp == 9) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      constexpr uint32_t idesc_sp = idesc_bf16(128, 64, 0, 0);  // S^T / dP^T: M=128 keys, N=64 queries
+      constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);  // dV / dK: B = dO_i / Q_i MN-major
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+      auto issue_sp = [&](int it) {
+        const int s = it % NS, bi = it & 1;
+        const uint32_t q = smem_u32(sStage + s * C::STAGE1), dO = q + C::T64;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_ss(tS(bi), desc_kmajor(aK, 128, kk), desc_kmajor(q, 64, kk), idesc_sp, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_ss(tP(bi), desc_kmajor(aV, 128, kk), desc_kmajor(dO, 64, kk), idesc_sp, kk > 0);
+        tc_commit(&bar_sp[bi]);
+      };
+      mbar_wait(&bar_kv, 0);
+      if (n_it > 0) {
+        mbar_wait(&bar_full[0], 0);
+        tc_fence_after();
+        issue_sp(0);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it % NS, bi = it & 1;
+        if (it + 1 < n_it) {
+          const int s1 = (it + 1) % NS;
+          mbar_wait(&bar_full[s1], ((it + 1) / NS) & 1);
+          tc_fence_after();
+          issue_sp(it + 1);
+        }
+        mbar_wait(&bar_ds[bi], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t q = smem_u32(sStage + s * C::STAGE1), dO = q + C::T64;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_ts(tdV, tS(bi) + kk * 8, desc_mnmajor(dO, 64, kk), idesc_acc, (it > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_ts(tdK, tP(bi) + kk * 8, desc_mnmajor(q, 64, kk), idesc_acc, (it > 0 || kk > 0) ? 1u : 0u);
+        if (it + NS < n_it) tc_commit(&bar_empty[s]);
+      }
+      tc_commit(&bar_acc);
+    }
+  } else {
+    // ================= elementwise warpgroups (warps 0-7) =================
+    const int wg = warp >> 2;                 // query columns [32 wg, 32 wg + 32) of each block
+    const uint32_t lb = (warp & 3) * 32;      // TMEM lane base
+    const int r = (warp & 3) * 32 + lane;     // key row within the tile
+    const int key = jt * 128 + r;
+    const float c = 1.4426950408889634f / sqrtf((float)D);
+    for (int it = 0; it < n_it; ++it) {
+      const int s = it % NS, bi = it & 1;
+      const int qi = i0 + it % per_h;
+      const float* lse2 = reinterpret_cast<const float*>(sStage + s * C::STAGE1 + 2 * C::T64) + 32 * wg;
+      const float* Dv = lse2 + 64;
+      mbar_wait(&bar_sp[bi], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[32], dr[32];
+      tmem_ld32(tmem_addr(tS(bi), lb, 32 * wg), sr);
+      tmem_ld32(tmem_addr(tP(bi), lb, 32 * wg), dr);
+      tmem_wait_ld();
+      uint32_t pk[16], dk[16];
+      const int q0 = qi * 64 + 32 * wg;  // first query of this thread's columns
+#pragma unroll
+      for (int cc = 0; cc < 32; cc += 2) {
+        float pp[2], dd[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          float pv = ex2(fmaf(__uint_as_float(sr[cc + u]), c, -lse2[cc + u]));
+          if (CAUSAL && q0 + cc + u < key) pv = 0.f;  // query < key is masked
+          pp[u] = pv;
+          dd[u] = pv * (__uint_as_float(dr[cc + u]) - Dv[cc + u]);
+        }
+        pk[cc / 2] = pack_bf16(pp[0], pp[1]);
+        dk[cc / 2] = pack_bf16(dd[0], dd[1]);
+      }
+      tmem_st16(tmem_addr(tS(bi), lb, 16 * wg), pk);
+      tmem_st16(tmem_addr(tP(bi), lb, 16 * wg), dk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_ds[bi]);
+    }
+    // ---- epilogue: WG0 writes dV, WG1 writes dK * (1/sqrt d)
+    mbar_wait(&bar_acc, 0);
+    tc_fence_after();
+    const float scale = wg == 0 ? 1.f : rsqrtf((float)D);
+    const uint32_t tacc = wg == 0 ? tdV : tdK;
+    __nv_bfloat16* out = (wg == 0 ? p.dv : p.dk) + (((size_t)b * p.N + key) * p.Hkv + kvh) * D;
+#pragma unroll
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(tmem_addr(tacc, lb, c0), v);
+      tmem_wait_ld();
+      uint4 o4[4];
+      uint32_t* op = reinterpret_cast<uint32_t*>(o4);
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        op[k] = pack_bf16(__uint_as_float(v[2 * k]) * scale, __uint_as_float(v[2 * k + 1]) * scale);
+      uint4* dst = reinterpret_cast<uint4*>(out + c0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dst[k] = o4[k];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc<512>(tb);
+}
+
+// ---------------------------------------------------------------- B2: dQ
+// TMEM: dQ [0,D)  buffer b: S [D+128b, +64)  dP [D+128b+64, +64)
+template <int D, bool CAUSAL>
+__global__ void __launch_bounds__(320, 1)
+    bwd_dq_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapdO,
+                  const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
+                  const BwdParams p) {
+  using C = BwdCfg<D>;
+  constexpr int NS = C::NS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sdO = smem + C::T128;
+  uint8_t* sStage = smem + 2 * C::T128;  // stage s: K_j [T64] V_j [T64]
+
+  __shared__ uint64_t bar_q, bar_full[NS], bar_empty[NS], bar_sp[2], bar_ds[2], bar_acc;
+  __shared__ uint32_t tmem_base_s;
+
+  const int warp = warp_id(), lane = lane_id();
+  const int T = p.N / 128;
+  const int it_q = CAUSAL ? (T - 1 - (int)blockIdx.x) : (int)blockIdx.x;  // query tile (heaviest first)
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int kvh = h / (p.Hq / p.Hkv);
+  const int n_it = CAUSAL ? 2 * it_q + 2 : p.N / 64;  // 64-key blocks
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_q, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar_sp[s], 1);
+      mbar_init(&bar_ds[s], 8);
+    }
+    mbar_init(&bar_acc, 1);
+    fence_barrier_init();
+  }
+  if (warp == 8) {
+    tma_prefetch(&mapQ);
+    tma_prefetch(&mapdO);
+    tma_prefetch(&mapK);
+    tma_prefetch(&mapV);
+  }
+  if (warp == 9) tmem_alloc<512>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tmem_base_s;
+  const uint32_t tdQ = tb;
+  auto tS = [&](int s) { return tb + D + 128 * s; };
+  auto tP = [&](int s) { return tb + D + 128 * s + 64; };
+
+  if (warp == 8) {
+    if (lane == 0) {
+      const uint64_t pol_keep = policy_evict_last();
+      const uint64_t pol_stream = policy_evict_normal();
+      mbar_arrive_expect_tx(&bar_q, 2 * C::T128);
+      for (int pn = 0; pn < C::PANELS; ++pn) {
+        tma_load_4d(&mapQ, &bar_q, sQ + pn * 128 * 128, pn * 64, h, it_q * 128, b, pol_stream);
+        tma_load_4d(&mapdO, &bar_q, sdO + pn * 128 * 128, pn * 64, h, it_q * 128, b, pol_stream);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it % NS;
+        const uint32_t ph = (it / NS) & 1;
+        uint8_t* st = sStage + s * C::STAGE2;
+        mbar_wait(&bar_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&bar_full[s], 2 * C::T64);
+        for (int pn = 0; pn < C::PANELS; ++pn) {
+          tma_load_4d(&mapK, &bar_full[s], st + pn * 64 * 128, pn * 64, kvh, it * 64, b, pol_keep);
+          tma_load_4d(&mapV, &bar_full[s], st + C::T64 + pn * 64 * 128, pn * 64, kvh, it * 64, b, pol_keep);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_sp = idesc_bf16(128, 64, 0, 0);  // S / dP: M=128 queries, N=64 keys
+      constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);  // dQ += dS K_j: K_j MN-major
+      const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO);
+      auto issue_sp = [&](int it) {
+        const int s = it % NS, bi = it & 1;
+        const uint32_t k = smem_u32(sStage + s * C::STAGE2), v = k + C::T64;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_ss(tS(bi), desc_kmajor(aQ, 128, kk), desc_kmajor(k, 64, kk), idesc_sp, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_ss(tP(bi), desc_kmajor(adO, 128, kk), desc_kmajor(v, 64, kk), idesc_sp, kk > 0);
+        tc_commit(&bar_sp[bi]);
+      };
+      mbar_wait(&bar_q, 0);
+      mbar_wait(&bar_full[0], 0);
+      tc_fence_after();
+      issue_sp(0);
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it % NS, bi = it & 1;
+        if (it + 1 < n_it) {
+          const int s1 = (it + 1) % NS;
+          mbar_wait(&bar_full[s1], ((it + 1) / NS) & 1);
+          tc_fence_after();
+          issue_sp(it + 1);
+        }
+        mbar_wait(&bar_ds[bi], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t k = smem_u32(sStage + s * C::STAGE2);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_ts(tdQ, tP(bi) + kk * 8, desc_mnmajor(k, 64, kk), idesc_acc, (it > 0 || kk > 0) ? 1u : 0u);
+        if (it + NS < n_it) tc_commit(&bar_empty[s]);
+      }
+      tc_commit(&bar_acc);
+    }
+  } else {
+    const int wg = warp >> 2;              // key columns [32 wg, 32 wg + 32) of each block
+    const uint32_t lb = (warp & 3) * 32;
+    const int r = (warp & 3) * 32 + lane;  // query row within the tile
+    const int q = it_q * 128 + r;
+    const float c = 1.4426950408889634f / sqrtf((float)D);
+    const size_t vrow = ((size_t)b * p.Hq + h) * p.N + q;
+    const float l2 = p.lse2[vrow], Dq = p.Dv[vrow];
+    for (int it = 0; it < n_it; ++it) {
+      const int bi = it & 1;
+      mbar_wait(&bar_sp[bi], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[32], dr[32];
+      tmem_ld32(tmem_addr(tS(bi), lb, 32 * wg), sr);
+      tmem_ld32(tmem_addr(tP(bi), lb, 32 * wg), dr);
+      tmem_wait_ld();
+      const int k0 = it * 64 + 32 * wg;
+      uint32_t dk[16];
+#pragma unroll
+      for (int cc = 0; cc < 32; cc += 2) {
+        float dd[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          float pv = ex2(fmaf(__uint_as_float(sr[cc + u]), c, -l2));
+          if (CAUSAL && k0 + cc + u > q) pv = 0.f;
+          dd[u] = pv * (__uint_as_float(dr[cc + u]) - Dq);
+        }
+        dk[cc / 2] = pack_bf16(dd[0], dd[1]);
+      }
+      tmem_st16(tmem_addr(tP(bi), lb, 16 * wg), dk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_ds[bi]);
+    }
+    // ---- epilogue: dQ * (1/sqrt d); WG0 writes columns [0, D/2), WG1 [D/2, D)
+    mbar_wait(&bar_acc, 0);
+    tc_fence_after();
+    const float scale = rsqrtf((float)D);
+    __nv_bfloat16* out = p.dq + (((size_t)b * p.N + q) * p.Hq + h) * D;
+#pragma unroll
+    for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(tmem_addr(tdQ, lb, c0), v);
+      tmem_wait_ld();
+      uint4 o4[4];
+      uint32_t* op = reinterpret_cast<uint32_t*>(o4);
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        op[k] = pack_bf16(__uint_as_float(v[2 * k]) * scale, __uint_as_float(v[2 * k + 1]) * scale);
+      uint4* dst = reinterpret_cast<uint4*>(out + c0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dst[k] = o4[k];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc<512>(tb);
+}
+
+// ---------------------------------------------------------------- host launch
+template <typename F>
+inline bool set_smem(F* fn, uint32_t bytes) {
+  return cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)bytes) == cudaSuccess;
+}
+
+template <int D, bool CAUSAL>
+hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,
+                       void* dQ, void* dK, void* dV, float* ws, int B, int Hq, int Hkv, int N, cudaStream_t stream,
+                       char* err, size_t errlen) {
+  using C = BwdCfg<D>;
+  float* Dv = ws;
+  float* lse2 = ws + (size_t)B * Hq * N;
+  CUtensorMap mQ64, mdO64, mK128, mV128, mQ128, mdO128, mK64, mV64;
+  bool ok = encode_bnhd(&mQ64, Q, B, N, Hq, D, 64) && encode_bnhd(&mdO64, dO, B, N, Hq, D, 64) &&
+            encode_bnhd(&mK128, K, B, N, Hkv, D, 128) && encode_bnhd(&mV128, V, B, N, Hkv, D, 128) &&
+            encode_bnhd(&mQ128, Q, B, N, Hq, D, 128) && encode_bnhd(&mdO128, dO, B, N, Hq, D, 128) &&
+            encode_bnhd(&mK64, K, B, N, Hkv, D, 64) && encode_bnhd(&mV64, V, B, N, Hkv, D, 64);
+  if (!ok) {
+    snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
+    return HK_ERR_DEVICE;
+  }
+  static bool attr_done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 64 || !attr_done[dev]) {
+    if (!set_smem(bwd_dkdv_kernel<D, CAUSAL>, C::SMEM1) || !set_smem(bwd_dq_kernel<D, CAUSAL>, C::SMEM2)) {
+      snprintf(err, errlen, "cudaFuncSetAttribute(max dynamic smem) failed");
+      return HK_ERR_DEVICE;
+    }
+    if (dev < 64) attr_done[dev] = true;
+  }
+  BwdParams p{Dv, lse2, reinterpret_cast<__nv_bfloat16*>(dQ), reinterpret_cast<__nv_bfloat16*>(dK),
+              reinterpret_cast<__nv_bfloat16*>(dV), B, Hq, Hkv, N};
+  // B0
+  const size_t rows = (size_t)B * N * Hq;
+  const size_t warps_needed = (rows + (32 / (D / 8)) - 1) / (32 / (D / 8));
+  size_t blocks = (warps_needed + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  bwd_pre_kernel<D><<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(O),
+                                                            reinterpret_cast<const __nv_bfloat16*>(dO), LSE, Dv, lse2,
+                                                            B, N, Hq);
+  // B1, B2
+  bwd_dkdv_kernel<D, CAUSAL><<<dim3(N / 128, Hkv, B), C::THREADS, C::SMEM1, stream>>>(mQ64, mdO64, mK128, mV128, p);
+  bwd_dq_kernel<D, CAUSAL><<<dim3(N / 128, Hq, B), C::THREADS, C::SMEM2, stream>>>(mQ128, mdO128, mK64, mV64, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(err, errlen, "hk_attn_bwd launch failed: %s", cudaGetErrorString(e));
+    return HK_ERR_LAUNCH;
+  }
+  return HK_OK;
+}
+
+inline hk_status launch_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                            const void* dO, void* dQ, void* dK, void* dV, float* ws, int B, int Hq, int Hkv, int N,
+                            int d, bool causal, cudaStream_t stream, char* err, size_t errlen) {
+  if (d == 64)
+    return causal ? launch_bwd_t<64, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen)
+                  : launch_bwd_t<64, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen);
+  return causal ? launch_bwd_t<128, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen)
+                : launch_bwd_t<128, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen);
+}
+
 }  // namespace hk

@@ -1,0 +1,61 @@
+"""Quick kernel timing probe (not the bench): CUDA-event timing of
+hk_attn_fwd / hk_attn_bwd on BASELINE-shaped configs."""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2511_08083_b200 import attn_bwd, attn_fwd  # noqa: E402
+from paper_2511_08083_b200.inputs import make_inputs  # noqa: E402
+
+CONFIGS = {
+    "C2-nc": (16, 4096, 16, 16, 128, False),
+    "C2-c": (16, 4096, 16, 16, 128, True),
+    "C3": (16, 8192, 32, 8, 128, True),
+    "C4-8192": (16, 8192, 32, 32, 64, True),
+    "C4-2048": (16, 2048, 32, 32, 64, True),
+    "C5-4096-nc": (16, 4096, 64, 8, 128, False),
+    "C5-4096-c": (16, 4096, 64, 8, 128, True),
+}
+
+
+def timeit(fn, iters, warm):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="C2-nc,C2-c,C3,C4-8192")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--bwd", action="store_true")
+    a = ap.parse_args()
+    for name in a.configs.split(","):
+        B, N, Hq, Hkv, d, causal = CONFIGS[name]
+        x = make_inputs(B, N, Hq, Hkv, d, seed=0, device="cuda")
+        flops = 4.0 * B * Hq * N * N * d * (0.5 if causal else 1.0)
+        o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
+        ms = timeit(lambda: attn_fwd(x["Q"], x["K"], x["V"], causal, out=o, lse=lse), a.iters, 3)
+        rec = {"config": name, "fwd_ms": round(ms, 4), "fwd_tflops": round(flops / ms / 1e9, 1)}
+        if a.bwd:
+            dq, dk, dv = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal)
+            ms_b = timeit(lambda: attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, dq=dq, dk=dk, dv=dv),
+                          a.iters, 3)
+            rec.update(bwd_ms=round(ms_b, 4), bwd_tflops=round(2.5 * flops / ms_b / 1e9, 1))
+        print(json.dumps(rec), flush=True)
+        del x
+
+
+if __name__ == "__main__":
+    main()
