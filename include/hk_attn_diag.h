@@ -10,6 +10,12 @@
  *   a_tmem != 0 stages A in tensor memory (the P*V / dS*K operand form),
  *   otherwise A is read from shared memory (K-major).
  * Supported: N in {64, 128}, K in {64, 128}. Same error conventions as hk_attn.h.
+ *
+ * hk_diag_bwd_phase: exactly the work of hk_attn_bwd (same arguments, same
+ * validation) but enqueues only one of its three kernels, so a profiler or
+ * bench can time each on the stream in isolation:
+ *   phase 0 = D-preprocess (writes the workspace), 1 = dK/dV pass, 2 = dQ pass.
+ * Phases 1 and 2 read the workspace written by phase 0.
  */
 #ifndef HK_ATTN_DIAG_H_
 #define HK_ATTN_DIAG_H_
@@ -19,6 +25,9 @@ extern "C" {
 #endif
 hk_status hk_diag_umma(const void* A, const void* B, float* D, int N, int K, int a_tmem, int b_mn,
                        cudaStream_t stream);
+hk_status hk_diag_bwd_phase(int phase, const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                            const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
+                            int B, int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream);
 #ifdef __cplusplus
 }
 #endif

@@ -24,6 +24,7 @@ SIGNATURES = {
     "hk_status_string": (ctypes.c_char_p, [_I]),
     "hk_attn_abi_version": (_I, []),
     "hk_diag_umma": (_I, [_P, _P, _P, _I, _I, _I, _I, _P]),
+    "hk_diag_bwd_phase": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _I, _I, _I, _I, _I, _I, _P]),
 }
 
 

@@ -472,7 +472,7 @@ inline bool set_smem(F* fn, uint32_t bytes) {
 template <int D, bool CAUSAL>
 hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,
                        void* dQ, void* dK, void* dV, float* ws, int B, int Hq, int Hkv, int N, cudaStream_t stream,
-                       char* err, size_t errlen) {
+                       char* err, size_t errlen, int phase) {
   using C = BwdCfg<D>;
   float* Dv = ws;
   float* lse2 = ws + (size_t)B * Hq * N;
@@ -502,12 +502,15 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   const size_t warps_needed = (rows + (32 / (D / 8)) - 1) / (32 / (D / 8));
   size_t blocks = (warps_needed + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  bwd_pre_kernel<D><<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(O),
-                                                            reinterpret_cast<const __nv_bfloat16*>(dO), LSE, Dv, lse2,
-                                                            B, N, Hq);
+  if (phase < 0 || phase == 0)
+    bwd_pre_kernel<D><<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(O),
+                                                              reinterpret_cast<const __nv_bfloat16*>(dO), LSE, Dv,
+                                                              lse2, B, N, Hq);
   // B1, B2
-  bwd_dkdv_kernel<D, CAUSAL><<<dim3(N / 128, Hkv, B), C::THREADS, C::SMEM1, stream>>>(mQ64, mdO64, mK128, mV128, p);
-  bwd_dq_kernel<D, CAUSAL><<<dim3(N / 128, Hq, B), C::THREADS, C::SMEM2, stream>>>(mQ128, mdO128, mK64, mV64, p);
+  if (phase < 0 || phase == 1)
+    bwd_dkdv_kernel<D, CAUSAL><<<dim3(N / 128, Hkv, B), C::THREADS, C::SMEM1, stream>>>(mQ64, mdO64, mK128, mV128, p);
+  if (phase < 0 || phase == 2)
+    bwd_dq_kernel<D, CAUSAL><<<dim3(N / 128, Hq, B), C::THREADS, C::SMEM2, stream>>>(mQ128, mdO128, mK64, mV64, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(err, errlen, "hk_attn_bwd launch failed: %s", cudaGetErrorString(e));
@@ -518,12 +521,12 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
 
 inline hk_status launch_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                             const void* dO, void* dQ, void* dK, void* dV, float* ws, int B, int Hq, int Hkv, int N,
-                            int d, bool causal, cudaStream_t stream, char* err, size_t errlen) {
+                            int d, bool causal, cudaStream_t stream, char* err, size_t errlen, int phase) {
   if (d == 64)
-    return causal ? launch_bwd_t<64, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen)
-                  : launch_bwd_t<64, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen);
-  return causal ? launch_bwd_t<128, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen)
-                : launch_bwd_t<128, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen);
+    return causal ? launch_bwd_t<64, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase)
+                  : launch_bwd_t<64, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase);
+  return causal ? launch_bwd_t<128, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase)
+                : launch_bwd_t<128, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase);
 }
 
 }  // namespace hk

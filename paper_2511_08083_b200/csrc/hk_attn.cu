@@ -99,6 +99,40 @@ hk_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
 
 }  // namespace
 
+static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                          const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes, int B,
+                          int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream) {
+  g_err[0] = 0;
+  hk_status s = validate_common(B, Hq, Hkv, N, d);
+  if (s != HK_OK) return s;
+  if (!Q || !K || !V || !O || !LSE || !dO || !dQ || !dK || !dV || !workspace)
+    return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  const void* ptrs[] = {Q, K, V, O, LSE, dO, dQ, dK, dV, workspace};
+  for (const void* ptr : ptrs)
+    if (!aligned16(ptr)) return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  if (workspace_bytes < hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d))
+    return fail(HK_ERR_INVALID_ARGUMENT, "workspace too small: %zu < %zu bytes", workspace_bytes,
+                hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d));
+  const size_t q_bytes = (size_t)B * N * Hq * d * 2, kv_bytes = (size_t)B * N * Hkv * d * 2;
+  const size_t lse_bytes = (size_t)B * Hq * N * 4;
+  const void* ins[] = {Q, K, V, O, LSE, dO};
+  const size_t in_sz[] = {q_bytes, kv_bytes, kv_bytes, q_bytes, lse_bytes, q_bytes};
+  void* outs[] = {dQ, dK, dV, workspace};
+  const size_t out_sz[] = {q_bytes, kv_bytes, kv_bytes, workspace_bytes};
+  for (int i = 0; i < 4; ++i) {
+    for (int k = 0; k < 6; ++k)
+      if (overlaps(outs[i], out_sz[i], ins[k], in_sz[k]))
+        return fail(HK_ERR_INVALID_ARGUMENT, "outputs/workspace must not alias inputs");
+    for (int k = i + 1; k < 4; ++k)
+      if (overlaps(outs[i], out_sz[i], outs[k], out_sz[k]))
+        return fail(HK_ERR_INVALID_ARGUMENT, "outputs/workspace must not alias each other");
+  }
+  s = check_device(nullptr);
+  if (s != HK_OK) return s;
+  return hk::launch_bwd(Q, K, V, O, LSE, dO, dQ, dK, dV, reinterpret_cast<float*>(workspace), B, Hq, Hkv, N, d,
+                        causal != 0, stream, g_err, sizeof(g_err), phase);
+}
+
 extern "C" {
 
 const char* hk_attn_last_error(void) { return g_err; }
@@ -159,35 +193,16 @@ size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d) {
 hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,
                       void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes, int B, int Hq, int Hkv,
                       int N, int d, int causal, cudaStream_t stream) {
+  return bwd_impl(-1, Q, K, V, O, LSE, dO, dQ, dK, dV, workspace, workspace_bytes, B, Hq, Hkv, N, d, causal, stream);
+}
+
+hk_status hk_diag_bwd_phase(int phase, const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                            const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
+                            int B, int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream) {
   g_err[0] = 0;
-  hk_status s = validate_common(B, Hq, Hkv, N, d);
-  if (s != HK_OK) return s;
-  if (!Q || !K || !V || !O || !LSE || !dO || !dQ || !dK || !dV || !workspace)
-    return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
-  const void* ptrs[] = {Q, K, V, O, LSE, dO, dQ, dK, dV, workspace};
-  for (const void* ptr : ptrs)
-    if (!aligned16(ptr)) return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
-  if (workspace_bytes < hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d))
-    return fail(HK_ERR_INVALID_ARGUMENT, "workspace too small: %zu < %zu bytes", workspace_bytes,
-                hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d));
-  const size_t q_bytes = (size_t)B * N * Hq * d * 2, kv_bytes = (size_t)B * N * Hkv * d * 2;
-  const size_t lse_bytes = (size_t)B * Hq * N * 4;
-  const void* ins[] = {Q, K, V, O, LSE, dO};
-  const size_t in_sz[] = {q_bytes, kv_bytes, kv_bytes, q_bytes, lse_bytes, q_bytes};
-  void* outs[] = {dQ, dK, dV, workspace};
-  const size_t out_sz[] = {q_bytes, kv_bytes, kv_bytes, workspace_bytes};
-  for (int i = 0; i < 4; ++i) {
-    for (int k = 0; k < 6; ++k)
-      if (overlaps(outs[i], out_sz[i], ins[k], in_sz[k]))
-        return fail(HK_ERR_INVALID_ARGUMENT, "outputs/workspace must not alias inputs");
-    for (int k = i + 1; k < 4; ++k)
-      if (overlaps(outs[i], out_sz[i], outs[k], out_sz[k]))
-        return fail(HK_ERR_INVALID_ARGUMENT, "outputs/workspace must not alias each other");
-  }
-  s = check_device(nullptr);
-  if (s != HK_OK) return s;
-  return hk::launch_bwd(Q, K, V, O, LSE, dO, dQ, dK, dV, reinterpret_cast<float*>(workspace), B, Hq, Hkv, N, d,
-                        causal != 0, stream, g_err, sizeof(g_err));
+  if (phase < 0 || phase > 2) return fail(HK_ERR_INVALID_ARGUMENT, "phase must be 0, 1 or 2");
+  return bwd_impl(phase, Q, K, V, O, LSE, dO, dQ, dK, dV, workspace, workspace_bytes, B, Hq, Hkv, N, d, causal,
+                  stream);
 }
 
 hk_status hk_diag_umma(const void* A, const void* Bm, float* D, int N, int K, int a_tmem, int b_mn,
