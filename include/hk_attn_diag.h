@@ -16,6 +16,13 @@
  * bench can time each on the stream in isolation:
  *   phase 0 = D-preprocess (writes the workspace), 1 = dK/dV pass, 2 = dQ pass.
  * Phases 1 and 2 read the workspace written by phase 0.
+ *
+ * hk_diag_rates: micro-benchmarks. kind 0: pipe issue rate of op `param`
+ * (0 ex2.f32, 1 cvt.bf16x2.f32, 2 fma.f32, 3 max.f32, 4 ex2.bf16x2, 5 add.f32),
+ * 148 CTAs x 512 threads x iters x 8 ops; out[cta] = clock64 cycles.
+ * kind 1: tcgen05.mma pacing, mode = param / 1000 (0 SS, 1 TS, 2 SS with B
+ * MN-major), N = param % 1000 in {64,128,256}; out[cta] = cycles per MMA.
+ * `out` is a device pointer to >= 148 floats.
  */
 #ifndef HK_ATTN_DIAG_H_
 #define HK_ATTN_DIAG_H_
@@ -28,6 +35,7 @@ hk_status hk_diag_umma(const void* A, const void* B, float* D, int N, int K, int
 hk_status hk_diag_bwd_phase(int phase, const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                             const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
                             int B, int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream);
+hk_status hk_diag_rates(int kind, int param, int iters, float* out, cudaStream_t stream);
 #ifdef __cplusplus
 }
 #endif

@@ -8,7 +8,9 @@ from __future__ import annotations
 import ctypes
 import os
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhkattn.so")
+# HK_LIB=debug selects the -DHK_DEBUG_HANG build (barrier waits trap with a message).
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                         "libhkattn_debug.so" if os.environ.get("HK_LIB") == "debug" else "libhkattn.so")
 _lib = None
 
 HK_STATUS = {0: "HK_OK", 1: "HK_ERR_INVALID_ARGUMENT", 2: "HK_ERR_UNSUPPORTED",
@@ -24,6 +26,7 @@ SIGNATURES = {
     "hk_status_string": (ctypes.c_char_p, [_I]),
     "hk_attn_abi_version": (_I, []),
     "hk_diag_umma": (_I, [_P, _P, _P, _I, _I, _I, _I, _P]),
+    "hk_diag_rates": (_I, [_I, _I, _I, _P, _P]),
     "hk_diag_bwd_phase": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _I, _I, _I, _I, _I, _I, _P]),
 }
 

@@ -9,6 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhkattn.so")
+LIB_DEBUG = os.path.join(PKG, "libhkattn_debug.so")  # -DHK_DEBUG_HANG: barrier waits trap instead of hanging
 SOURCES = [os.path.join(CSRC, "hk_attn.cu")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
@@ -29,23 +30,24 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    lib = LIB_DEBUG if debug else LIB
+    if not force and not debug and not needs_build():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *SOURCES]
+    tmp = lib + ".tmp"
+    cmd = [NVCC, *FLAGS, *(["-DHK_DEBUG_HANG"] if debug else []), "-o", tmp, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libhkattn.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
-        f.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    if not debug:
+        with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+            f.write(r.stderr)
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv))

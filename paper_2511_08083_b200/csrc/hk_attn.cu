@@ -17,6 +17,7 @@
 #include "bwd.cuh"
 #include "fwd.cuh"
 #include "tma_host.h"
+#include "rates_diag.cuh"
 #include "umma_diag.cuh"
 
 namespace {
@@ -233,6 +234,39 @@ hk_status hk_diag_umma(const void* A, const void* Bm, float* D, int N, int K, in
   HK_DIAG(128, 128, false, true) HK_DIAG(128, 128, true, false) HK_DIAG(128, 128, true, true)
 #undef HK_DIAG
   return fail(HK_ERR_UNSUPPORTED, "unsupported diag configuration");
+}
+
+hk_status hk_diag_rates(int kind, int param, int iters, float* out, cudaStream_t stream) {
+  g_err[0] = 0;
+  if (!out || iters <= 0) return fail(HK_ERR_INVALID_ARGUMENT, "bad arguments");
+  hk_status s = check_device(nullptr);
+  if (s != HK_OK) return s;
+  static float* sink = nullptr;
+  if (!sink && cudaMalloc(&sink, 16) != cudaSuccess) return fail(HK_ERR_DEVICE, "cudaMalloc failed");
+  if (kind == 0) {
+    switch (param) {
+      case 0: hk::pipe_rate_kernel<0><<<148, 512, 0, stream>>>(iters, out, sink); break;
+      case 1: hk::pipe_rate_kernel<1><<<148, 512, 0, stream>>>(iters, out, sink); break;
+      case 2: hk::pipe_rate_kernel<2><<<148, 512, 0, stream>>>(iters, out, sink); break;
+      case 3: hk::pipe_rate_kernel<3><<<148, 512, 0, stream>>>(iters, out, sink); break;
+      case 4: hk::pipe_rate_kernel<4><<<148, 512, 0, stream>>>(iters, out, sink); break;
+      case 5: hk::pipe_rate_kernel<5><<<148, 512, 0, stream>>>(iters, out, sink); break;
+      default: return fail(HK_ERR_UNSUPPORTED, "unknown op");
+    }
+    return launched("hk_diag_rates");
+  }
+  const uint32_t smem = 128 * 128 * 2 + 256 * 128 * 2 + 1024;
+#define HK_RATE(MODE, NN)                                          \
+  if (param == MODE * 1000 + NN) {                                 \
+    auto* fn = hk::mma_rate_kernel<MODE, NN>;                      \
+    if ((s = ensure_smem(fn, smem)) != HK_OK) return s;            \
+    fn<<<148, 128, smem, stream>>>(iters, out);                    \
+    return launched("hk_diag_rates");                              \
+  }
+  HK_RATE(0, 64) HK_RATE(0, 128) HK_RATE(0, 256) HK_RATE(1, 64) HK_RATE(1, 128) HK_RATE(1, 256)
+  HK_RATE(2, 64) HK_RATE(2, 128) HK_RATE(2, 256)
+#undef HK_RATE
+  return fail(HK_ERR_UNSUPPORTED, "unknown mma mode");
 }
 
 }  // extern "C"

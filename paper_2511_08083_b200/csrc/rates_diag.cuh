@@ -1,0 +1,89 @@
+// Diagnostic micro-benchmarks (not the hot path): issue rates of the pipes the
+// softmax uses, and tcgen05.mma pacing for the operand forms the kernels use.
+#pragma once
+#include "ptx.cuh"
+
+namespace hk {
+
+// op: 0 ex2.approx.f32, 1 cvt.rn.bf16x2.f32, 2 fma.rn.f32 (3 regs), 3 max.f32,
+//     4 ex2.approx.ftz.bf16x2, 5 add.f32
+template <int OP>
+__global__ void __launch_bounds__(512) pipe_rate_kernel(int iters, float* out_cycles, float* sink) {
+  float a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = 0.001f * (threadIdx.x + i);
+  uint32_t u[8] = {};
+  const float b = 1.0001f, c = 0.9999f;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (OP == 0) asm volatile("ex2.approx.f32 %0, %0;" : "+f"(a[i]));
+      if (OP == 1) asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(u[i]) : "f"(a[i]), "f"(a[(i + 1) & 7]));
+      if (OP == 2) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(a[i]) : "f"(b), "f"(c));
+      if (OP == 3) asm volatile("max.f32 %0, %0, %1;" : "+f"(a[i]) : "f"(a[(i + 3) & 7]));
+      if (OP == 4) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(u[i]));
+      if (OP == 5) asm volatile("add.f32 %0, %0, %1;" : "+f"(a[i]) : "f"(b));
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i] + __uint_as_float(u[i]);
+  if (s == 12345.f) sink[0] = s;
+  if (threadIdx.x == 0) out_cycles[blockIdx.x] = (float)(t1 - t0);
+}
+
+// tcgen05.mma pacing: one CTA per SM, one thread issues iters x 8 MMAs
+// (M=128, N, K=16) on resident smem / TMEM operands; out = cycles per MMA.
+// mode 0: SS (A 128 rows K-major, B N rows K-major); mode 1: TS (A in TMEM,
+// B MN-major [16][N] slices); mode 2: SS with B MN-major.
+template <int MODE, int N>
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int iters, float* out_cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase_s;
+  // zero the operand tiles so the MMAs see finite data
+  for (int i = threadIdx.x; i < (128 * 128 * 2 + 256 * 128 * 2) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp_id() == 0) tmem_alloc<512>(&tbase_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tbase_s;
+  const uint32_t a_s = smem_u32(smem), b_s = a_s + 128 * 128 * 2;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16(128, N, 0, MODE == 0 ? 0 : 1);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if (MODE == 0)
+          umma_ss(tb, sdesc_sw128(a_s + (kk / 4) * 128 * 128 + (kk % 4) * 32, 16, 1024),
+                  sdesc_sw128(b_s + (kk / 4) * N * 128 + (kk % 4) * 32, 16, 1024), idesc, 1);
+        else if (MODE == 1)
+          umma_ts(tb, tb + 256 + kk * 8, sdesc_sw128(b_s + kk * 16 * 128, 128 * 128, 1024), idesc, 1);
+        else
+          umma_ss(tb, sdesc_sw128(a_s + (kk / 4) * 128 * 128 + (kk % 4) * 32, 16, 1024),
+                  sdesc_sw128(b_s + kk * 16 * 128, 128 * 128, 1024), idesc, 1);
+      }
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    out_cycles[blockIdx.x] = (float)(t1 - t0) / (iters * 8);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc<512>(tb);
+}
+
+}  // namespace hk

@@ -1,0 +1,31 @@
+"""Measure pipe issue rates and tcgen05.mma pacing on the GPU (diag entry point)."""
+import ctypes
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2511_08083_b200 import _lib  # noqa: E402
+
+L = _lib.lib()
+out = torch.zeros(148, device="cuda")
+res = {}
+names = ["ex2.f32", "cvt.bf16x2.f32", "fma.f32", "max.f32", "ex2.bf16x2", "add.f32"]
+for op, nm in enumerate(names):
+    iters = 4096
+    for _ in range(2):
+        _lib.check(L.hk_diag_rates(0, op, iters, ctypes.c_void_p(out.data_ptr()), None))
+    torch.cuda.synchronize()
+    cyc = out.float().mean().item()
+    res[nm + " per clk per SM"] = round(512 * iters * 8 / cyc, 2)
+for mode, mn in enumerate(["SS", "TS", "SS_Bmn"]):
+    for n in (64, 128, 256):
+        for _ in range(2):
+            _lib.check(L.hk_diag_rates(1, mode * 1000 + n, 2000, ctypes.c_void_p(out.data_ptr()), None))
+        torch.cuda.synchronize()
+        cyc = out.float().mean().item()
+        res[f"mma {mn} M=128 N={n} K=16 cycles"] = round(cyc, 2)
+        res[f"mma {mn} M=128 N={n} flop/clk/SM"] = round(2 * 128 * n * 16 / cyc, 1)
+print(json.dumps(res, indent=1))
