@@ -248,12 +248,13 @@ def main():
 
     from paper_2511_08083_b200 import _lib, attn_bwd, attn_fwd, bwd_workspace_bytes
     from paper_2511_08083_b200.inputs import make_inputs
+    from paper_2511_08083_b200.shard import weak_shard
 
     rank, world, local = dist_setup(args.gpus)
     B, N, Hq, Hkv, d, causal, label = cfg
     peaks = load_peaks()
-    # weak scaling: rank r owns global batches [r B, (r+1) B)
-    batches = list(range(rank * B, (rank + 1) * B))
+    # weak scaling: rank r owns global batches [r B, (r+1) B) (paper_2511_08083_b200/shard.py)
+    batches = list(weak_shard(rank, world, B, Hq, Hkv).batches)
     x = make_inputs(B * world, N, Hq, Hkv, d, seed=args.seed, device="cuda", batches=batches)
     q, k, v, do = x["Q"], x["K"], x["V"], x["dO"]
     o = torch.empty_like(q)

@@ -20,7 +20,10 @@ __global__ void __launch_bounds__(512) pipe_rate_kernel(int iters, float* out_cy
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (OP == 0) asm volatile("ex2.approx.f32 %0, %0;" : "+f"(a[i]));
-      if (OP == 1) asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(u[i]) : "f"(a[i]), "f"(a[(i + 1) & 7]));
+      if (OP == 1) {  // dependent chain: the packed result feeds the next conversion
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(u[i]) : "f"(a[i]), "f"(a[(i + 1) & 7]));
+        a[i] = __uint_as_float(u[i]);
+      }
       if (OP == 2) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(a[i]) : "f"(b), "f"(c));
       if (OP == 3) asm volatile("max.f32 %0, %0, %1;" : "+f"(a[i]) : "f"(a[(i + 3) & 7]));
       if (OP == 4) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(u[i]));
