@@ -20,9 +20,16 @@
  * hk_diag_rates: micro-benchmarks. kind 0: pipe issue rate of op `param`
  * (0 ex2.f32, 1 cvt.bf16x2.f32, 2 fma.f32, 3 max.f32, 4 ex2.bf16x2, 5 add.f32),
  * 148 CTAs x 512 threads x iters x 8 ops; out[cta] = clock64 cycles.
+ * kind 2: tcgen05.ld (32x32b.x32) bandwidth with `param` warps x 128 columns.
+ * kind 3: forward softmax step, param = 10 * (emulated exps per 8) + warpgroups.
  * kind 1: tcgen05.mma pacing, mode = param / 1000 (0 SS, 1 TS, 2 SS with B
  * MN-major), N = param % 1000 in {64,128,256}; out[cta] = cycles per MMA.
  * `out` is a device pointer to >= 148 floats.
+ *
+ * hk_diag_trace_read: copy the in-kernel event trace of an HK_TRACE build
+ * (pairs of u64: event<<48 | a<<32 | b, then clock64) into the host buffer
+ * `dst` (capacity `bytes`); returns the number of u64 words via the status
+ * HK_OK and writes nothing on non-trace builds (count 0). reset != 0 clears it.
  */
 #ifndef HK_ATTN_DIAG_H_
 #define HK_ATTN_DIAG_H_
@@ -36,6 +43,7 @@ hk_status hk_diag_bwd_phase(int phase, const void* Q, const void* K, const void*
                             const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
                             int B, int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream);
 hk_status hk_diag_rates(int kind, int param, int iters, float* out, cudaStream_t stream);
+hk_status hk_diag_trace_read(void* dst, size_t bytes, int reset);
 #ifdef __cplusplus
 }
 #endif

@@ -9,8 +9,10 @@ import ctypes
 import os
 
 # HK_LIB=debug selects the -DHK_DEBUG_HANG build (barrier waits trap with a message).
+# HK_LIB=trace selects the -DHK_TRACE build (in-kernel event trace, hk_diag_trace_read).
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
-                         "libhkattn_debug.so" if os.environ.get("HK_LIB") == "debug" else "libhkattn.so")
+                         {"debug": "libhkattn_debug.so", "trace": "libhkattn_trace.so"}.get(
+                             os.environ.get("HK_LIB", ""), "libhkattn.so"))
 _lib = None
 
 HK_STATUS = {0: "HK_OK", 1: "HK_ERR_INVALID_ARGUMENT", 2: "HK_ERR_UNSUPPORTED",
@@ -27,6 +29,7 @@ SIGNATURES = {
     "hk_attn_abi_version": (_I, []),
     "hk_diag_umma": (_I, [_P, _P, _P, _I, _I, _I, _I, _P]),
     "hk_diag_rates": (_I, [_I, _I, _I, _P, _P]),
+    "hk_diag_trace_read": (_I, [_P, _Z, _I]),
     "hk_diag_bwd_phase": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _I, _I, _I, _I, _I, _I, _P]),
 }
 

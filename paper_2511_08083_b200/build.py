@@ -10,6 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhkattn.so")
 LIB_DEBUG = os.path.join(PKG, "libhkattn_debug.so")  # -DHK_DEBUG_HANG: barrier waits trap instead of hanging
+LIB_TRACE = os.path.join(PKG, "libhkattn_trace.so")  # -DHK_TRACE: in-kernel clock64 event trace
 SOURCES = [os.path.join(CSRC, "hk_attn.cu")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
@@ -30,19 +31,20 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
-    lib = LIB_DEBUG if debug else LIB
-    if not force and not debug and not needs_build():
+def build(force: bool = False, verbose: bool = False, debug: bool = False, trace: bool = False) -> str:
+    lib = LIB_DEBUG if debug else LIB_TRACE if trace else LIB
+    if not force and not (debug or trace) and not needs_build():
         return LIB
     tmp = lib + ".tmp"
-    cmd = [NVCC, *FLAGS, *(["-DHK_DEBUG_HANG"] if debug else []), "-o", tmp, *SOURCES]
+    extra = (["-DHK_DEBUG_HANG"] if debug else []) + (["-DHK_TRACE"] if trace else [])
+    cmd = [NVCC, *FLAGS, *extra, "-o", tmp, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libhkattn.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    if not debug:
+    if not (debug or trace):
         with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
             f.write(r.stderr)
     os.replace(tmp, lib)
@@ -50,4 +52,4 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv, trace="--trace" in sys.argv))

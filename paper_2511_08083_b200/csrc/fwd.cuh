@@ -8,11 +8,13 @@
 // rescaled by exp2(m_old - m_new) before P V accumulates (mul_col then
 // mma_AtB: P:1398-1400), LSE = max ln2 + ln(norm).
 //
-// B200 design (DESIGN.md §Forward): one CTA = (b, h, two 128-row Q tiles).
+// B200 design (DESIGN.md §6): one CTA = (b, h, two 128-row Q tiles).
 //   warps 0-3  softmax WG0: Q tile 0, one thread per query row (TMEM lane)
 //   warps 4-7  softmax WG1: Q tile 1
 //   warp  8    TMA producer: Q0/Q1 once, then a K ring and a V ring
 //   warp  9    MMA issuer (one thread): S_t = Q_t K_j^T, O_t += P_t V_j
+//   warps 10-11 idle (WG2 = warps 8-11 drops to 72 registers, WG0/WG1 rise to 216:
+//   128*72 + 256*216 = 64512 = the CTA pool at launch, 384 x 168)
 // TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D,256+2D);
 // bf16 P_t is written over S_t's first 64 columns (A operand from TMEM).
 // The two Q tiles ping-pong: while WG0 does softmax on S0(j+1) the tensor
@@ -20,13 +22,17 @@
 // O rescale is lazy: the running max only moves when it grows by more than
 // RESCALE_TH (log2 units); l and O always share the same (possibly stale)
 // max, which is exact in exact arithmetic (reading #8).
+// Softmax issue economy: 3-input max, packed f32x2 FMA/ADD,
+// and EMU_OF_8/8 of the exponentials evaluated by a polynomial on the FMA
+// pipe instead of the MUFU (16 ex2/clk/SM, the co-bottleneck at d=128).
 #pragma once
 #include "ptx.cuh"
+#include "softmax.cuh"
 
 namespace hk {
 
 struct FwdParams {
-  float* lse;   // [B][Hq][N]
+  float* lse;        // [B][Hq][N]
   __nv_bfloat16* o;  // [B][N][Hq][D]
   int B, Hq, Hkv, N;
   int num_pairs;  // ceil(N / 256)
@@ -34,15 +40,13 @@ struct FwdParams {
 
 template <int D>
 struct FwdCfg {
-  static constexpr int BM = 128, BN = 128;
   static constexpr int PANELS = D / 64;
   static constexpr uint32_t TILE_BYTES = 128 * D * 2;  // one 128-row tile
   static constexpr int NS = (D == 128) ? 2 : 4;        // K/V ring depth
   static constexpr uint32_t SMEM = 2 * TILE_BYTES + 2 * NS * TILE_BYTES + 1024;
   static constexpr int THREADS = 384;
+  static constexpr int EMU_OF_8 = (D == 128) ? 3 : 4;  // exps per 8 on the FMA pipe
 };
-
-constexpr float RESCALE_TH = 8.0f;
 
 template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(384, 1)
@@ -54,9 +58,9 @@ __global__ void __launch_bounds__(384, 1)
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                 // 2 tiles
-  uint8_t* sK = smem + 2 * TB;        // NS tiles
-  uint8_t* sV = sK + NS * TB;         // NS tiles
+  uint8_t* sQ = smem;           // 2 tiles
+  uint8_t* sK = smem + 2 * TB;  // NS tiles
+  uint8_t* sV = sK + NS * TB;   // NS tiles
 
   __shared__ uint64_t bar_q, bar_kfull[NS], bar_kempty[NS], bar_vfull[NS], bar_vempty[NS];
   __shared__ uint64_t bar_s[2], bar_p[2], bar_o[2];
@@ -102,12 +106,11 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tmem_base_s;
-  const uint32_t tS[2] = {tbase, tbase + 128};
-  const uint32_t tO[2] = {tbase + 256, tbase + 256 + D};
 
-  if (warp == 8) {
-    // ================= TMA producer =================
-    if (lane == 0) {
+  if (warp >= 8) {
+    reg_dealloc<72>();
+    if (warp == 8 && lane == 0) {
+      // ================= TMA producer =================
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
       mbar_arrive_expect_tx(&bar_q, (has1 ? 2 : 1) * TB);
@@ -115,9 +118,9 @@ __global__ void __launch_bounds__(384, 1)
         tma_load_4d(&mapQ, &bar_q, sQ + pnl * 128 * 128, pnl * 64, h, qt0 * 128, b, pol_q);
         if (has1) tma_load_4d(&mapQ, &bar_q, sQ + TB + pnl * 128 * 128, pnl * 64, h, qt1 * 128, b, pol_q);
       }
+      int s = 0;
+      uint32_t ph = 0;
       for (int j = 0; j < nkv; ++j) {
-        const int s = j % NS;
-        const uint32_t ph = (j / NS) & 1;
         mbar_wait(&bar_kempty[s], ph ^ 1);
         mbar_arrive_expect_tx(&bar_kfull[s], TB);
         for (int pnl = 0; pnl < C::PANELS; ++pnl)
@@ -126,72 +129,79 @@ __global__ void __launch_bounds__(384, 1)
         mbar_arrive_expect_tx(&bar_vfull[s], TB);
         for (int pnl = 0; pnl < C::PANELS; ++pnl)
           tma_load_4d(&mapV, &bar_vfull[s], sV + s * TB + pnl * 128 * 128, pnl * 64, kvh, j * 128, b, pol_kv);
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1;
+        }
       }
-    }
-  } else if (warp == 9) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
+    } else if (warp == 9 && lane == 0) {
+      // ================= MMA issuer =================
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);  // S = Q K^T: A K-major, B K-major
       constexpr uint32_t idesc_o = idesc_bf16(128, D, 0, 1);    // O += P V: A TMEM, B (V) MN-major
-      const int nk[2] = {nkv0, nkv1};
       auto issue_s = [&](int t, int s) {
         const uint32_t qa = smem_u32(sQ + t * TB);
         const uint32_t ka = smem_u32(sK + s * TB);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk / 4) * 128 * 128 + (kk % 4) * 32;
-          umma_ss(tS[t], sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), idesc_s, kk > 0);
+          umma_ss(tbase + 128 * t, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), idesc_s,
+                  kk > 0);
         }
+        tc_commit(&bar_s[t]);
       };
       auto issue_pv = [&](int t, int s, int j) {
         const uint32_t va = smem_u32(sV + s * TB);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
-          umma_ts(tO[t], tS[t] + kk * 8, sdesc_sw128(va + kk * 16 * 128, 128 * 128, 1024), idesc_o,
-                  (j > 0 || kk > 0) ? 1u : 0u);
+          umma_ts(tbase + 256 + D * t, tbase + 128 * t + kk * 8, sdesc_sw128(va + kk * 16 * 128, 128 * 128, 1024),
+                  idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
       };
       mbar_wait(&bar_q, 0);
       mbar_wait(&bar_kfull[0], 0);
       tc_fence_after();
       issue_s(0, 0);
-      tc_commit(&bar_s[0]);
-      if (nk[1] > 0) {
-        issue_s(1, 0);
-        tc_commit(&bar_s[1]);
-      }
+      if (nkv1 > 0) issue_s(1, 0);
       tc_commit(&bar_kempty[0]);
+      int s = 0;
+      uint32_t ph = 0;
       for (int j = 0; j < nkv; ++j) {
-        const int s = j % NS;
-        const uint32_t ph = (j / NS) & 1;
-        const int s1 = (j + 1) % NS;
-        const uint32_t ph1 = ((j + 1) / NS) & 1;
+        const int s1 = s + 1 == NS ? 0 : s + 1;
+        const uint32_t ph1 = s + 1 == NS ? ph ^ 1 : ph;
         mbar_wait(&bar_vfull[s], ph);
         bool k_next_waited = false;
+#pragma unroll
         for (int t = 0; t < 2; ++t) {
-          if (j >= nk[t]) continue;
-          mbar_wait(&bar_p[t], j & 1);
-          tc_fence_after();
-          issue_pv(t, s, j);
-          if (j + 1 < nk[t]) {
-            if (!k_next_waited) {
-              mbar_wait(&bar_kfull[s1], ph1);
-              tc_fence_after();
-              k_next_waited = true;
+          const int nk = t == 0 ? nkv0 : nkv1;
+          if (j < nk) {
+            mbar_wait(&bar_p[t], j & 1);
+            tc_fence_after();
+            hk_trace(10 + t, j, 0);  // MMA: P_t(j) seen, PV issue
+            issue_pv(t, s, j);
+            if (j + 1 < nk) {
+              if (!k_next_waited) {
+                mbar_wait(&bar_kfull[s1], ph1);
+                tc_fence_after();
+                k_next_waited = true;
+              }
+              issue_s(t, s1);
+            } else {
+              tc_commit(&bar_o[t]);
             }
-            issue_s(t, s1);
-            tc_commit(&bar_s[t]);
-          } else {
-            tc_commit(&bar_o[t]);
           }
         }
-        tc_commit(&bar_vempty[s]);
+        if (j + 1 < nkv) tc_commit(&bar_vempty[s]);
         if (k_next_waited) tc_commit(&bar_kempty[s1]);
+        s = s1;
+        ph = ph1;
       }
     }
-  } else if (warp < 8) {
+  } else {
     // ================= softmax warpgroups =================
+    reg_alloc<216>();
     const int t = warp >> 2;  // Q tile of this warpgroup
     const int nk = t == 0 ? nkv0 : nkv1;
+    const uint32_t tS = tbase + 128 * t;
+    const uint32_t tO = tbase + 256 + D * t;
     if (nk > 0) {
       const int qt = t == 0 ? qt0 : qt1;
       const uint32_t lane_base = (warp & 3) * 32;
@@ -200,59 +210,17 @@ __global__ void __launch_bounds__(384, 1)
       float m = -INFINITY;  // running max, log2-scaled units
       float l = 0.f;        // running row sum
       for (int j = 0; j < nk; ++j) {
+        if (threadIdx.x % 128 == 0) hk_trace(1, t, j);  // softmax: start waiting for S_t(j)
         mbar_wait(&bar_s[t], j & 1);
         tc_fence_after();
-        uint32_t sr[128];
-#pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32)
-          tmem_ld32(tmem_addr(tS[t], lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(&sr[c0]));
-        tmem_wait_ld();
-        float* s = reinterpret_cast<float*>(sr);
-        if (CAUSAL && j == qt) {
-#pragma unroll
-          for (int cc = 0; cc < 128; ++cc)
-            if (cc > r) s[cc] = -INFINITY;  // key j*128+cc > query qt*128+r
-        }
-        float mx = s[0];
-#pragma unroll
-        for (int cc = 1; cc < 128; ++cc) mx = fmaxf(mx, s[cc]);
-        const float mxs = mx * c;
-        float m_use = m, alpha = 1.f;
-        if (mxs > m + RESCALE_TH) {  // also taken on the first tile (m = -inf)
-          m_use = mxs;
-          alpha = ex2(m - m_use);
-        }
-        float rs = 0.f;
-#pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int cc = 0; cc < 32; cc += 2) {
-            const float p0 = ex2(fmaf(s[c0 + cc], c, -m_use));
-            const float p1 = ex2(fmaf(s[c0 + cc + 1], c, -m_use));
-            rs += p0 + p1;
-            pk[cc / 2] = pack_bf16(p0, p1);
-          }
-          tmem_st16(tmem_addr(tS[t], lane_base, c0 / 2), pk);
-        }
-        l = l * alpha + rs;
-        // O_t holds P_t(j-1) V_{j-1}: complete, since bar_s[t] tracked every earlier MMA.
-        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 32) {
-            uint32_t o[32];
-            tmem_ld32(tmem_addr(tO[t], lane_base, c0), o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int cc = 0; cc < 32; ++cc) o[cc] = __float_as_uint(__uint_as_float(o[cc]) * alpha);
-            tmem_st32(tmem_addr(tO[t], lane_base, c0), o);
-          }
-        }
-        m = m_use;
+        if (threadIdx.x % 128 == 0) hk_trace(2, t, j);  // S_t(j) ready
+        const bool diag = CAUSAL && j == qt;
+        softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, diag, j > 0);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_p[t]);
+        if (threadIdx.x % 128 == 0) hk_trace(3, t, j);  // P_t(j) published
       }
       // ---- epilogue: O = O_acc / l (bf16), LSE = (m + log2 l) ln 2
       mbar_wait(&bar_o[t], 0);
@@ -263,7 +231,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t o[32];
-        tmem_ld32(tmem_addr(tO[t], lane_base, c0), o);
+        tmem_ld32(tmem_addr(tO, lane_base, c0), o);
         tmem_wait_ld();
         uint4 v[4];
         uint32_t* vp = reinterpret_cast<uint32_t*>(v);

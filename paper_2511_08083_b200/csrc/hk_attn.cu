@@ -244,14 +244,40 @@ hk_status hk_diag_rates(int kind, int param, int iters, float* out, cudaStream_t
   static float* sink = nullptr;
   if (!sink && cudaMalloc(&sink, 16) != cudaSuccess) return fail(HK_ERR_DEVICE, "cudaMalloc failed");
   if (kind == 0) {
+    const int threads = param >= 100 ? 128 : 512;  // param + 100: one warp per SMSP
+    param %= 100;
     switch (param) {
-      case 0: hk::pipe_rate_kernel<0><<<148, 512, 0, stream>>>(iters, out, sink); break;
-      case 1: hk::pipe_rate_kernel<1><<<148, 512, 0, stream>>>(iters, out, sink); break;
-      case 2: hk::pipe_rate_kernel<2><<<148, 512, 0, stream>>>(iters, out, sink); break;
-      case 3: hk::pipe_rate_kernel<3><<<148, 512, 0, stream>>>(iters, out, sink); break;
-      case 4: hk::pipe_rate_kernel<4><<<148, 512, 0, stream>>>(iters, out, sink); break;
-      case 5: hk::pipe_rate_kernel<5><<<148, 512, 0, stream>>>(iters, out, sink); break;
+      case 0: hk::pipe_rate_kernel<0><<<148, threads, 0, stream>>>(iters, out, sink); break;
+      case 1: hk::pipe_rate_kernel<1><<<148, threads, 0, stream>>>(iters, out, sink); break;
+      case 2: hk::pipe_rate_kernel<2><<<148, threads, 0, stream>>>(iters, out, sink); break;
+      case 3: hk::pipe_rate_kernel<3><<<148, threads, 0, stream>>>(iters, out, sink); break;
+      case 4: hk::pipe_rate_kernel<4><<<148, threads, 0, stream>>>(iters, out, sink); break;
+      case 5: hk::pipe_rate_kernel<5><<<148, threads, 0, stream>>>(iters, out, sink); break;
+      case 6: hk::pipe_rate_kernel<6><<<148, threads, 0, stream>>>(iters, out, sink); break;
+      case 7: hk::pipe_rate_kernel<7><<<148, threads, 0, stream>>>(iters, out, sink); break;
+      case 8: hk::pipe_rate_kernel<8><<<148, threads, 0, stream>>>(iters, out, sink); break;
+      case 9: hk::pipe_rate_kernel<9><<<148, threads, 0, stream>>>(iters, out, sink); break;
+      case 10: hk::pipe_rate_kernel<10><<<148, threads, 0, stream>>>(iters, out, sink); break;
       default: return fail(HK_ERR_UNSUPPORTED, "unknown op");
+    }
+    return launched("hk_diag_rates");
+  }
+  if (kind == 2) {  // TMEM load bandwidth: param = number of warps (4, 8 or 16), 128 columns each
+    if (param != 4 && param != 8 && param != 16) return fail(HK_ERR_UNSUPPORTED, "warps must be 4, 8 or 16");
+    hk::tmem_ld_rate_kernel<128><<<148, 32 * param, 0, stream>>>(iters, out, sink);
+    return launched("hk_diag_rates");
+  }
+  if (kind == 3) {  // softmax step: param = 10 * EMU_OF_8 + warpgroups (1 or 2)
+    const int nwg = param % 10, emu = param / 10;
+    if (nwg < 1 || nwg > 2) return fail(HK_ERR_UNSUPPORTED, "1 or 2 warpgroups");
+    dim3 g(148), blk(128 * nwg);
+    switch (emu) {
+      case 0: hk::softmax_rate_kernel<0><<<g, blk, 0, stream>>>(iters, out, sink); break;
+      case 2: hk::softmax_rate_kernel<2><<<g, blk, 0, stream>>>(iters, out, sink); break;
+      case 3: hk::softmax_rate_kernel<3><<<g, blk, 0, stream>>>(iters, out, sink); break;
+      case 4: hk::softmax_rate_kernel<4><<<g, blk, 0, stream>>>(iters, out, sink); break;
+      case 5: hk::softmax_rate_kernel<5><<<g, blk, 0, stream>>>(iters, out, sink); break;
+      default: return fail(HK_ERR_UNSUPPORTED, "emu must be 0, 2, 3, 4 or 5");
     }
     return launched("hk_diag_rates");
   }
@@ -267,6 +293,32 @@ hk_status hk_diag_rates(int kind, int param, int iters, float* out, cudaStream_t
   HK_RATE(2, 64) HK_RATE(2, 128) HK_RATE(2, 256)
 #undef HK_RATE
   return fail(HK_ERR_UNSUPPORTED, "unknown mma mode");
+}
+
+hk_status hk_diag_trace_read(void* dst, size_t bytes, int reset) {
+  g_err[0] = 0;
+#ifdef HK_TRACE
+  unsigned n = 0;
+  if (cudaMemcpyFromSymbol(&n, hk::g_hk_trace_n, sizeof(n)) != cudaSuccess)
+    return fail(HK_ERR_DEVICE, "trace count read failed");
+  if (n > (1u << 16)) n = 1u << 16;
+  size_t want = (size_t)n * 8;
+  if (dst && bytes >= 8) {
+    if (want > bytes - 8) want = (bytes - 8) / 8 * 8;
+    unsigned long long cnt = want / 8;
+    memcpy(dst, &cnt, 8);
+    if (want && cudaMemcpyFromSymbol(static_cast<char*>(dst) + 8, hk::g_hk_trace, want) != cudaSuccess)
+      return fail(HK_ERR_DEVICE, "trace read failed");
+  }
+  if (reset) {
+    unsigned z = 0;
+    cudaMemcpyToSymbol(hk::g_hk_trace_n, &z, sizeof(z));
+  }
+#else
+  (void)reset;
+  if (dst && bytes >= 8) memset(dst, 0, 8);
+#endif
+  return HK_OK;
 }
 
 }  // extern "C"

@@ -26,6 +26,27 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// ------------------------------------------------------------------ tracing (HK_TRACE builds only)
+// hk_trace(ev, a, b): record (event, a, b, clock64) from one traced CTA into
+// a device ring read back by hk_diag_trace_read (include/hk_attn_diag.h).
+#ifdef HK_TRACE
+__device__ unsigned long long g_hk_trace[1 << 16];
+__device__ unsigned int g_hk_trace_n;
+__device__ __forceinline__ bool hk_trace_cta() {
+  return blockIdx.x == gridDim.x / 2 && blockIdx.y == 0 && blockIdx.z == 0;
+}
+__device__ __forceinline__ void hk_trace(uint32_t ev, uint32_t a, uint32_t b) {
+  if (!hk_trace_cta()) return;
+  const unsigned i = atomicAdd(&g_hk_trace_n, 2u);
+  if (i + 1 < (1u << 16)) {
+    g_hk_trace[i] = ((unsigned long long)ev << 48) | ((unsigned long long)(a & 0xFFFF) << 32) | (b & 0xFFFFFFFFu);
+    g_hk_trace[i + 1] = (unsigned long long)clock64();
+  }
+}
+#else
+__device__ __forceinline__ void hk_trace(uint32_t, uint32_t, uint32_t) {}
+#endif
+
 // ------------------------------------------------------------------ mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -256,6 +277,67 @@ __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+
+// ------------------------------------------------------------------ packed fp32x2 (sm_100 FFMA2/FADD2/FMUL2)
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// 2^x for a pair on the FMA pipe (offloads the MUFU): x = n + f, n = rint(x) via the
+// 1.5*2^23 magic add, f in [-1/2, 1/2], 2^f by a degree-3 minimax polynomial
+// (max relative error 7.7e-5, below bf16's 3.9e-3), 2^n added into the exponent bits.
+// Valid for x <= 127; x is clamped at -125 (result ~2e-38, not 0) so that the
+// exponent-field add cannot underflow for 2^f < 1.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 j = add2(x, magic);
+  const float2 f = sub2(x, sub2(j, magic));
+  float2 p = fma2(make_float2(0.05508885905f, 0.05508885905f), f, make_float2(0.242604658f, 0.242604658f));
+  p = fma2(p, f, make_float2(0.6932762861f, 0.6932762861f));
+  p = fma2(p, f, make_float2(0.999928891658f, 0.999928891658f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
 }
 
 // ------------------------------------------------------------------ math

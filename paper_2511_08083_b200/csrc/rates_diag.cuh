@@ -2,6 +2,7 @@
 // softmax uses, and tcgen05.mma pacing for the operand forms the kernels use.
 #pragma once
 #include "ptx.cuh"
+#include "softmax.cuh"
 
 namespace hk {
 
@@ -28,6 +29,23 @@ __global__ void __launch_bounds__(512) pipe_rate_kernel(int iters, float* out_cy
       if (OP == 3) asm volatile("max.f32 %0, %0, %1;" : "+f"(a[i]) : "f"(a[(i + 3) & 7]));
       if (OP == 4) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(u[i]));
       if (OP == 5) asm volatile("add.f32 %0, %0, %1;" : "+f"(a[i]) : "f"(b));
+      if (OP == 6) {  // fma.rn.f32x2 on register pairs (a[i], a[i^1])
+        if ((i & 1) == 0) {
+          float2 v = fma2(make_float2(a[i], a[i + 1]), make_float2(b, c), make_float2(a[(i + 2) & 7], a[(i + 3) & 7]));
+          a[i] = v.x;
+          a[i + 1] = v.y;
+        }
+      }
+      if (OP == 7) {
+        if ((i & 1) == 0) {
+          float2 v = add2(make_float2(a[i], a[i + 1]), make_float2(a[(i + 2) & 7], a[(i + 3) & 7]));
+          a[i] = v.x;
+          a[i + 1] = v.y;
+        }
+      }
+      if (OP == 8) a[i] = max3f(a[i], a[(i + 3) & 7], a[(i + 5) & 7]);
+      if (OP == 9) a[i] = __int_as_float(__float_as_int(a[i]) + (__float_as_int(a[(i + 3) & 7]) << 23));
+      if (OP == 10) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(a[i]) : "f"(a[(i + 3) & 7]), "f"(a[(i + 5) & 7]));
     }
   }
   __syncthreads();
@@ -87,6 +105,78 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int iters, float* out_
   tc_fence_before();
   __syncthreads();
   if (warp_id() == 0) tmem_dealloc<512>(tb);
+}
+
+// TMEM -> register bandwidth: W warps (W/4 warpgroups) each repeatedly load
+// their 32 lanes x NC columns with tcgen05.ld.32x32b.x32; out = cycles.
+template <int NC>
+__global__ void tmem_ld_rate_kernel(int iters, float* out_cycles, float* sink) {
+  __shared__ uint32_t tbase_s;
+  if (warp_id() == 0) tmem_alloc<512>(&tbase_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tbase_s + ((warp_id() & 3) * 32 << 16) + (warp_id() / 4) * NC;
+  float acc = 0.f;
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c0 = 0; c0 < NC; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(tb + c0, r);
+      tmem_wait_ld();
+      acc += __uint_as_float(r[0]) + __uint_as_float(r[31]);
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (acc == 1234.5f) sink[0] = acc;
+  if (threadIdx.x == 0) out_cycles[blockIdx.x] = (float)(t1 - t0);
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc<512>(tbase_s);
+}
+
+// Forward softmax step throughput in isolation (no MMAs): NWG warpgroups each
+// run softmax_step on their own 128-column TMEM score tile `iters` times;
+// out = cycles per step (clock64, thread 0). The running max is reset every
+// step so the (rare) O-rescale branch is not exercised.
+template <int EMU_OF_8>
+__global__ void softmax_rate_kernel(int iters, float* out_cycles, float* sink) {
+  __shared__ uint32_t tbase_s;
+  if (warp_id() == 0) tmem_alloc<512>(&tbase_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const int t = warp_id() / 4;
+  const uint32_t lane_base = (warp_id() & 3) * 32;
+  const int r = lane_base + lane_id();
+  const uint32_t tS = tbase_s + 128 * t, tO = tbase_s + 256 + 128 * t;
+  uint32_t init[32];
+  for (int c0 = 0; c0 < 128; c0 += 32) {
+    for (int k = 0; k < 32; ++k) {
+      uint32_t hsh = (r * 131 + c0 + k) * 2654435761u;
+      init[k] = __float_as_uint(((hsh >> 8) & 0xFFFF) / 6553.6f - 5.f);
+    }
+    tmem_st32(tmem_addr(tS, lane_base, c0), init);
+  }
+  tmem_wait_st();
+  __syncthreads();
+  const float c = 1.4426950408889634f / sqrtf(128.f);
+  float l = 0.f, msum = 0.f;
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    float m = -INFINITY;
+    softmax_step<128, EMU_OF_8>(tS, tO, lane_base, r, c, m, l, false, false);
+    msum += m;
+  }
+  tmem_wait_st();
+  const long long t1 = clock64();
+  if (l + msum == 1234.5f) sink[0] = l;
+  if (threadIdx.x == 0) out_cycles[blockIdx.x] = (float)(t1 - t0) / iters;
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc<512>(tbase_s);
 }
 
 }  // namespace hk

@@ -1,0 +1,112 @@
+// One online-softmax step of the forward pass for one query row per thread
+// (PAPER.md P:1338-1340): read the 128 scores of
+// this row from TMEM, row max, P = 2^(c s - m) packed to bf16 back into TMEM
+// (over the scores, as the A operand of O += P V), row sum, and the lazy O
+// rescale. Shared by fwd_kernel and the softmax_rate micro-benchmark.
+#pragma once
+#include "ptx.cuh"
+
+namespace hk {
+
+constexpr float RESCALE_TH = 8.0f;
+constexpr float EXP_MAGIC = 12582912.f;  // 1.5 * 2^23: x + magic rounds x to an integer in the low mantissa
+
+// P for 32 consecutive scores (16 pairs), packed to bf16 pairs; the row sum is
+// accumulated in `acc`. EMU_OF_8 of every 8 pairs are evaluated on the FMA
+// pipe: with an integral running max m, j = c s + (magic - m) holds
+// n = rint(c s - m) in its mantissa, f = c s - m - n is recovered exactly from
+// (magic - m) - j, 2^f comes from a degree-3 minimax polynomial (relative
+// error 7.7e-5 < bf16's 3.9e-3) and n is added into the exponent bits. Scores
+// are clamped so c s - m >= -125 (the exponent add cannot underflow).
+template <bool EMU, int EMU_OF_8>
+__device__ __forceinline__ void softmax_chunk32(const float* s, float c, float m, float smin, uint32_t (&pk)[16],
+                                                float2 (&acc)[2]) {
+  const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
+  const float2 bias2 = make_float2(EXP_MAGIC - m, EXP_MAGIC - m);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    float2 e;
+    if (EMU && (k % 8) < EMU_OF_8) {
+      const float2 sc = make_float2(fmaxf(s[2 * k], smin), fmaxf(s[2 * k + 1], smin));
+      const float2 j = fma2(sc, c2, bias2);
+      const float2 f = fma2(sc, c2, sub2(bias2, j));
+      float2 q = fma2(make_float2(0.05508885905f, 0.05508885905f), f, make_float2(0.242604658f, 0.242604658f));
+      q = fma2(q, f, make_float2(0.6932762861f, 0.6932762861f));
+      q = fma2(q, f, make_float2(0.999928891658f, 0.999928891658f));
+      e = make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(j.x) << 23)),
+                      __int_as_float(__float_as_int(q.y) + (__float_as_int(j.y) << 23)));
+    } else {
+      const float2 x = fma2(make_float2(s[2 * k], s[2 * k + 1]), c2, nm2);
+      e = make_float2(ex2(x.x), ex2(x.y));
+    }
+    acc[k & 1] = add2(acc[k & 1], e);
+    pk[k] = pack_bf16(e.x, e.y);
+  }
+}
+
+// tS: this tile's score columns (fp32 S in, bf16 P out over its first 64
+// columns); tO: its O accumulator (rescaled in place when the max moves).
+// m, l: running max (log2 units, always integral) and row sum. `diag`: causal
+// diagonal tile (mask key > query, all exps on the MUFU so masked P is 0).
+// `o_live`: O already holds earlier P V products.
+template <int D, int EMU_OF_8>
+__device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t lane_base, int r, float c,
+                                             float& m, float& l, bool diag, bool o_live) {
+  float s[128];
+#pragma unroll
+  for (int c0 = 0; c0 < 128; c0 += 32)
+    tmem_ld32(tmem_addr(tS, lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(&s[c0]));
+  tmem_wait_ld();
+  if (diag) {
+#pragma unroll
+    for (int cc = 0; cc < 128; ++cc)
+      if (cc > r) s[cc] = -INFINITY;  // key > query
+  }
+  // row max: 8 independent 3-input-max chains, then combine
+  float mx8[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) mx8[a] = fmaxf(s[a], s[a + 8]);
+#pragma unroll
+  for (int k = 16; k < 128; k += 16)
+#pragma unroll
+    for (int a = 0; a < 8; ++a) mx8[a] = max3f(mx8[a], s[k + a], s[k + 8 + a]);
+  const float mx = max3f(max3f(mx8[0], mx8[1], mx8[2]), max3f(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
+  const float mxs = mx * c;
+  float m_use = m, alpha = 1.f;
+  if (mxs > m + RESCALE_TH) {  // also taken on the first tile (m = -inf)
+    m_use = ceilf(mxs);        // integral max: exact f in the polynomial exp
+    alpha = ex2(m - m_use);
+  }
+  const float smin = (m_use - 125.f) / c;
+  float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c0 = 0; c0 < 128; c0 += 32) {
+    uint32_t pk[16];
+    if (diag)
+      softmax_chunk32<false, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);
+    else
+      softmax_chunk32<true, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);
+    tmem_st16(tmem_addr(tS, lane_base, c0 / 2), pk);
+  }
+  const float2 rs2 = add2(acc[0], acc[1]);
+  l = l * alpha + (rs2.x + rs2.y);
+  // O holds P(j-1) V_{j-1}, complete: the S barrier tracked every earlier MMA.
+  if (o_live && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      float o[32];
+      tmem_ld32(tmem_addr(tO, lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(o));
+      tmem_wait_ld();
+#pragma unroll
+      for (int cc = 0; cc < 32; cc += 2) {
+        const float2 v = mul2(make_float2(o[cc], o[cc + 1]), make_float2(alpha, alpha));
+        o[cc] = v.x;
+        o[cc + 1] = v.y;
+      }
+      tmem_st32(tmem_addr(tO, lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(o));
+    }
+  }
+  m = m_use;
+}
+
+}  // namespace hk

@@ -12,14 +12,18 @@ from paper_2511_08083_b200 import _lib  # noqa: E402
 L = _lib.lib()
 out = torch.zeros(148, device="cuda")
 res = {}
-names = ["ex2.f32", "cvt.bf16x2.f32", "fma.f32", "max.f32", "ex2.bf16x2", "add.f32"]
+names = ["ex2.f32", "cvt.bf16x2.f32", "fma.f32 (const operands)", "max.f32", "ex2.bf16x2", "add.f32",
+         "fma.f32x2 (pairs, counted per element)", "add.f32x2 (pairs, counted per element)", "max3.f32",
+         "int shift-add", "fma.f32 (3 register operands)"]
 for op, nm in enumerate(names):
     iters = 4096
-    for _ in range(2):
-        _lib.check(L.hk_diag_rates(0, op, iters, ctypes.c_void_p(out.data_ptr()), None))
-    torch.cuda.synchronize()
-    cyc = out.float().mean().item()
-    res[nm + " per clk per SM"] = round(512 * iters * 8 / cyc, 2)
+    for threads, tag in ((512, "16 warps/SM"), (128, "4 warps/SM (1 per SMSP)")):
+        for _ in range(2):
+            _lib.check(L.hk_diag_rates(0, op + (100 if threads == 128 else 0), iters,
+                                       ctypes.c_void_p(out.data_ptr()), None))
+        torch.cuda.synchronize()
+        cyc = out.float().mean().item()
+        res[f"{nm} per clk per SM, {tag}"] = round(threads * iters * 8 / cyc, 2)
 for mode, mn in enumerate(["SS", "TS", "SS_Bmn"]):
     for n in (64, 128, 256):
         for _ in range(2):
@@ -28,4 +32,17 @@ for mode, mn in enumerate(["SS", "TS", "SS_Bmn"]):
         cyc = out.float().mean().item()
         res[f"mma {mn} M=128 N={n} K=16 cycles"] = round(cyc, 2)
         res[f"mma {mn} M=128 N={n} flop/clk/SM"] = round(2 * 128 * n * 16 / cyc, 1)
+for w in (4, 8, 16):
+    iters = 1000
+    for _ in range(2):
+        _lib.check(L.hk_diag_rates(2, w, iters, ctypes.c_void_p(out.data_ptr()), None))
+    torch.cuda.synchronize()
+    cyc = out.float().mean().item()
+    res[f"tcgen05.ld 32x32b {w} warps bytes/clk/SM"] = round(w * 32 * 128 * 4 * iters / cyc, 1)
+for emu in (0, 2, 3, 4, 5):
+    for nwg in (1, 2):
+        for _ in range(2):
+            _lib.check(L.hk_diag_rates(3, 10 * emu + nwg, 200, ctypes.c_void_p(out.data_ptr()), None))
+        torch.cuda.synchronize()
+        res[f"softmax step emu {emu}/8, {nwg} WG: cycles/step"] = round(out.float().mean().item(), 1)
 print(json.dumps(res, indent=1))
