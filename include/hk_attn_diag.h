@@ -22,14 +22,15 @@
  * 148 CTAs x 512 threads x iters x 8 ops; out[cta] = clock64 cycles.
  * kind 2: tcgen05.ld (32x32b.x32) bandwidth with `param` warps x 128 columns.
  * kind 3: forward softmax step, param = 10 * (emulated exps per 8) + warpgroups.
+ * kind 4: TMA load throughput per SM with boxes of `param` rows x 128 B.
  * kind 1: tcgen05.mma pacing, mode = param / 1000 (0 SS, 1 TS, 2 SS with B
  * MN-major), N = param % 1000 in {64,128,256}; out[cta] = cycles per MMA.
  * `out` is a device pointer to >= 148 floats.
  *
- * hk_diag_trace_read: copy the in-kernel event trace of an HK_TRACE build
- * (pairs of u64: event<<48 | a<<32 | b, then clock64) into the host buffer
- * `dst` (capacity `bytes`); returns the number of u64 words via the status
- * HK_OK and writes nothing on non-trace builds (count 0). reset != 0 clears it.
+ * hk_diag_trace_read: copy the in-kernel event table of an HK_TRACE build
+ * (64 events x 1024 slots of u64 clock64, slot = (event, iteration mod 1024),
+ * 0 = not recorded; 512 KiB) into the host buffer `dst` (capacity `bytes`);
+ * zero-fills `dst` on non-trace builds. reset != 0 clears the table.
  */
 #ifndef HK_ATTN_DIAG_H_
 #define HK_ATTN_DIAG_H_

@@ -75,17 +75,25 @@ struct BwdParams {
 
 // 128 x 128 tiles throughout: tcgen05.mma with N=64 paces at 48 cycles per
 // K=16 step instead of 32 (measured, scripts/rates.py), N=128 at full rate.
+// Each per-iteration operand has its own ring, released right after its last
+// MMA, so the next load starts as early as possible (a 64 KB stage needs
+// ~1450 cycles to land).
 template <int D>
 struct BwdCfg {
   static constexpr int PANELS = D / 64;
   static constexpr uint32_t T128 = 128 * D * 2;  // a 128-row [rows][D] bf16 tile
-  static constexpr int NS = (D == 128) ? 2 : 3;  // ring depth
-  // B1: K_j, V_j resident + NS x {Q_i, dO_i, lse2_i, D_i}
-  static constexpr uint32_t STAGE1 = 2 * T128 + 1024;
-  static constexpr uint32_t SMEM1 = 2 * T128 + NS * STAGE1 + 1024;
-  // B2: Q_i, dO_i resident + NS x {K_j, V_j}
-  static constexpr uint32_t STAGE2 = 2 * T128;
-  static constexpr uint32_t SMEM2 = 2 * T128 + NS * STAGE2 + 1024;
+  static constexpr int NSA = (D == 128) ? 3 : 4;  // ring A depth
+  static constexpr int NSB = (D == 128) ? 2 : 4;  // ring B depth
+  // B1: K_j, V_j resident; ring A = {Q_i}, ring B = {dO_i, lse2_i, D_i} (both freed after dK).
+  // At D=128 this is 224 KB + barriers: no room for alignment slack, so the
+  // barriers live at the end of the dynamic region (no static shared memory)
+  // and the kernel checks that the dynamic base is 1024-aligned.
+  static constexpr uint32_t SLOT_B1 = T128 + 1024;
+  static constexpr uint32_t BAR_BYTES = 256;
+  static constexpr uint32_t SLACK1 = (D == 128) ? 0 : 1024;
+  static constexpr uint32_t SMEM1 = 2 * T128 + NSA * T128 + NSB * SLOT_B1 + BAR_BYTES + SLACK1;
+  // B2: Q_i, dO_i resident; ring A = {K_j}, ring B = {V_j}
+  static constexpr uint32_t SMEM2 = 2 * T128 + (NSA + NSB) * T128 + 1024;
   static constexpr int THREADS = 320;  // 8 elementwise warps + TMA warp + MMA warp
 };
 
@@ -101,6 +109,16 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int rows, int kk
 // Packed bf16 operand in TMEM written by two warpgroups: columns 16kk.. of the
 // 128-wide contraction live at packed column kk*8 (kk < 4) or 64 + (kk-4)*8.
 __device__ __forceinline__ uint32_t packed_col(int kk) { return kk < 4 ? kk * 8 : 64 + (kk - 4) * 8; }
+
+// P = 2^x for a pair of backward scores (x = c s - LSE2 <= ~0): BWD_EMU_OF_8
+// of every 8 pairs on the FMA pipe (ex2_poly2), the rest on the MUFU, which
+// otherwise needs 1024 of each block's 1536-2048 tensor cycles.
+constexpr int BWD_EMU_OF_8 = 3;
+template <int EMU_OF_8>
+__device__ __forceinline__ float2 bwd_exp2_pair(float2 x, int k) {
+  if ((k % 8) < EMU_OF_8) return ex2_poly2(x);
+  return make_float2(ex2(x.x), ex2(x.y));
+}
 
 __device__ __forceinline__ void lds_v4(const void* p, float& a, float& b, float& c, float& d) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(smem_u32(p)));
@@ -131,15 +149,27 @@ __global__ void __launch_bounds__(320, 1)
                     const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                     const BwdParams p) {
   using C = BwdCfg<D>;
-  constexpr int NS = C::NS;
+  constexpr int NSA = C::NSA, NSB = C::NSB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if (C::SLACK1 == 0 && smem != smem_raw) __trap();  // the D=128 layout has no alignment slack
   uint8_t* sK = smem;
   uint8_t* sV = smem + C::T128;
-  uint8_t* sStage = smem + 2 * C::T128;  // stage s: Q [T128] dO [T128] lse2 [512 B] D [512 B]
-
-  __shared__ uint64_t bar_kv, bar_full[NS], bar_empty[NS], bar_s, bar_dp, bar_p, bar_ds, bar_acc;
-  __shared__ uint32_t tmem_base_s;
+  uint8_t* sA = smem + 2 * C::T128;   // ring A slot s: Q [T128]
+  uint8_t* sB = sA + NSA * C::T128;   // ring B slot s: dO [T128] lse2 [512 B] D [512 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NSB * C::SLOT_B1);
+  uint64_t* fullA = bars;             // [NSA]
+  uint64_t* emptyA = bars + NSA;      // [NSA]
+  uint64_t* fullB = bars + 2 * NSA;   // [NSB]
+  uint64_t* emptyB = fullB + NSB;     // [NSB]
+  uint64_t& bar_kv = emptyB[NSB];
+  uint64_t& bar_s = emptyB[NSB + 1];
+  uint64_t& bar_dp = emptyB[NSB + 2];
+  uint64_t& bar_p = emptyB[NSB + 3];
+  uint64_t& bar_ds = emptyB[NSB + 4];
+  uint64_t& bar_acc = emptyB[NSB + 5];
+  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(emptyB + NSB + 6);
+  static_assert((2 * NSA + 2 * NSB + 7) * 8 <= C::BAR_BYTES, "barrier area");
 
   const int warp = warp_id(), lane = lane_id();
   const int T = p.N / 128;
@@ -152,9 +182,13 @@ __global__ void __launch_bounds__(320, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&bar_kv, 1);
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&bar_full[s], 1);
-      mbar_init(&bar_empty[s], 1);
+    for (int s = 0; s < NSA; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < NSB; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
     }
     mbar_init(&bar_s, 1);
     mbar_init(&bar_dp, 1);
@@ -186,79 +220,93 @@ __global__ void __launch_bounds__(320, 1)
         tma_load_4d(&mapK, &bar_kv, sK + pn * 128 * 128, pn * 64, kvh, jt * 128, b, pol_stream);
         tma_load_4d(&mapV, &bar_kv, sV + pn * 128 * 128, pn * 64, kvh, jt * 128, b, pol_stream);
       }
-      int h = kvh * G, qi = i0, s = 0;
-      uint32_t ph = 0;
+      // blocking waits (the hardware suspends the warp: no issue slots taken
+      // from the elementwise warps sharing its SM sub-partition)
+      int h = kvh * G, qi = i0;
       for (int it = 0; it < n_it; ++it) {
-        uint8_t* st = sStage + s * C::STAGE1;
-        mbar_wait(&bar_empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&bar_full[s], 2 * C::T128 + 1024);
-        for (int pn = 0; pn < C::PANELS; ++pn) {
-          tma_load_4d(&mapQ, &bar_full[s], st + pn * 128 * 128, pn * 64, h, qi * 128, b, pol_keep);
-          tma_load_4d(&mapdO, &bar_full[s], st + C::T128 + pn * 128 * 128, pn * 64, h, qi * 128, b, pol_keep);
-        }
+        const int sa = it % NSA, sb = it % NSB;
+        mbar_wait(&emptyA[sa], ((it / NSA) & 1) ^ 1);
+        hk_trace(20, it, 0);  // producer: ring A slot free, loads for it issued
+        mbar_arrive_expect_tx(&fullA[sa], C::T128);
+        for (int pn = 0; pn < C::PANELS; ++pn)
+          tma_load_4d(&mapQ, &fullA[sa], sA + sa * C::T128 + pn * 128 * 128, pn * 64, h, qi * 128, b, pol_keep);
+        mbar_wait(&emptyB[sb], ((it / NSB) & 1) ^ 1);
+        uint8_t* st = sB + sb * C::SLOT_B1;
+        mbar_arrive_expect_tx(&fullB[sb], C::T128 + 1024);
+        for (int pn = 0; pn < C::PANELS; ++pn)
+          tma_load_4d(&mapdO, &fullB[sb], st + pn * 128 * 128, pn * 64, h, qi * 128, b, pol_keep);
         const size_t off = ((size_t)b * p.Hq + h) * p.N + (size_t)qi * 128;
-        bulk_load(st + 2 * C::T128, p.lse2 + off, 512, &bar_full[s]);
-        bulk_load(st + 2 * C::T128 + 512, p.Dv + off, 512, &bar_full[s]);
+        bulk_load(st + C::T128, p.lse2 + off, 512, &fullB[sb]);
+        bulk_load(st + C::T128 + 512, p.Dv + off, 512, &fullB[sb]);
         if (++qi == T) {
           qi = i0;
           ++h;
         }
-        if (++s == NS) {
-          s = 0;
-          ph ^= 1;
-        }
       }
     }
   } else if (warp == 9) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
-      constexpr uint32_t idesc_sp = idesc_bf16(128, 128, 0, 0);  // S^T / dP^T: M=128 keys, N=128 queries
-      constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);   // dV / dK: B = dO_i / Q_i MN-major
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-      auto stage_q = [&](int it) { return smem_u32(sStage + (it % NS) * C::STAGE1); };
-      auto issue_s = [&](int it) {
-        const uint32_t q = stage_q(it);
+    // ================= MMA issuer (whole warp, one elected lane issues) =================
+    constexpr uint32_t idesc_sp = idesc_bf16(128, 128, 0, 0);  // S^T / dP^T: M=128 keys, N=128 queries
+    constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);   // dV / dK: B = dO_i / Q_i MN-major
+    constexpr uint64_t KMAJ = sdesc_sw128_const(16, 1024);
+    constexpr uint64_t MNMAJ = sdesc_sw128_const(128 * 128, 1024);
+    const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aA = smem_u32(sA), aB = smem_u32(sB);
+    auto kmaj = [&](uint32_t base, int kk) { return KMAJ | ((base + (kk / 4) * 128 * 128 + (kk % 4) * 32) >> 4); };
+    auto mnmaj = [&](uint32_t base, int kk) { return MNMAJ | ((base + kk * 16 * 128) >> 4); };
+    auto slotQ = [&](int it) { return aA + (it % NSA) * C::T128; };
+    auto slotO = [&](int it) { return aB + (it % NSB) * C::SLOT_B1; };
+    auto issue_s = [&](int it) {
+      const uint32_t q = slotQ(it);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_ss(tS, desc_kmajor(aK, 128, kk), desc_kmajor(q, 128, kk), idesc_sp, kk > 0);
-        tc_commit(&bar_s);
-      };
-      auto issue_dp = [&](int it) {
-        const uint32_t dO = stage_q(it) + C::T128;
+      for (int kk = 0; kk < D / 16; ++kk) umma_ss_w(tS, kmaj(aK, kk), kmaj(q, kk), idesc_sp, kk > 0);
+      tc_commit_w(&bar_s);
+    };
+    auto issue_dp = [&](int it) {
+      hk_trace(14, it, 0);  // MMA: dP^T(it) issue
+      const uint32_t dO = slotO(it);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_ss(tP, desc_kmajor(aV, 128, kk), desc_kmajor(dO, 128, kk), idesc_sp, kk > 0);
-        tc_commit(&bar_dp);
-      };
-      mbar_wait(&bar_kv, 0);
-      mbar_wait(&bar_full[0], 0);
+      for (int kk = 0; kk < D / 16; ++kk) umma_ss_w(tP, kmaj(aV, kk), kmaj(dO, kk), idesc_sp, kk > 0);
+      tc_commit_w(&bar_dp);
+    };
+    mbar_wait(&bar_kv, 0);
+    mbar_wait(&fullA[0], 0);
+    tc_fence_after();
+    issue_s(0);
+    mbar_wait(&fullB[0], 0);
+    tc_fence_after();
+    issue_dp(0);
+    for (int it = 0; it < n_it; ++it) {
+      const uint32_t q = slotQ(it), dO = slotO(it);
+      const uint32_t acc = it > 0 ? 1u : 0u;
+      const bool more = it + 1 < n_it;
+      mbar_wait(&bar_p, it & 1);
       tc_fence_after();
-      issue_s(0);
-      issue_dp(0);
-      for (int it = 0; it < n_it; ++it) {
-        const uint32_t q = stage_q(it), dO = q + C::T128;
-        const uint32_t acc = it > 0 ? 1u : 0u;
-        mbar_wait(&bar_p, it & 1);
-        tc_fence_after();
+      hk_trace(10, it, 0);  // MMA: P^T(it) seen, dV issue
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_ts(tdV, tS + packed_col(kk), desc_mnmajor(dO, 128, kk), idesc_acc, (acc | kk) ? 1u : 0u);
-        const bool more = it + 1 < n_it;
-        if (more) {
-          mbar_wait(&bar_full[(it + 1) % NS], ((it + 1) / NS) & 1);
-          tc_fence_after();
-          issue_s(it + 1);
-        }
-        mbar_wait(&bar_ds, it & 1);
+      for (int kk = 0; kk < 8; ++kk)
+        umma_ts_w(tdV, tS + packed_col(kk), mnmaj(dO, kk), idesc_acc, (acc | kk) ? 1u : 0u);
+      if (more) {
+        mbar_wait(&fullA[(it + 1) % NSA], ((it + 1) / NSA) & 1);
         tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_ts(tdK, tP + packed_col(kk), desc_mnmajor(q, 128, kk), idesc_acc, (acc | kk) ? 1u : 0u);
-        if (it + NS < n_it) tc_commit(&bar_empty[it % NS]);
-        if (more) issue_dp(it + 1);
+        hk_trace(13, it + 1, 0);  // ring A slot it+1 landed, S^T issue
+        issue_s(it + 1);
       }
-      tc_commit(&bar_acc);
+      mbar_wait(&bar_ds, it & 1);
+      tc_fence_after();
+      hk_trace(11, it, 0);  // MMA: dS^T(it) seen, dK issue
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        umma_ts_w(tdK, tP + packed_col(kk), mnmaj(q, kk), idesc_acc, (acc | kk) ? 1u : 0u);
+      // Q(it) (last use dK) and dO/lse2/D(it) (last uses dV, the dS phase): free both
+      if (it + NSA < n_it) tc_commit_w(&emptyA[it % NSA]);
+      if (it + NSB < n_it) tc_commit_w(&emptyB[it % NSB]);
+      if (more) {  // dP^T(it+1) overwrites dS^T(it): after dK(it) in issue order
+        mbar_wait(&fullB[(it + 1) % NSB], ((it + 1) / NSB) & 1);
+        tc_fence_after();
+        issue_dp(it + 1);
+      }
     }
+    tc_commit_w(&bar_acc);
   } else {
     // ================= elementwise warpgroups (warps 0-7) =================
     const int wg = warp >> 2;              // query columns [64 wg, 64 wg + 64) of each block
@@ -269,12 +317,15 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t cS = tS + 64 * wg, cP = tP + 64 * wg;
     int qi = i0, s = 0;
     for (int it = 0; it < n_it; ++it) {
-      const uint8_t* vec = sStage + s * C::STAGE1 + 2 * C::T128;  // lse2 [128], then D [128]
+      const uint8_t* vec = sB + s * C::SLOT_B1 + C::T128;  // lse2 [128], then D [128]
       const uint32_t par = it & 1;
       float v[64];
       // ---- phase 1: P^T = exp2(c S^T - LSE2) (masked), bf16 into TMEM for dV += P^T dO
+      if (threadIdx.x == 0) hk_trace(1, it, 0);
+      mbar_wait(&fullB[s], (it / NSB) & 1);  // lse2/D ride with dO in ring B: landed?
       mbar_wait(&bar_s, par);
       tc_fence_after();
+      if (threadIdx.x == 0) hk_trace(2, it, 0);
       tmem_ld64(tmem_addr(cS, lb, 0), v);
       tmem_wait_ld();
       const int q0 = qi * 128 + 64 * wg;
@@ -282,10 +333,14 @@ __global__ void __launch_bounds__(320, 1)
       for (int c4 = 0; c4 < 64; c4 += 4) {
         float l0, l1, l2, l3;
         lds_v4(vec + 4 * (64 * wg + c4), l0, l1, l2, l3);
-        v[c4 + 0] = ex2(fmaf(v[c4 + 0], c, -l0));
-        v[c4 + 1] = ex2(fmaf(v[c4 + 1], c, -l1));
-        v[c4 + 2] = ex2(fmaf(v[c4 + 2], c, -l2));
-        v[c4 + 3] = ex2(fmaf(v[c4 + 3], c, -l3));
+        const float2 xa = fma2(make_float2(v[c4], v[c4 + 1]), make_float2(c, c), make_float2(-l0, -l1));
+        const float2 xb = fma2(make_float2(v[c4 + 2], v[c4 + 3]), make_float2(c, c), make_float2(-l2, -l3));
+        const float2 ea = bwd_exp2_pair<BWD_EMU_OF_8>(xa, c4 / 2);
+        const float2 eb = bwd_exp2_pair<BWD_EMU_OF_8>(xb, c4 / 2 + 1);
+        v[c4] = ea.x;
+        v[c4 + 1] = ea.y;
+        v[c4 + 2] = eb.x;
+        v[c4 + 3] = eb.y;
       }
       if (CAUSAL && qi == jt) {
 #pragma unroll
@@ -297,9 +352,11 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_p);
+      if (threadIdx.x == 0) hk_trace(3, it, 0);
       // ---- phase 2: dS^T = P^T (dP^T - D), bf16 into TMEM for dK += dS^T Q
       mbar_wait(&bar_dp, par);
       tc_fence_after();
+      if (threadIdx.x == 0) hk_trace(4, it, 0);
       float dp[64];
       tmem_ld64(tmem_addr(cP, lb, 0), dp);
       tmem_wait_ld();
@@ -317,8 +374,9 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_ds);
+      if (threadIdx.x == 0) hk_trace(5, it, 0);
       if (++qi == T) qi = i0;
-      if (++s == NS) s = 0;
+      if (++s == NSB) s = 0;
     }
     // ---- epilogue: WG0 writes dV, WG1 writes dK * (1/sqrt d)
     mbar_wait(&bar_acc, 0);
@@ -356,14 +414,15 @@ __global__ void __launch_bounds__(320, 1)
                   const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                   const BwdParams p) {
   using C = BwdCfg<D>;
-  constexpr int NS = C::NS;
+  constexpr int NSA = C::NSA, NSB = C::NSB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sdO = smem + C::T128;
-  uint8_t* sStage = smem + 2 * C::T128;  // stage s: K_j [T128] V_j [T128]
+  uint8_t* sA = smem + 2 * C::T128;   // ring A slot s: K_j [T128]
+  uint8_t* sB = sA + NSA * C::T128;   // ring B slot s: V_j [T128]
 
-  __shared__ uint64_t bar_q, bar_full[NS], bar_empty[NS], bar_s[2], bar_dp, bar_ds, bar_acc;
+  __shared__ uint64_t bar_q, fullA[NSA], emptyA[NSA], fullB[NSB], emptyB[NSB], bar_s[2], bar_dp, bar_ds, bar_acc;
   __shared__ uint32_t tmem_base_s;
 
   const int warp = warp_id(), lane = lane_id();
@@ -375,9 +434,13 @@ __global__ void __launch_bounds__(320, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&bar_q, 1);
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&bar_full[s], 1);
-      mbar_init(&bar_empty[s], 1);
+    for (int s = 0; s < NSA; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < NSB; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
     }
     mbar_init(&bar_s[0], 1);
     mbar_init(&bar_s[1], 1);
@@ -408,66 +471,83 @@ __global__ void __launch_bounds__(320, 1)
         tma_load_4d(&mapQ, &bar_q, sQ + pn * 128 * 128, pn * 64, h, iq * 128, b, pol_stream);
         tma_load_4d(&mapdO, &bar_q, sdO + pn * 128 * 128, pn * 64, h, iq * 128, b, pol_stream);
       }
-      int s = 0;
-      uint32_t ph = 0;
+      // K (ring A, freed after dQ) for block it+1 goes out right after V (ring B,
+      // freed after dP) for block it, keeping K one block ahead.
+      mbar_arrive_expect_tx(&fullA[0], C::T128);
+      for (int pn = 0; pn < C::PANELS; ++pn)
+        tma_load_4d(&mapK, &fullA[0], sA + pn * 128 * 128, pn * 64, kvh, 0, b, pol_keep);
       for (int it = 0; it < n_it; ++it) {
-        uint8_t* st = sStage + s * C::STAGE2;
-        mbar_wait(&bar_empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&bar_full[s], 2 * C::T128);
-        for (int pn = 0; pn < C::PANELS; ++pn) {
-          tma_load_4d(&mapK, &bar_full[s], st + pn * 128 * 128, pn * 64, kvh, it * 128, b, pol_keep);
-          tma_load_4d(&mapV, &bar_full[s], st + C::T128 + pn * 128 * 128, pn * 64, kvh, it * 128, b, pol_keep);
-        }
-        if (++s == NS) {
-          s = 0;
-          ph ^= 1;
+        const int sb = it % NSB;
+        mbar_wait(&emptyB[sb], ((it / NSB) & 1) ^ 1);
+        mbar_arrive_expect_tx(&fullB[sb], C::T128);
+        for (int pn = 0; pn < C::PANELS; ++pn)
+          tma_load_4d(&mapV, &fullB[sb], sB + sb * C::T128 + pn * 128 * 128, pn * 64, kvh, it * 128, b, pol_keep);
+        if (it + 1 < n_it) {
+          const int sa = (it + 1) % NSA;
+          mbar_wait(&emptyA[sa], (((it + 1) / NSA) & 1) ^ 1);
+          mbar_arrive_expect_tx(&fullA[sa], C::T128);
+          for (int pn = 0; pn < C::PANELS; ++pn)
+            tma_load_4d(&mapK, &fullA[sa], sA + sa * C::T128 + pn * 128 * 128, pn * 64, kvh, (it + 1) * 128, b,
+                        pol_keep);
         }
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_sp = idesc_bf16(128, 128, 0, 0);  // S / dP: M=128 queries, N=128 keys
-      constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);   // dQ += dS K_j: K_j MN-major
-      const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO);
-      auto stage_k = [&](int it) { return smem_u32(sStage + (it % NS) * C::STAGE2); };
-      auto issue_s = [&](int it) {
-        const uint32_t k = stage_k(it);
-        const uint32_t t = tS0 + 128 * (it & 1);
+    // ================= MMA issuer (whole warp, one elected lane issues) =================
+    constexpr uint32_t idesc_sp = idesc_bf16(128, 128, 0, 0);  // S / dP: M=128 queries, N=128 keys
+    constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);   // dQ += dS K_j: K_j MN-major
+    constexpr uint64_t KMAJ = sdesc_sw128_const(16, 1024);
+    constexpr uint64_t MNMAJ = sdesc_sw128_const(128 * 128, 1024);
+    const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), aA = smem_u32(sA), aB = smem_u32(sB);
+    auto kmaj = [&](uint32_t base, int kk) { return KMAJ | ((base + (kk / 4) * 128 * 128 + (kk % 4) * 32) >> 4); };
+    auto mnmaj = [&](uint32_t base, int kk) { return MNMAJ | ((base + kk * 16 * 128) >> 4); };
+    auto slotK = [&](int it) { return aA + (it % NSA) * C::T128; };
+    auto slotV = [&](int it) { return aB + (it % NSB) * C::T128; };
+    auto issue_s = [&](int it) {
+      const uint32_t k = slotK(it);
+      const uint32_t t = tS0 + 128 * (it & 1);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_ss(t, desc_kmajor(aQ, 128, kk), desc_kmajor(k, 128, kk), idesc_sp, kk > 0);
-        tc_commit(&bar_s[it & 1]);
-      };
-      auto issue_dp = [&](int it) {
-        const uint32_t v = stage_k(it) + C::T128;
+      for (int kk = 0; kk < D / 16; ++kk) umma_ss_w(t, kmaj(aQ, kk), kmaj(k, kk), idesc_sp, kk > 0);
+      tc_commit_w(&bar_s[it & 1]);
+    };
+    auto issue_dp = [&](int it) {
+      const uint32_t v = slotV(it);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_ss(tP, desc_kmajor(adO, 128, kk), desc_kmajor(v, 128, kk), idesc_sp, kk > 0);
-        tc_commit(&bar_dp);
-      };
-      mbar_wait(&bar_q, 0);
-      mbar_wait(&bar_full[0], 0);
-      tc_fence_after();
-      issue_s(0);
-      issue_dp(0);
-      for (int it = 0; it < n_it; ++it) {
-        const bool more = it + 1 < n_it;
-        if (more) {
-          mbar_wait(&bar_full[(it + 1) % NS], ((it + 1) / NS) & 1);
-          tc_fence_after();
-          issue_s(it + 1);
-        }
-        mbar_wait(&bar_ds, it & 1);
+      for (int kk = 0; kk < D / 16; ++kk) umma_ss_w(tP, kmaj(adO, kk), kmaj(v, kk), idesc_sp, kk > 0);
+      tc_commit_w(&bar_dp);
+      if (it + NSB < n_it) tc_commit_w(&emptyB[it % NSB]);  // V(it): dP(it) is its only use
+    };
+    mbar_wait(&bar_q, 0);
+    mbar_wait(&fullA[0], 0);
+    tc_fence_after();
+    issue_s(0);
+    mbar_wait(&fullB[0], 0);
+    tc_fence_after();
+    issue_dp(0);
+    for (int it = 0; it < n_it; ++it) {
+      const bool more = it + 1 < n_it;
+      if (more) {
+        mbar_wait(&fullA[(it + 1) % NSA], ((it + 1) / NSA) & 1);
         tc_fence_after();
-        const uint32_t k = stage_k(it);
+        issue_s(it + 1);
+      }
+      mbar_wait(&bar_ds, it & 1);
+      tc_fence_after();
+      hk_trace(11, it, 1);  // MMA: dS(it) seen, dQ issue
+      {
+        const uint32_t k = slotK(it);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_ts(tdQ, tP + packed_col(kk), desc_mnmajor(k, 128, kk), idesc_acc, (it > 0 || kk > 0) ? 1u : 0u);
-        if (it + NS < n_it) tc_commit(&bar_empty[it % NS]);
-        if (more) issue_dp(it + 1);
+          umma_ts_w(tdQ, tP + packed_col(kk), mnmaj(k, kk), idesc_acc, (it > 0 || kk > 0) ? 1u : 0u);
       }
-      tc_commit(&bar_acc);
+      if (it + NSA < n_it) tc_commit_w(&emptyA[it % NSA]);  // K(it): last use dQ(it)
+      if (more) {  // dP(it+1) overwrites dS(it): after dQ(it) in issue order
+        mbar_wait(&fullB[(it + 1) % NSB], ((it + 1) / NSB) & 1);
+        tc_fence_after();
+        issue_dp(it + 1);
+      }
     }
+    tc_commit_w(&bar_acc);
   } else {
     const int wg = warp >> 2;              // key columns [64 wg, 64 wg + 64) of each block
     const uint32_t lb = (warp & 3) * 32;
@@ -480,20 +560,29 @@ __global__ void __launch_bounds__(320, 1)
     for (int it = 0; it < n_it; ++it) {
       const uint32_t cS = tS0 + 128 * (it & 1) + 64 * wg;
       float v[64];
+      if (threadIdx.x == 0) hk_trace(1, it, 1);
       mbar_wait(&bar_s[it & 1], (it >> 1) & 1);
       tc_fence_after();
+      if (threadIdx.x == 0) hk_trace(2, it, 1);
       tmem_ld64(tmem_addr(cS, lb, 0), v);
       tmem_wait_ld();
 #pragma unroll
-      for (int cc = 0; cc < 64; ++cc) v[cc] = ex2(fmaf(v[cc], c, -l2));
+      for (int k = 0; k < 32; ++k) {
+        const float2 e = bwd_exp2_pair<BWD_EMU_OF_8>(
+            fma2(make_float2(v[2 * k], v[2 * k + 1]), make_float2(c, c), make_float2(-l2, -l2)), k);
+        v[2 * k] = e.x;
+        v[2 * k + 1] = e.y;
+      }
       if (CAUSAL && it == iq) {
         const int k0 = it * 128 + 64 * wg;
 #pragma unroll
         for (int cc = 0; cc < 64; ++cc)
           if (k0 + cc > q) v[cc] = 0.f;
       }
+      if (threadIdx.x == 0) hk_trace(3, it, 1);
       mbar_wait(&bar_dp, it & 1);
       tc_fence_after();
+      if (threadIdx.x == 0) hk_trace(4, it, 1);
       float dp[64];
       tmem_ld64(tmem_addr(cP, lb, 0), dp);
       tmem_wait_ld();
@@ -504,6 +593,7 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_ds);
+      if (threadIdx.x == 0) hk_trace(5, it, 1);
     }
     // ---- epilogue: dQ * (1/sqrt d); WG0 writes columns [0, D/2), WG1 [D/2, D)
     mbar_wait(&bar_acc, 0);

@@ -134,34 +134,37 @@ __global__ void __launch_bounds__(384, 1)
           ph ^= 1;
         }
       }
-    } else if (warp == 9 && lane == 0) {
-      // ================= MMA issuer =================
+    } else if (warp == 9) {
+      // ================= MMA issuer (whole warp, one elected lane issues) =================
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);  // S = Q K^T: A K-major, B K-major
       constexpr uint32_t idesc_o = idesc_bf16(128, D, 0, 1);    // O += P V: A TMEM, B (V) MN-major
+      constexpr uint64_t KMAJ = sdesc_sw128_const(16, 1024);
+      constexpr uint64_t VMN = sdesc_sw128_const(128 * 128, 1024);
+      const uint64_t dq0 = KMAJ | (smem_u32(sQ) >> 4);
+      const uint64_t dk0 = KMAJ | (smem_u32(sK) >> 4);
+      const uint64_t dv0 = VMN | (smem_u32(sV) >> 4);
       auto issue_s = [&](int t, int s) {
-        const uint32_t qa = smem_u32(sQ + t * TB);
-        const uint32_t ka = smem_u32(sK + s * TB);
+        const uint64_t qd = dq0 + ((t * TB) >> 4), kd = dk0 + ((s * TB) >> 4);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk / 4) * 128 * 128 + (kk % 4) * 32;
-          umma_ss(tbase + 128 * t, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(ka + off, 16, 1024), idesc_s,
-                  kk > 0);
+          const uint32_t off = ((kk / 4) * 128 * 128 + (kk % 4) * 32) >> 4;
+          umma_ss_w(tbase + 128 * t, qd + off, kd + off, idesc_s, kk > 0);
         }
-        tc_commit(&bar_s[t]);
+        tc_commit_w(&bar_s[t]);
       };
       auto issue_pv = [&](int t, int s, int j) {
-        const uint32_t va = smem_u32(sV + s * TB);
+        const uint64_t vd = dv0 + ((s * TB) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
-          umma_ts(tbase + 256 + D * t, tbase + 128 * t + kk * 8, sdesc_sw128(va + kk * 16 * 128, 128 * 128, 1024),
-                  idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_ts_w(tbase + 256 + D * t, tbase + 128 * t + kk * 8, vd + ((kk * 16 * 128) >> 4), idesc_o,
+                    (j > 0 || kk > 0) ? 1u : 0u);
       };
       mbar_wait(&bar_q, 0);
       mbar_wait(&bar_kfull[0], 0);
       tc_fence_after();
       issue_s(0, 0);
       if (nkv1 > 0) issue_s(1, 0);
-      tc_commit(&bar_kempty[0]);
+      tc_commit_w(&bar_kempty[0]);
       int s = 0;
       uint32_t ph = 0;
       for (int j = 0; j < nkv; ++j) {
@@ -185,12 +188,12 @@ __global__ void __launch_bounds__(384, 1)
               }
               issue_s(t, s1);
             } else {
-              tc_commit(&bar_o[t]);
+              tc_commit_w(&bar_o[t]);
             }
           }
         }
-        if (j + 1 < nkv) tc_commit(&bar_vempty[s]);
-        if (k_next_waited) tc_commit(&bar_kempty[s1]);
+        if (j + 1 < nkv) tc_commit_w(&bar_vempty[s]);
+        if (k_next_waited) tc_commit_w(&bar_kempty[s1]);
         s = s1;
         ph = ph1;
       }
@@ -210,17 +213,17 @@ __global__ void __launch_bounds__(384, 1)
       float m = -INFINITY;  // running max, log2-scaled units
       float l = 0.f;        // running row sum
       for (int j = 0; j < nk; ++j) {
-        if (threadIdx.x % 128 == 0) hk_trace(1, t, j);  // softmax: start waiting for S_t(j)
+        if (threadIdx.x % 128 == 0) hk_trace(1 + 4 * t, j, 0);  // softmax: start waiting for S_t(j)
         mbar_wait(&bar_s[t], j & 1);
         tc_fence_after();
-        if (threadIdx.x % 128 == 0) hk_trace(2, t, j);  // S_t(j) ready
+        if (threadIdx.x % 128 == 0) hk_trace(2 + 4 * t, j, 0);  // S_t(j) ready
         const bool diag = CAUSAL && j == qt;
         softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, diag, j > 0);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_p[t]);
-        if (threadIdx.x % 128 == 0) hk_trace(3, t, j);  // P_t(j) published
+        if (threadIdx.x % 128 == 0) hk_trace(3 + 4 * t, j, 0);  // P_t(j) published
       }
       // ---- epilogue: O = O_acc / l (bf16), LSE = (m + log2 l) ln 2
       mbar_wait(&bar_o[t], 0);

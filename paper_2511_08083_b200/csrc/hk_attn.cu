@@ -267,6 +267,24 @@ hk_status hk_diag_rates(int kind, int param, int iters, float* out, cudaStream_t
     hk::tmem_ld_rate_kernel<128><<<148, 32 * param, 0, stream>>>(iters, out, sink);
     return launched("hk_diag_rates");
   }
+  if (kind == 4) {  // TMA throughput: param = rows per box (64, 128 or 256); 64 MB source buffer
+    static void* src = nullptr;
+    const int total_rows = 64 * 1024 * 1024 / 128;
+    if (!src && cudaMalloc(&src, (size_t)total_rows * 128) != cudaSuccess) return fail(HK_ERR_DEVICE, "cudaMalloc");
+    CUtensorMap m;
+    if (!hk::encode_bnhd(&m, src, 1, total_rows, 1, 64, param)) return fail(HK_ERR_DEVICE, "encode");
+    const uint32_t smem = 8 * param * 128 + 1024;
+#define HK_TMA_RATE(R)                                                        \
+  if (param == R) {                                                           \
+    auto* fn = hk::tma_rate_kernel<R>;                                        \
+    if ((s = ensure_smem(fn, smem)) != HK_OK) return s;                       \
+    fn<<<148, 64, smem, stream>>>(m, iters, total_rows, out);                 \
+    return launched("hk_diag_rates");                                         \
+  }
+    HK_TMA_RATE(64) HK_TMA_RATE(128) HK_TMA_RATE(256)
+#undef HK_TMA_RATE
+    return fail(HK_ERR_UNSUPPORTED, "rows must be 64, 128 or 256");
+  }
   if (kind == 3) {  // softmax step: param = 10 * EMU_OF_8 + warpgroups (1 or 2)
     const int nwg = param % 10, emu = param / 10;
     if (nwg < 1 || nwg > 2) return fail(HK_ERR_UNSUPPORTED, "1 or 2 warpgroups");
@@ -298,25 +316,16 @@ hk_status hk_diag_rates(int kind, int param, int iters, float* out, cudaStream_t
 hk_status hk_diag_trace_read(void* dst, size_t bytes, int reset) {
   g_err[0] = 0;
 #ifdef HK_TRACE
-  unsigned n = 0;
-  if (cudaMemcpyFromSymbol(&n, hk::g_hk_trace_n, sizeof(n)) != cudaSuccess)
-    return fail(HK_ERR_DEVICE, "trace count read failed");
-  if (n > (1u << 16)) n = 1u << 16;
-  size_t want = (size_t)n * 8;
-  if (dst && bytes >= 8) {
-    if (want > bytes - 8) want = (bytes - 8) / 8 * 8;
-    unsigned long long cnt = want / 8;
-    memcpy(dst, &cnt, 8);
-    if (want && cudaMemcpyFromSymbol(static_cast<char*>(dst) + 8, hk::g_hk_trace, want) != cudaSuccess)
-      return fail(HK_ERR_DEVICE, "trace read failed");
-  }
-  if (reset) {
-    unsigned z = 0;
-    cudaMemcpyToSymbol(hk::g_hk_trace_n, &z, sizeof(z));
+  const size_t n = 64 * 1024 * sizeof(unsigned long long);
+  if (dst && bytes >= n && cudaMemcpyFromSymbol(dst, hk::g_hk_trace, n) != cudaSuccess)
+    return fail(HK_ERR_DEVICE, "trace read failed");
+  if (reset && cudaMemset(nullptr, 0, 0) == cudaSuccess) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, hk::g_hk_trace) == cudaSuccess) cudaMemset(p, 0, n);
   }
 #else
   (void)reset;
-  if (dst && bytes >= 8) memset(dst, 0, 8);
+  if (dst && bytes) memset(dst, 0, bytes);
 #endif
   return HK_OK;
 }

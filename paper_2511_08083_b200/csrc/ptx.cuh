@@ -27,21 +27,16 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 // ------------------------------------------------------------------ tracing (HK_TRACE builds only)
-// hk_trace(ev, a, b): record (event, a, b, clock64) from one traced CTA into
-// a device ring read back by hk_diag_trace_read (include/hk_attn_diag.h).
+// hk_trace(ev, a, b): one traced CTA stores clock64 at slot (ev, a mod 1024)
+// of a device table (a plain store: no atomics on the hot path) read back by
+// hk_diag_trace_read (include/hk_attn_diag.h). `b` is unused (kept for call sites).
 #ifdef HK_TRACE
-__device__ unsigned long long g_hk_trace[1 << 16];
-__device__ unsigned int g_hk_trace_n;
+__device__ unsigned long long g_hk_trace[64 * 1024];
 __device__ __forceinline__ bool hk_trace_cta() {
   return blockIdx.x == gridDim.x / 2 && blockIdx.y == 0 && blockIdx.z == 0;
 }
-__device__ __forceinline__ void hk_trace(uint32_t ev, uint32_t a, uint32_t b) {
-  if (!hk_trace_cta()) return;
-  const unsigned i = atomicAdd(&g_hk_trace_n, 2u);
-  if (i + 1 < (1u << 16)) {
-    g_hk_trace[i] = ((unsigned long long)ev << 48) | ((unsigned long long)(a & 0xFFFF) << 32) | (b & 0xFFFFFFFFu);
-    g_hk_trace[i + 1] = (unsigned long long)clock64();
-  }
+__device__ __forceinline__ void hk_trace(uint32_t ev, uint32_t a, uint32_t) {
+  if (hk_trace_cta()) g_hk_trace[(ev & 63) * 1024 + (a & 1023)] = (unsigned long long)clock64();
 }
 #else
 __device__ __forceinline__ void hk_trace(uint32_t, uint32_t, uint32_t) {}
@@ -92,6 +87,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 #endif
+
+// Non-blocking probe of a phase (all lanes of a converged warp call it; the
+// result is OR-ed across the warp so the warp never diverges on it).
+__device__ __forceinline__ bool mbar_test_warp(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return __any_sync(0xffffffffu, ok != 0);
+}
+
+// Non-blocking probe from a single thread.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
@@ -258,6 +280,14 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
   return d;
 }
 
+// Constant part of a SWIZZLE_128B descriptor (LBO, SBO, version, layout); OR in
+// (smem address >> 4) for the start field. Shared-memory addresses are < 2^18,
+// so adding byte offsets >> 4 to a descriptor never carries out of the field.
+__host__ __device__ constexpr uint64_t sdesc_sw128_const(uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  return ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) | ((uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
 // D[tmem] (+)= A[smem] * B[smem]
 __device__ __forceinline__ void umma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                         uint32_t accumulate) {
@@ -278,7 +308,36 @@ __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-
+// Warp-collective forms: called by all 32 lanes of a converged warp with
+// warp-uniform operands (kept in uniform registers); one elected lane issues.
+__device__ __forceinline__ void umma_ss_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 
 // ------------------------------------------------------------------ packed fp32x2 (sm_100 FFMA2/FADD2/FMUL2)
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {

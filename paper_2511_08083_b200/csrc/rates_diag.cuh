@@ -179,4 +179,46 @@ __global__ void softmax_rate_kernel(int iters, float* out_cycles, float* sink) {
   if (warp_id() == 0) tmem_dealloc<512>(tbase_s);
 }
 
+// TMA load throughput: one CTA per SM, one thread streams `iters` boxes of
+// 64 x ROWS bf16 (ROWS x 128 B) through an 8-slot ring from an L2-resident
+// [rows][64] tensor; a consumer warp frees each slot when it lands.
+// out[cta] = cycles.
+template <int ROWS>
+__global__ void __launch_bounds__(64, 1) tma_rate_kernel(const __grid_constant__ CUtensorMap map, int iters,
+                                                          int total_rows, float* out_cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int SLOTS = 8;
+  constexpr uint32_t BYTES = ROWS * 128;
+  __shared__ uint64_t full[SLOTS], empty[SLOTS];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < SLOTS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  if (threadIdx.x == 0) {
+    const uint64_t pol = policy_evict_last();
+    for (int it = 0; it < iters; ++it) {
+      const int s = it % SLOTS;
+      mbar_wait(&empty[s], ((it / SLOTS) & 1) ^ 1);
+      mbar_arrive_expect_tx(&full[s], BYTES);
+      const int row = ((blockIdx.x * 7 + it) * ROWS) % total_rows;
+      tma_load_4d(&map, &full[s], smem + s * BYTES, 0, 0, row, 0, pol);
+    }
+  } else if (threadIdx.x == 32) {
+    for (int it = 0; it < iters; ++it) {
+      const int s = it % SLOTS;
+      mbar_wait(&full[s], (it / SLOTS) & 1);
+      mbar_arrive(&empty[s]);
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) out_cycles[blockIdx.x] = (float)(t1 - t0);
+}
+
 }  // namespace hk

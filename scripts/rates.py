@@ -45,4 +45,11 @@ for emu in (0, 2, 3, 4, 5):
             _lib.check(L.hk_diag_rates(3, 10 * emu + nwg, 200, ctypes.c_void_p(out.data_ptr()), None))
         torch.cuda.synchronize()
         res[f"softmax step emu {emu}/8, {nwg} WG: cycles/step"] = round(out.float().mean().item(), 1)
+for rows in (64, 128):
+    iters = 2000
+    for _ in range(2):
+        _lib.check(L.hk_diag_rates(4, rows, iters, ctypes.c_void_p(out.data_ptr()), None))
+    torch.cuda.synchronize()
+    cyc = out.float().mean().item()
+    res[f"TMA load {rows * 128 // 1024} KB boxes, 148 SMs, bytes/clk/SM"] = round(rows * 128 * iters / cyc, 1)
 print(json.dumps(res, indent=1))

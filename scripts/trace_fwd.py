@@ -23,29 +23,26 @@ x = make_inputs(B, N, Hq, Hkv, d, seed=0, device="cuda")
 L = _lib.lib()
 attn_fwd(x["Q"], x["K"], x["V"], causal)
 torch.cuda.synchronize()
-buf = np.zeros(1 << 17, dtype=np.uint64)
+buf = np.zeros(64 * 1024, dtype=np.uint64)
 L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1)
 attn_fwd(x["Q"], x["K"], x["V"], causal)
 torch.cuda.synchronize()
 _lib.check(L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1))
-n = int(buf[0])
-w = buf[1:1 + n].reshape(-1, 2)
-ev = {}
-for hdr, clk in w:
-    e, a, b = int(hdr) >> 48, (int(hdr) >> 32) & 0xFFFF, int(hdr) & 0xFFFFFFFF
-    ev[(e, a, b)] = int(clk)
-t0 = min(ev.values())
+tab = buf.reshape(64, 1024)
+ev = {(e, a): int(tab[e, a]) for e in range(64) for a in range(1024) if tab[e, a]}
 res = {}
+f = lambda v: round(st.median(v), 1) if v else None
 for t in (0, 1):
-    js = sorted(b for (e, a, b) in ev if e == 2 and a == t)
+    js = sorted(a for (e, a) in ev if e == 2 + 4 * t)
     if not js:
         continue
-    wait = [ev[(2, t, j)] - ev[(1, t, j)] for j in js if (1, t, j) in ev]
-    X = [ev[(3, t, j)] - ev[(2, t, j)] for j in js if (3, t, j) in ev]
-    chain = [ev[(2, t, j + 1)] - ev[(3, t, j)] for j in js if (2, t, j + 1) in ev and (3, t, j) in ev]
-    lag = [ev[(10 + t, j, 0)] - ev[(3, t, j)] for j in js if (10 + t, j, 0) in ev and (3, t, j) in ev]
-    period = [ev[(2, t, j + 1)] - ev[(2, t, j)] for j in js if (2, t, j + 1) in ev]
-    f = lambda v: round(st.median(v), 1) if v else None
+    E = lambda k, j: ev.get((k + 4 * t, j))
+    d = lambda a, b: [b_ - a_ for a_, b_ in zip(a, b) if a_ and b_]
+    wait = d([E(1, j) for j in js], [E(2, j) for j in js])
+    X = d([E(2, j) for j in js], [E(3, j) for j in js])
+    chain = d([E(3, j) for j in js], [E(2, j + 1) for j in js])
+    lag = d([E(3, j) for j in js], [ev.get((10 + t, j)) for j in js])
+    period = d([E(2, j) for j in js], [E(2, j + 1) for j in js])
     res[f"tile{t}"] = {"n": len(js), "wait_for_S": f(wait), "softmax_X": f(X), "P_to_nextS": f(chain),
                        "mma_lag_after_P": f(lag), "period": f(period)}
 print(json.dumps(res, indent=1))
