@@ -23,6 +23,7 @@
  * kind 2: tcgen05.ld (32x32b.x32) bandwidth with `param` warps x 128 columns.
  * kind 3: forward softmax step, param = 10 * (emulated exps per 8) + warpgroups.
  * kind 4: TMA load throughput per SM with boxes of `param` rows x 128 B.
+ * kind 5: fp32 red.global.add.v4 throughput into a `param` x 64 KB region.
  * kind 1: tcgen05.mma pacing, mode = param / 1000 (0 SS, 1 TS, 2 SS with B
  * MN-major), N = param % 1000 in {64,128,256}; out[cta] = cycles per MMA.
  * `out` is a device pointer to >= 148 floats.

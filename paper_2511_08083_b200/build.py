@@ -37,6 +37,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False, trace
         return LIB
     tmp = lib + ".tmp"
     extra = (["-DHK_DEBUG_HANG"] if debug else []) + (["-DHK_TRACE"] if trace else [])
+    extra += os.environ.get("HK_EXTRA", "").split()  # e.g. tuning -D flags
     cmd = [NVCC, *FLAGS, *extra, "-o", tmp, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -45,7 +45,13 @@ struct FwdCfg {
   static constexpr int NS = (D == 128) ? 2 : 4;        // K/V ring depth
   static constexpr uint32_t SMEM = 2 * TILE_BYTES + 2 * NS * TILE_BYTES + 1024;
   static constexpr int THREADS = 384;
-  static constexpr int EMU_OF_8 = (D == 128) ? 3 : 4;  // exps per 8 on the FMA pipe
+#ifndef HK_FWD_EMU128
+#define HK_FWD_EMU128 3
+#endif
+#ifndef HK_FWD_EMU64
+#define HK_FWD_EMU64 3
+#endif
+  static constexpr int EMU_OF_8 = (D == 128) ? HK_FWD_EMU128 : HK_FWD_EMU64;  // exps per 8 on the FMA pipe
 };
 
 template <int D, bool CAUSAL>

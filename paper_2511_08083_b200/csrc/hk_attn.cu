@@ -267,6 +267,18 @@ hk_status hk_diag_rates(int kind, int param, int iters, float* out, cudaStream_t
     hk::tmem_ld_rate_kernel<128><<<148, 32 * param, 0, stream>>>(iters, out, sink);
     return launched("hk_diag_rates");
   }
+  if (kind == 5) {  // L2 fp32 reduce-add: param = region size in 64 KB tiles
+    static float* dst = nullptr;
+    static int have = 0;
+    if (have < param) {
+      if (dst) cudaFree(dst);
+      if (cudaMalloc(&dst, (size_t)param * 65536) != cudaSuccess) return fail(HK_ERR_DEVICE, "cudaMalloc");
+      cudaMemset(dst, 0, (size_t)param * 65536);
+      have = param;
+    }
+    hk::red_rate_kernel<<<148, 256, 0, stream>>>(dst, param, iters, out);
+    return launched("hk_diag_rates");
+  }
   if (kind == 4) {  // TMA throughput: param = rows per box (64, 128 or 256); 64 MB source buffer
     static void* src = nullptr;
     const int total_rows = 64 * 1024 * 1024 / 128;

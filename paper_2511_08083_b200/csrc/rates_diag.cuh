@@ -221,4 +221,26 @@ __global__ void __launch_bounds__(64, 1) tma_rate_kernel(const __grid_constant__
   if (threadIdx.x == 0) out_cycles[blockIdx.x] = (float)(t1 - t0);
 }
 
+// fp32 reduce-add throughput into L2: each CTA adds `iters` 128x128 fp32 tiles
+// (64 KB, rows of 512 B like a dQ accumulator row) into a `tiles`-tile region
+// with red.global.add.v4.f32; out[cta] = cycles.
+__global__ void __launch_bounds__(256) red_rate_kernel(float* dst, int tiles, int iters, float* out_cycles) {
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    float* tile = dst + (size_t)((blockIdx.x * 7 + it * 13) % tiles) * 128 * 128;
+    // thread t: row t/2, half (t%2) of the row: 64 floats = 16 x v4
+    float* rowp = tile + (threadIdx.x / 2) * 128 + (threadIdx.x % 2) * 64;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float v = 1e-3f * (k + 1);
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(rowp + 4 * k), "f"(v), "f"(v), "f"(v),
+                   "f"(v)
+                   : "memory");
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) out_cycles[blockIdx.x] = (float)(t1 - t0);
+}
+
 }  // namespace hk

@@ -52,4 +52,11 @@ for rows in (64, 128):
     torch.cuda.synchronize()
     cyc = out.float().mean().item()
     res[f"TMA load {rows * 128 // 1024} KB boxes, 148 SMs, bytes/clk/SM"] = round(rows * 128 * iters / cyc, 1)
+for tiles in (256, 4096):
+    iters = 200
+    for _ in range(2):
+        _lib.check(L.hk_diag_rates(5, tiles, iters, ctypes.c_void_p(out.data_ptr()), None))
+    torch.cuda.synchronize()
+    cyc = out.float().max().item()
+    res[f"red.add.v4.f32 64KB tiles into {tiles * 64 // 1024} MB, bytes/clk chip"] = round(148 * 65536 * iters / cyc, 1)
 print(json.dumps(res, indent=1))

@@ -32,7 +32,7 @@ tab = buf.reshape(64, 1024)
 ev = {(e, a): int(tab[e, a]) for e in range(64) for a in range(1024) if tab[e, a]}
 res = {}
 f = lambda v: round(st.median(v), 1) if v else None
-for t in (0, 1):
+for t in (0, 1):  # t = softmax warpgroup (column half)
     js = sorted(a for (e, a) in ev if e == 2 + 4 * t)
     if not js:
         continue
@@ -41,7 +41,7 @@ for t in (0, 1):
     wait = d([E(1, j) for j in js], [E(2, j) for j in js])
     X = d([E(2, j) for j in js], [E(3, j) for j in js])
     chain = d([E(3, j) for j in js], [E(2, j + 1) for j in js])
-    lag = d([E(3, j) for j in js], [ev.get((10 + t, j)) for j in js])
+    lag = d([E(3, j) for j in js], [ev.get((10, j)) for j in js])
     period = d([E(2, j) for j in js], [E(2, j + 1) for j in js])
     res[f"tile{t}"] = {"n": len(js), "wait_for_S": f(wait), "softmax_X": f(X), "P_to_nextS": f(chain),
                        "mma_lag_after_P": f(lag), "period": f(period)}
