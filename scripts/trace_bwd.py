@@ -53,5 +53,8 @@ for phase, name in ((1, "dkdv"), (2, "dq")):
                  "mma_dV_to_S": f(g(10, 13, 1)), "mma_S_to_dK": f([ev[(11, i)] - ev[(13, i + 1)] for i in its
                                                                    if (11, i) in ev and (13, i + 1) in ev]),
                  "mma_dK_to_dP": f(g(11, 14, 1)), "mma_dP_to_nextdV": f(g(14, 10)),
-                 "mma_dV_period": f(g(10, 10, 1))}
+                 "mma_dV_period": f(g(10, 10, 1)),
+                 "mma_S_to_dQ(dq)": f(g(13, 11)) if name == "dq" else None,
+                 "mma_dQ_to_dP(dq)": f(g(11, 14, 1)) if name == "dq" else None,
+                 "mma_dQ_period(dq)": f(g(11, 11, 1)) if name == "dq" else None}
 print(json.dumps(out, indent=1))
