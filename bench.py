@@ -130,15 +130,24 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ distributed
-def dist_setup(n_gpus):
+def dist_setup(n_gpus, backend="nccl"):
+    """One process per GPU (torchrun env). backend="gloo" is a debugging aid that
+    lets several ranks share one device (local rank modulo the device count) to
+    exercise the multi-rank path on a single-GPU box; timings are then not
+    per-GPU numbers."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dev = local % torch.cuda.device_count() if backend == "gloo" else local
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+        local = dev
     else:
         torch.cuda.set_device(0)
     return rank, world, local
@@ -155,7 +164,8 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -238,6 +248,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: debugging aid, ranks may share a GPU (not a per-GPU measurement)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
@@ -250,7 +262,7 @@ def main():
     from paper_2511_08083_b200.inputs import make_inputs
     from paper_2511_08083_b200.shard import weak_shard
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup(args.gpus, args.dist_backend)
     B, N, Hq, Hkv, d, causal, label = cfg
     peaks = load_peaks()
     # weak scaling: rank r owns global batches [r B, (r+1) B) (paper_2511_08083_b200/shard.py)
@@ -355,7 +367,8 @@ def main():
            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
            "config": {"workload": args.config, "label": label, "B_per_gpu": B, "global_batch": B * world,
                       "N": N, "Hq": Hq, "Hkv": Hkv, "d": d, "causal": causal,
-                      "parallelism": f"units (batch x KV-head) sharded over {world} GPU(s), no exchange",
+                      "parallelism": f"units (batch x KV-head) sharded over {world} GPU(s), no exchange"
+                                     + ("" if args.dist_backend == "nccl" else " [gloo debug: ranks share a GPU]"),
                       "l2": l2_note},
            "per_gpu_tflops": round(value / world, 2),
            "pct_of_peak": {"spec_2250": round(100 * value / world / SPEC_PEAK_TFLOPS, 2),
