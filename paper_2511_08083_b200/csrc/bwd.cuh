@@ -406,15 +406,24 @@ __global__ void __launch_bounds__(320, 1)
 
 // ---------------------------------------------------------------- B2: dQ
 // CTA = (query tile iq, h, b); loop over 128-key blocks j.
-// TMEM: dQ [0,D)  S double buffer [D,D+128) [D+128,D+256)  dP [D+256,D+384);
-// bf16 dS overwrites dP. MMA order: S(j+1), dQ(j) [needs dS(j)], dP(j+1).
+// Q_i and dO_i are resident, so after they land (TMA) the elementwise warps
+// copy them into TMEM and S = Q_i K_j^T and dP = dO_i V_j^T run with A from
+// TMEM: per block the tensor core then reads only K_j (twice) and V_j from
+// SMEM (96 KB instead of 160 KB), which with the 64 KB of TMA traffic keeps
+// the pass under the 128 B/clk shared-memory bandwidth.
+// TMEM: dQ [0,D)  S [D,D+128)  dP [D+128,D+256)  Q_A [D+256,D+256+D/2)  dO_A [+D/2);
+// bf16 dS overwrites dP. S is single-buffered but released as soon as the
+// elementwise warps have loaded it (bar_sfree), so S(j+1) still overlaps the
+// exponentials of block j. MMA order: S(j+1), dQ(j) [needs dS(j)], dP(j+1).
 template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(320, 1)
     bwd_dq_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapdO,
                   const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                   const BwdParams p) {
   using C = BwdCfg<D>;
-  constexpr int NSA = C::NSA, NSB = C::NSB;
+  // V ring: NSB slots of its own + 2 that reuse the Q_i / dO_i staging area once
+  // those are copied into TMEM (slot 0.. of ring B first, then sQ, sdO).
+  constexpr int NSA = C::NSA, NSB = C::NSB + 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -422,7 +431,12 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sA = smem + 2 * C::T128;   // ring A slot s: K_j [T128]
   uint8_t* sB = sA + NSA * C::T128;   // ring B slot s: V_j [T128]
 
-  __shared__ uint64_t bar_q, fullA[NSA], emptyA[NSA], fullB[NSB], emptyB[NSB], bar_s[2], bar_dp, bar_ds, bar_acc;
+  auto vslot = [&](int it) -> uint8_t* {
+    const int s = it % NSB;
+    return s < C::NSB ? sB + s * C::T128 : smem + (s - C::NSB) * C::T128;
+  };
+  __shared__ uint64_t bar_q, bar_qa, fullA[NSA], emptyA[NSA], fullB[NSB], emptyB[NSB], bar_s, bar_sfree, bar_dp,
+      bar_ds, bar_acc;
   __shared__ uint32_t tmem_base_s;
 
   const int warp = warp_id(), lane = lane_id();
@@ -434,6 +448,7 @@ __global__ void __launch_bounds__(320, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&bar_q, 1);
+    mbar_init(&bar_qa, 8);
     for (int s = 0; s < NSA; ++s) {
       mbar_init(&fullA[s], 1);
       mbar_init(&emptyA[s], 1);
@@ -442,8 +457,8 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&fullB[s], 1);
       mbar_init(&emptyB[s], 1);
     }
-    mbar_init(&bar_s[0], 1);
-    mbar_init(&bar_s[1], 1);
+    mbar_init(&bar_s, 1);
+    mbar_init(&bar_sfree, 8);
     mbar_init(&bar_dp, 1);
     mbar_init(&bar_ds, 8);
     mbar_init(&bar_acc, 1);
@@ -460,7 +475,7 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tb = tmem_base_s;
-  const uint32_t tdQ = tb, tS0 = tb + D, tP = tb + D + 256;
+  const uint32_t tdQ = tb, tS = tb + D, tP = tb + D + 128, tQa = tb + D + 256, tdOa = tQa + D / 2;
 
   if (warp == 8) {
     if (lane == 0) {
@@ -479,9 +494,10 @@ __global__ void __launch_bounds__(320, 1)
       for (int it = 0; it < n_it; ++it) {
         const int sb = it % NSB;
         mbar_wait(&emptyB[sb], ((it / NSB) & 1) ^ 1);
+        if (it == C::NSB) mbar_wait(&bar_qa, 0);  // Q/dO staging copied to TMEM: reuse it for V
         mbar_arrive_expect_tx(&fullB[sb], C::T128);
         for (int pn = 0; pn < C::PANELS; ++pn)
-          tma_load_4d(&mapV, &fullB[sb], sB + sb * C::T128 + pn * 128 * 128, pn * 64, kvh, it * 128, b, pol_keep);
+          tma_load_4d(&mapV, &fullB[sb], vslot(it) + pn * 128 * 128, pn * 64, kvh, it * 128, b, pol_keep);
         if (it + 1 < n_it) {
           const int sa = (it + 1) % NSA;
           mbar_wait(&emptyA[sa], (((it + 1) / NSA) & 1) ^ 1);
@@ -494,30 +510,31 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp == 9) {
     // ================= MMA issuer (whole warp, one elected lane issues) =================
-    constexpr uint32_t idesc_sp = idesc_bf16(128, 128, 0, 0);  // S / dP: M=128 queries, N=128 keys
+    constexpr uint32_t idesc_sp = idesc_bf16(128, 128, 0, 0);  // S / dP: A (Q/dO) from TMEM, B K-major
     constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);   // dQ += dS K_j: K_j MN-major
     constexpr uint64_t KMAJ = sdesc_sw128_const(16, 1024);
     constexpr uint64_t MNMAJ = sdesc_sw128_const(128 * 128, 1024);
-    const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), aA = smem_u32(sA), aB = smem_u32(sB);
+    const uint32_t aA = smem_u32(sA);
     auto kmaj = [&](uint32_t base, int kk) { return KMAJ | ((base + (kk / 4) * 128 * 128 + (kk % 4) * 32) >> 4); };
     auto mnmaj = [&](uint32_t base, int kk) { return MNMAJ | ((base + kk * 16 * 128) >> 4); };
     auto slotK = [&](int it) { return aA + (it % NSA) * C::T128; };
-    auto slotV = [&](int it) { return aB + (it % NSB) * C::T128; };
+    auto slotV = [&](int it) { return smem_u32(vslot(it)); };
     auto issue_s = [&](int it) {
+      hk_trace(13, it, 1);  // MMA: S(it) issue
       const uint32_t k = slotK(it);
-      const uint32_t t = tS0 + 128 * (it & 1);
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) umma_ss_w(t, kmaj(aQ, kk), kmaj(k, kk), idesc_sp, kk > 0);
-      tc_commit_w(&bar_s[it & 1]);
+      for (int kk = 0; kk < D / 16; ++kk) umma_ts_w(tS, tQa + kk * 8, kmaj(k, kk), idesc_sp, kk > 0);
+      tc_commit_w(&bar_s);
     };
     auto issue_dp = [&](int it) {
+      hk_trace(14, it, 1);  // MMA: dP(it) issue
       const uint32_t v = slotV(it);
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) umma_ss_w(tP, kmaj(adO, kk), kmaj(v, kk), idesc_sp, kk > 0);
+      for (int kk = 0; kk < D / 16; ++kk) umma_ts_w(tP, tdOa + kk * 8, kmaj(v, kk), idesc_sp, kk > 0);
       tc_commit_w(&bar_dp);
       if (it + NSB < n_it) tc_commit_w(&emptyB[it % NSB]);  // V(it): dP(it) is its only use
     };
-    mbar_wait(&bar_q, 0);
+    mbar_wait(&bar_qa, 0);  // Q_A, dO_A written to TMEM by the elementwise warps
     mbar_wait(&fullA[0], 0);
     tc_fence_after();
     issue_s(0);
@@ -527,6 +544,7 @@ __global__ void __launch_bounds__(320, 1)
     for (int it = 0; it < n_it; ++it) {
       const bool more = it + 1 < n_it;
       if (more) {
+        mbar_wait(&bar_sfree, it & 1);  // S(it) loaded by the elementwise warps
         mbar_wait(&fullA[(it + 1) % NSA], ((it + 1) / NSA) & 1);
         tc_fence_after();
         issue_s(it + 1);
@@ -553,19 +571,43 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lb = (warp & 3) * 32;
     const int r = (warp & 3) * 32 + lane;  // query row within the tile
     const int q = iq * 128 + r;
+    // ---- prologue: WG0 copies Q_i, WG1 dO_i from swizzled SMEM rows into TMEM (A operands)
+    mbar_wait(&bar_q, 0);
+    {
+      const uint8_t* src = wg == 0 ? sQ : sdO;
+      const uint32_t dst = wg == 0 ? tQa : tdOa;
+#pragma unroll
+      for (int pn = 0; pn < C::PANELS; ++pn) {
+        uint32_t w[32];
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {  // 16-B chunk ch of the row sits at chunk ch ^ (r % 8) (128B swizzle)
+          const uint32_t a = smem_u32(src + pn * 128 * 128 + r * 128 + ((ch ^ (r & 7)) * 16));
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(w[4 * ch]), "=r"(w[4 * ch + 1]), "=r"(w[4 * ch + 2]), "=r"(w[4 * ch + 3])
+                       : "r"(a));
+        }
+        tmem_st32(tmem_addr(dst + 32 * pn, lb, 0), w);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_qa);
+    }
     const float c = 1.4426950408889634f / sqrtf((float)D);
     const size_t vrow = ((size_t)b * p.Hq + h) * p.N + q;
     const float l2 = p.lse2[vrow], Dq = p.Dv[vrow];
-    const uint32_t cP = tP + 64 * wg;
+    const uint32_t cP = tP + 64 * wg, cS = tS + 64 * wg;
     for (int it = 0; it < n_it; ++it) {
-      const uint32_t cS = tS0 + 128 * (it & 1) + 64 * wg;
       float v[64];
       if (threadIdx.x == 0) hk_trace(1, it, 1);
-      mbar_wait(&bar_s[it & 1], (it >> 1) & 1);
+      mbar_wait(&bar_s, it & 1);
       tc_fence_after();
       if (threadIdx.x == 0) hk_trace(2, it, 1);
       tmem_ld64(tmem_addr(cS, lb, 0), v);
       tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_sfree);  // S buffer free for S(it+1)
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const float2 e = bwd_exp2_pair<BWD_EMU_OF_8>(
