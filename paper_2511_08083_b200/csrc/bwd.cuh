@@ -681,7 +681,7 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   bool ok = encode_bnhd(&mQ, Q, B, N, Hq, D, 128) && encode_bnhd(&mdO, dO, B, N, Hq, D, 128) &&
             encode_bnhd(&mK, K, B, N, Hkv, D, 128) && encode_bnhd(&mV, V, B, N, Hkv, D, 128);
   if (!ok) {
-    snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
+    snprintf(err, errlen, "cuTensorMapEncodeTiled failed (CUresult %d)", last_encode_result());
     return HK_ERR_DEVICE;
   }
   static bool attr_done[64] = {};

@@ -43,6 +43,10 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 hk_status check_device(int* num_sms) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(HK_ERR_DEVICE, "cudaGetDevice failed");
+  // Bind the device's primary context to this host thread: the driver-API tensor-map
+  // encoder needs a current context, and a fresh thread (e.g. autograd's backward
+  // thread) has none until a runtime call makes it current.
+  if (cudaSetDevice(dev) != cudaSuccess) return fail(HK_ERR_DEVICE, "cudaSetDevice(%d) failed", dev);
   int major = 0, minor = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
@@ -171,7 +175,7 @@ hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, floa
   CUtensorMap mq, mk, mv;
   if (!hk::encode_bnhd(&mq, Q, B, N, Hq, d, 128) || !hk::encode_bnhd(&mk, K, B, N, Hkv, d, 128) ||
       !hk::encode_bnhd(&mv, V, B, N, Hkv, d, 128))
-    return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed");
+    return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (CUresult %d)", hk::last_encode_result());
   hk::FwdParams p;
   p.lse = LSE;
   p.o = reinterpret_cast<__nv_bfloat16*>(O);
@@ -217,7 +221,7 @@ hk_status hk_diag_umma(const void* A, const void* Bm, float* D, int N, int K, in
   // A: [128][K] as (d=K, H=1, N=128, B=1); B: [N][K] (K-major) or [K][N] (MN-major).
   bool ok = hk::encode_bnhd(&ma, A, 1, 128, 1, K, 128);
   ok = ok && (b_mn ? hk::encode_bnhd(&mb, Bm, 1, K, 1, N, K) : hk::encode_bnhd(&mb, Bm, 1, N, 1, K, N));
-  if (!ok) return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed");
+  if (!ok) return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (CUresult %d)", hk::last_encode_result());
   const uint32_t smem = 128 * K * 2 + N * K * 2 + 1024;
   auto* A16 = reinterpret_cast<const __nv_bfloat16*>(A);
 #define HK_DIAG(NN, KK, AT, BMN)                                                   \

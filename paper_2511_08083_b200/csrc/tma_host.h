@@ -25,9 +25,18 @@ inline PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 // A BNHD bf16 tensor [B][N][H][d] viewed as the 4-D map (d, H, N, B), box
 // (64, 1, box_rows, 1), 128-byte swizzle: one box = box_rows x 128 B, the
 // canonical SWIZZLE_128B K-major atom stacked along rows.
+// Last CUresult from encode_bnhd (per thread), for error messages.
+inline int& last_encode_result() {
+  static thread_local int r = 0;
+  return r;
+}
+
 inline bool encode_bnhd(CUtensorMap* map, const void* base, int B, int N, int H, int d, int box_rows) {
   auto fn = get_encode_fn();
-  if (!fn) return false;
+  if (!fn) {
+    last_encode_result() = -1;
+    return false;
+  }
   cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)H, (cuuint64_t)N, (cuuint64_t)B};
   cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)H * d * 2, (cuuint64_t)N * H * d * 2};
   cuuint32_t box[4] = {64, 1, (cuuint32_t)box_rows, 1};
@@ -35,6 +44,7 @@ inline bool encode_bnhd(CUtensorMap* map, const void* base, int B, int N, int H,
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  last_encode_result() = (int)r;
   return r == CUDA_SUCCESS;
 }
 

@@ -1,0 +1,30 @@
+"""Python binding validation (CPU: every check fires before any CUDA call)."""
+import pytest
+import torch
+
+from paper_2511_08083_b200 import api
+
+
+def t(*shape, dtype=torch.bfloat16):
+    return torch.zeros(*shape, dtype=dtype)
+
+
+def test_rejects_cpu_and_bad_dtype_and_layout():
+    q, k, v = t(1, 128, 2, 64), t(1, 128, 2, 64), t(1, 128, 2, 64)
+    with pytest.raises(ValueError, match="CUDA"):
+        api.attn_fwd(q, k, v)
+    with pytest.raises(ValueError):
+        api._check_tensor("q", t(2, 2, dtype=torch.float32))
+    with pytest.raises(ValueError):
+        api._shapes(t(1, 128, 2, 64), t(1, 64, 2, 64), t(1, 64, 2, 64))
+    with pytest.raises(ValueError):
+        api._shapes(t(1, 128, 2, 64), t(1, 128, 2, 32), t(1, 128, 2, 32))
+    assert api._shapes(t(2, 256, 8, 128), t(2, 256, 2, 128), t(2, 256, 2, 128)) == (2, 256, 8, 2, 128)
+
+
+def test_library_missing_is_loud(monkeypatch, tmp_path):
+    from paper_2511_08083_b200 import _lib
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "_LIB_PATH", str(tmp_path / "missing.so"))
+    with pytest.raises(RuntimeError, match="not built"):
+        _lib.lib()

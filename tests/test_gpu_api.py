@@ -1,0 +1,41 @@
+"""Public API on the GPU: the autograd Function against the oracle, and the
+shard property the multi-GPU split relies on (a batch slice computed alone is
+bitwise identical to the same slice of the full run)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2511_08083_b200.inputs import make_inputs
+from util import TOL_MAXABS, TOL_RELL2, gen, np64, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_autograd_function(causal):
+    from paper_2511_08083_b200 import Attention
+    x = gen(1, 384, 4, 2, 128, seed=21)
+    q, k, v = (x[n].clone().requires_grad_() for n in ("Q", "K", "V"))
+    o = Attention.apply(q, k, v, causal)
+    o.backward(x["dO"])
+    torch.cuda.synchronize()
+    ref = oracle.attn_fwd_bwd(np64(x["Q"]), np64(x["K"]), np64(x["V"]), np64(x["dO"]), causal)
+    assert np.abs(np64(o) - ref["O"]).max() <= TOL_MAXABS
+    for name, t in (("dQ", q.grad), ("dK", k.grad), ("dV", v.grad)):
+        assert rel_l2(np64(t), ref[name]) <= TOL_RELL2, name
+
+
+@pytest.mark.parametrize("d,causal", [(128, True), (64, False)])
+def test_batch_shard_bitwise(d, causal):
+    from paper_2511_08083_b200 import attn_bwd, attn_fwd
+    B, N, Hq, Hkv = 4, 512, 8, 2
+    full = make_inputs(B, N, Hq, Hkv, d, seed=9, device="cuda")
+    part = make_inputs(B, N, Hq, Hkv, d, seed=9, device="cuda", batches=[2, 3])
+    outs = []
+    for x in (full, part):
+        o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
+        outs.append((o, lse) + attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal))
+    torch.cuda.synchronize()
+    for a, b in zip(*outs):
+        assert torch.equal(a[2:4], b)
