@@ -13,7 +13,8 @@
  *   Q, O, dO, dQ : [B][N][Hq][d]  bf16, contiguous, d fastest ("BNHD")
  *   K, V, dK, dV : [B][N][Hkv][d] bf16, contiguous
  *   LSE          : [B][Hq][N]     fp32
- * Supported: d in {64, 128}; N % 128 == 0, N >= 128; Hq % Hkv == 0.
+ * Supported: d in {64, 128}; any N >= 1 (a ragged last 128-row tile is masked,
+ * never read past N in the caller's buffers); Hq % Hkv == 0.
  *
  * Ownership: every pointer is a CUDA device pointer owned by the caller; the
  * library allocates no device memory and keeps no per-call state. All work is
@@ -41,7 +42,7 @@ typedef enum {
   HK_OK = 0,
   HK_ERR_INVALID_ARGUMENT = 1, /* null / misaligned (16 B) pointer; B,Hq,Hkv,N <= 0; Hq % Hkv != 0;
                                   an output aliases an input; workspace too small             */
-  HK_ERR_UNSUPPORTED = 2,      /* d not in {64,128}; N % 128 != 0; a dimension too large       */
+  HK_ERR_UNSUPPORTED = 2,      /* d not in {64,128}; a dimension too large                     */
   HK_ERR_DEVICE = 3,           /* current device is not CC 10.0 (sm_100) or setup failed       */
   HK_ERR_LAUNCH = 4            /* the launch itself failed (cudaGetLastError after enqueue)    */
 } hk_status;
@@ -52,7 +53,7 @@ hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, floa
                       int Hkv, int N, int d, int causal, cudaStream_t stream);
 
 /* Bytes of fp32 workspace hk_attn_bwd needs: D = rowsum(dO * O) and LSE*log2(e),
- * each [B][Hq][N] fp32, i.e. 2*B*Hq*N*4. */
+ * each [B][Hq][Np] fp32 with Np = N rounded up to a multiple of 128, i.e. 2*B*Hq*Np*4. */
 size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d);
 
 /* Backward: given Q, K, V, the forward's O and LSE, and dO, writes dQ, dK, dV

@@ -30,7 +30,7 @@ template <int D>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ O,
                                                       const __nv_bfloat16* __restrict__ dO,
                                                       const float* __restrict__ lse, float* __restrict__ Dout,
-                                                      float* __restrict__ lse2, int B, int N, int H) {
+                                                      float* __restrict__ lse2, int B, int N, int H, int Np) {
   constexpr int LPR = D / 8;  // lanes per row
   constexpr int RPW = 32 / LPR;
   const size_t rows = (size_t)B * N * H;
@@ -57,20 +57,30 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
     for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (row < rows && sub == 0) {
       const size_t h = row % H, n = (row / H) % N, b = row / ((size_t)H * N);
-      const size_t idx = (b * H + h) * N + n;
+      const size_t idx = (b * H + h) * Np + n;  // workspace rows are padded to Np
       Dout[idx] = acc;
-      lse2[idx] = lse[idx] * 1.4426950408889634f;
+      lse2[idx] = lse[(b * H + h) * N + n] * 1.4426950408889634f;
+    }
+  }
+  // ragged N: padding rows of each (b, h) get LSE2 = +inf and D = 0, so the padded
+  // query rows of the last tile give P = 0 and dS = 0 in the dK/dV pass
+  if (Np > N) {
+    const size_t pad = (size_t)Np - N, npad = (size_t)B * H * pad;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad; i += (size_t)gridDim.x * blockDim.x) {
+      const size_t bh = i / pad, n = N + i % pad;
+      Dout[bh * Np + n] = 0.f;
+      lse2[bh * Np + n] = INFINITY;
     }
   }
 }
 
 struct BwdParams {
-  const float* Dv;    // [B][Hq][N]
-  const float* lse2;  // [B][Hq][N]
+  const float* Dv;    // [B][Hq][Np], Np = N rounded up to 128
+  const float* lse2;  // [B][Hq][Np]
   __nv_bfloat16* dq;  // [B][N][Hq][D]
   __nv_bfloat16* dk;  // [B][N][Hkv][D]
   __nv_bfloat16* dv;  // [B][N][Hkv][D]
-  int B, Hq, Hkv, N;
+  int B, Hq, Hkv, N, Np;
 };
 
 // 128 x 128 tiles throughout: tcgen05.mma with N=64 paces at 48 cycles per
@@ -172,7 +182,7 @@ __global__ void __launch_bounds__(320, 1)
   static_assert((2 * NSA + 2 * NSB + 7) * 8 <= C::BAR_BYTES, "barrier area");
 
   const int warp = warp_id(), lane = lane_id();
-  const int T = p.N / 128;
+  const int T = p.Np / 128;
   const int jt = CAUSAL ? (T - 1 - (int)blockIdx.x) : (int)blockIdx.x;  // key tile (heaviest first)
   const int kvh = blockIdx.y, b = blockIdx.z;
   const int G = p.Hq / p.Hkv;
@@ -235,7 +245,7 @@ __global__ void __launch_bounds__(320, 1)
         mbar_arrive_expect_tx(&fullB[sb], C::T128 + 1024);
         for (int pn = 0; pn < C::PANELS; ++pn)
           tma_load_4d(&mapdO, &fullB[sb], st + pn * 128 * 128, pn * 64, h, qi * 128, b, pol_keep);
-        const size_t off = ((size_t)b * p.Hq + h) * p.N + (size_t)qi * 128;
+        const size_t off = ((size_t)b * p.Hq + h) * p.Np + (size_t)qi * 128;
         bulk_load(st + C::T128, p.lse2 + off, 512, &fullB[sb]);
         bulk_load(st + C::T128 + 512, p.Dv + off, 512, &fullB[sb]);
         if (++qi == T) {
@@ -383,7 +393,8 @@ __global__ void __launch_bounds__(320, 1)
     tc_fence_after();
     const float scale = wg == 0 ? 1.f : rsqrtf((float)D);
     const uint32_t tacc = wg == 0 ? tdV : tdK;
-    __nv_bfloat16* out = (wg == 0 ? p.dv : p.dk) + (((size_t)b * p.N + key) * p.Hkv + kvh) * D;
+    const bool key_ok = key < p.N;  // key rows of a ragged last tile beyond N are not stored
+    __nv_bfloat16* out = (wg == 0 ? p.dv : p.dk) + (((size_t)b * p.N + (key_ok ? key : 0)) * p.Hkv + kvh) * D;
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
       uint32_t o[32];
@@ -395,8 +406,10 @@ __global__ void __launch_bounds__(320, 1)
       for (int k = 0; k < 16; ++k)
         op[k] = pack_bf16(__uint_as_float(o[2 * k]) * scale, __uint_as_float(o[2 * k + 1]) * scale);
       uint4* dst = reinterpret_cast<uint4*>(out + c0);
+      if (key_ok) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) dst[k] = o4[k];
+        for (int k = 0; k < 4; ++k) dst[k] = o4[k];
+      }
     }
   }
   tc_fence_before();
@@ -440,7 +453,7 @@ __global__ void __launch_bounds__(320, 1)
   __shared__ uint32_t tmem_base_s;
 
   const int warp = warp_id(), lane = lane_id();
-  const int T = p.N / 128;
+  const int T = p.Np / 128;
   const int iq = CAUSAL ? (T - 1 - (int)blockIdx.x) : (int)blockIdx.x;  // query tile (heaviest first)
   const int h = blockIdx.y, b = blockIdx.z;
   const int kvh = h / (p.Hq / p.Hkv);
@@ -594,7 +607,7 @@ __global__ void __launch_bounds__(320, 1)
       if (lane == 0) mbar_arrive(&bar_qa);
     }
     const float c = 1.4426950408889634f / sqrtf((float)D);
-    const size_t vrow = ((size_t)b * p.Hq + h) * p.N + q;
+    const size_t vrow = ((size_t)b * p.Hq + h) * p.Np + q;
     const float l2 = p.lse2[vrow], Dq = p.Dv[vrow];
     const uint32_t cP = tP + 64 * wg, cS = tS + 64 * wg;
     for (int it = 0; it < n_it; ++it) {
@@ -641,7 +654,8 @@ __global__ void __launch_bounds__(320, 1)
     mbar_wait(&bar_acc, 0);
     tc_fence_after();
     const float scale = rsqrtf((float)D);
-    __nv_bfloat16* out = p.dq + (((size_t)b * p.N + q) * p.Hq + h) * D;
+    const bool q_ok = q < p.N;  // query rows of a ragged last tile beyond N are not stored
+    __nv_bfloat16* out = p.dq + (((size_t)b * p.N + (q_ok ? q : 0)) * p.Hq + h) * D;
 #pragma unroll
     for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
       uint32_t o[32];
@@ -653,8 +667,10 @@ __global__ void __launch_bounds__(320, 1)
       for (int k = 0; k < 16; ++k)
         op[k] = pack_bf16(__uint_as_float(o[2 * k]) * scale, __uint_as_float(o[2 * k + 1]) * scale);
       uint4* dst = reinterpret_cast<uint4*>(out + c0);
+      if (q_ok) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) dst[k] = o4[k];
+        for (int k = 0; k < 4; ++k) dst[k] = o4[k];
+      }
     }
   }
   tc_fence_before();
@@ -674,8 +690,9 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
                        void* dQ, void* dK, void* dV, float* ws, int B, int Hq, int Hkv, int N, cudaStream_t stream,
                        char* err, size_t errlen, int phase) {
   using C = BwdCfg<D>;
+  const int Np = (N + 127) / 128 * 128;  // workspace rows padded to whole tiles
   float* Dv = ws;
-  float* lse2 = ws + (size_t)B * Hq * N;
+  float* lse2 = ws + (size_t)B * Hq * Np;
   // every operand tile is a 128-row box (two 64-column panels at D=128)
   CUtensorMap mQ, mdO, mK, mV;
   bool ok = encode_bnhd(&mQ, Q, B, N, Hq, D, 128) && encode_bnhd(&mdO, dO, B, N, Hq, D, 128) &&
@@ -695,7 +712,7 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     if (dev < 64) attr_done[dev] = true;
   }
   BwdParams p{Dv, lse2, reinterpret_cast<__nv_bfloat16*>(dQ), reinterpret_cast<__nv_bfloat16*>(dK),
-              reinterpret_cast<__nv_bfloat16*>(dV), B, Hq, Hkv, N};
+              reinterpret_cast<__nv_bfloat16*>(dV), B, Hq, Hkv, N, Np};
   // B0
   const size_t rows = (size_t)B * N * Hq;
   const size_t warps_needed = (rows + (32 / (D / 8)) - 1) / (32 / (D / 8));
@@ -704,12 +721,12 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   if (phase < 0 || phase == 0)
     bwd_pre_kernel<D><<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(O),
                                                               reinterpret_cast<const __nv_bfloat16*>(dO), LSE, Dv,
-                                                              lse2, B, N, Hq);
+                                                              lse2, B, N, Hq, Np);
   // B1, B2
   if (phase < 0 || phase == 1)
-    bwd_dkdv_kernel<D, CAUSAL><<<dim3(N / 128, Hkv, B), C::THREADS, C::SMEM1, stream>>>(mQ, mdO, mK, mV, p);
+    bwd_dkdv_kernel<D, CAUSAL><<<dim3(Np / 128, Hkv, B), C::THREADS, C::SMEM1, stream>>>(mQ, mdO, mK, mV, p);
   if (phase < 0 || phase == 2)
-    bwd_dq_kernel<D, CAUSAL><<<dim3(N / 128, Hq, B), C::THREADS, C::SMEM2, stream>>>(mQ, mdO, mK, mV, p);
+    bwd_dq_kernel<D, CAUSAL><<<dim3(Np / 128, Hq, B), C::THREADS, C::SMEM2, stream>>>(mQ, mdO, mK, mV, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(err, errlen, "hk_attn_bwd launch failed: %s", cudaGetErrorString(e));

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(384, 1)
   const int h = blockIdx.y;
   const int b = blockIdx.z;
   const int kvh = h / (p.Hq / p.Hkv);
-  const int T = p.N / 128;             // 128-row tiles along the sequence
+  const int T = (p.N + 127) / 128;     // 128-row tiles along the sequence (last one may be ragged)
   const int qt0 = 2 * pair, qt1 = 2 * pair + 1;
   const bool has1 = qt1 < T;
   const int nkv0 = CAUSAL ? qt0 + 1 : T;
@@ -224,7 +224,10 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         if (threadIdx.x % 128 == 0) hk_trace(2 + 4 * t, j, 0);  // S_t(j) ready
         const bool diag = CAUSAL && j == qt;
-        softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, diag, j > 0);
+        // keys >= N (zero-filled by TMA) only need a mask when not causal: under the
+        // causal mask they already lie beyond every valid query row
+        const int kvalid = (!CAUSAL && j == T - 1) ? p.N - j * 128 : 128;
+        softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, diag, j > 0, kvalid);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -236,7 +239,8 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       const float inv_l = 1.f / l;
       const int row = qt * 128 + r;
-      __nv_bfloat16* orow = p.o + (((size_t)b * p.N + row) * p.Hq + h) * D;
+      const bool row_ok = row < p.N;  // rows of a ragged last tile beyond N are not stored
+      __nv_bfloat16* orow = p.o + (((size_t)b * p.N + (row_ok ? row : 0)) * p.Hq + h) * D;
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t o[32];
@@ -248,10 +252,12 @@ __global__ void __launch_bounds__(384, 1)
         for (int cc = 0; cc < 16; ++cc)
           vp[cc] = pack_bf16(__uint_as_float(o[2 * cc]) * inv_l, __uint_as_float(o[2 * cc + 1]) * inv_l);
         uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+        if (row_ok) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = v[q];
+          for (int q = 0; q < 4; ++q) dst[q] = v[q];
+        }
       }
-      p.lse[((size_t)b * p.Hq + h) * p.N + row] = (m + __log2f(l)) * 0.69314718055994531f;
+      if (row_ok) p.lse[((size_t)b * p.Hq + h) * p.N + row] = (m + __log2f(l)) * 0.69314718055994531f;
     }
   }
 

@@ -85,7 +85,6 @@ hk_status validate_common(int B, int Hq, int Hkv, int N, int d) {
     return fail(HK_ERR_INVALID_ARGUMENT, "B, Hq, Hkv, N must be positive (got %d, %d, %d, %d)", B, Hq, Hkv, N);
   if (Hq % Hkv != 0) return fail(HK_ERR_INVALID_ARGUMENT, "Hq (%d) must be a multiple of Hkv (%d)", Hq, Hkv);
   if (d != 64 && d != 128) return fail(HK_ERR_UNSUPPORTED, "head dim d=%d unsupported (need 64 or 128)", d);
-  if (N % 128 != 0) return fail(HK_ERR_UNSUPPORTED, "N=%d must be a multiple of 128", N);
   if (Hq > 65535 || B > 65535) return fail(HK_ERR_UNSUPPORTED, "Hq and B must be <= 65535");
   return HK_OK;
 }
@@ -183,7 +182,7 @@ hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, floa
   p.Hq = Hq;
   p.Hkv = Hkv;
   p.N = N;
-  p.num_pairs = (N / 128 + 1) / 2;
+  p.num_pairs = ((N + 127) / 128 + 1) / 2;
   if (d == 64) return causal ? launch_fwd<64, true>(mq, mk, mv, p, stream) : launch_fwd<64, false>(mq, mk, mv, p, stream);
   return causal ? launch_fwd<128, true>(mq, mk, mv, p, stream) : launch_fwd<128, false>(mq, mk, mv, p, stream);
 }
@@ -192,7 +191,8 @@ size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d) {
   (void)Hkv;
   (void)d;
   if (B <= 0 || Hq <= 0 || N <= 0) return 0;
-  return (size_t)2 * B * Hq * N * sizeof(float);
+  const size_t Np = ((size_t)N + 127) / 128 * 128;  // rows padded to whole 128-row tiles
+  return (size_t)2 * B * Hq * Np * sizeof(float);
 }
 
 hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,

@@ -47,20 +47,23 @@ __device__ __forceinline__ void softmax_chunk32(const float* s, float c, float m
 // tS: this tile's score columns (fp32 S in, bf16 P out over its first 64
 // columns); tO: its O accumulator (rescaled in place when the max moves).
 // m, l: running max (log2 units, always integral) and row sum. `diag`: causal
-// diagonal tile (mask key > query, all exps on the MUFU so masked P is 0).
-// `o_live`: O already holds earlier P V products.
+// diagonal tile (mask key > query); `kvalid` < 128: only the first kvalid keys
+// of this block exist (ragged N). Masked blocks run all exps on the MUFU so a
+// masked P is exactly 0. `o_live`: O already holds earlier P V products.
 template <int D, int EMU_OF_8>
 __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t lane_base, int r, float c,
-                                             float& m, float& l, bool diag, bool o_live) {
+                                             float& m, float& l, bool diag, bool o_live, int kvalid = 128) {
   float s[128];
 #pragma unroll
   for (int c0 = 0; c0 < 128; c0 += 32)
     tmem_ld32(tmem_addr(tS, lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(&s[c0]));
   tmem_wait_ld();
-  if (diag) {
+  const bool masked = diag || kvalid < 128;
+  if (masked) {
+    const int lim = diag ? (r + 1 < kvalid ? r + 1 : kvalid) : kvalid;  // keys [0, lim) visible
 #pragma unroll
     for (int cc = 0; cc < 128; ++cc)
-      if (cc > r) s[cc] = -INFINITY;  // key > query
+      if (cc >= lim) s[cc] = -INFINITY;
   }
   // row max: 8 independent 3-input-max chains, then combine
   float mx8[8];
@@ -82,7 +85,7 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
 #pragma unroll
   for (int c0 = 0; c0 < 128; c0 += 32) {
     uint32_t pk[16];
-    if (diag)
+    if (masked)
       softmax_chunk32<false, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);
     else
       softmax_chunk32<true, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);

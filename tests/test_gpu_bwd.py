@@ -6,7 +6,7 @@ import pytest
 import torch
 
 import oracle
-from util import TOL_RELL2, gen, np64, rel_l2
+from util import TOL_MAXABS, TOL_RELL2, gen, np64, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -18,6 +18,10 @@ CASES = [
     (1, 512, 2, 2, 128),
     (2, 256, 6, 3, 64),
     (1, 256, 8, 1, 128),    # G=8, d=128 (the 70B head geometry at small N)
+    (1, 200, 4, 2, 128),    # ragged: N % 128 != 0
+    (2, 333, 2, 1, 64),     # ragged, 3 tiles
+    (1, 77, 2, 2, 128),     # a single partial tile
+    (1, 1, 2, 1, 64),       # N = 1
 ]
 
 
@@ -25,12 +29,25 @@ def run(B, N, Hq, Hkv, d, causal, seed, std_qk=None):
     from paper_2511_08083_b200 import attn_bwd, attn_fwd
     x = gen(B, N, Hq, Hkv, d, seed=seed, std_qk=std_qk)
     o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
-    ws = torch.empty(2 * B * Hq * N, dtype=torch.float32, device="cuda")
+    Np = (N + 127) // 128 * 128
+    ws = torch.empty(2 * B * Hq * Np, dtype=torch.float32, device="cuda")
     dq, dk, dv = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, workspace=ws)
     torch.cuda.synchronize()
     ref = oracle.attn_fwd_bwd(np64(x["Q"]), np64(x["K"]), np64(x["V"]), np64(x["dO"]), causal)
-    errs = {n: rel_l2(np64(t), ref[n]) for n, t in (("dQ", dq), ("dK", dk), ("dV", dv))}
-    errs["D"] = rel_l2(np64(ws[: B * Hq * N]).reshape(B, Hq, N), ref["D"])
+    errs = {}
+    for n, t in (("dQ", dq), ("dK", dk), ("dV", dv)):
+        got = np64(t)
+        if np.linalg.norm(ref[n]) < 1e-9 * np.sqrt(ref[n].size):
+            # Identically zero gradient (N = 1: dS = P (dP - D) = 0 exactly). Relative L2 is
+            # undefined; what the GPU returns is the usual FlashAttention rounding noise: P is
+            # rounded to bf16 inside O while l sums the fp32 P (reading #6), and D is taken from
+            # the bf16 O (reading #11), so dP - D carries ~2^-9 |dO.V| — for N = 1 that noise is
+            # the whole signal. Bound it absolutely at 2 x the O tolerance (scaled into the
+            # rel-L2 slot so one threshold applies).
+            errs[n] = float(np.abs(got).max()) * (TOL_RELL2 / (2 * TOL_MAXABS))
+        else:
+            errs[n] = rel_l2(got, ref[n])
+    errs["D"] = rel_l2(np64(ws[: B * Hq * Np]).reshape(B, Hq, Np)[:, :, :N], ref["D"])
     return errs
 
 

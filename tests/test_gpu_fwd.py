@@ -16,6 +16,10 @@ CASES = [
     (1, 640, 8, 1, 64),     # 5 tiles, G=8
     (1, 512, 2, 2, 128),
     (2, 256, 6, 3, 64),
+    (1, 200, 4, 2, 128),    # ragged: N % 128 != 0 (last tile 72 rows)
+    (2, 333, 2, 1, 64),     # ragged, 3 tiles, G=2
+    (1, 77, 2, 2, 128),     # a single partial tile
+    (1, 1, 2, 1, 64),       # N = 1
 ]
 
 
