@@ -13,8 +13,8 @@
 //   warps 4-7  softmax WG1: Q tile 1
 //   warp  8    TMA producer: Q0/Q1 once, then a K ring and a V ring
 //   warp  9    MMA issuer (one thread): S_t = Q_t K_j^T, O_t += P_t V_j
-//   warps 10-11 idle (WG2 = warps 8-11 drops to 72 registers, WG0/WG1 rise to 216:
-//   128*72 + 256*216 = 64512 = the CTA pool at launch, 384 x 168)
+//   warps 10-11 idle (WG2 = warps 8-11 drops to 112 registers, WG0/WG1 rise to 192:
+//   128*112 + 256*192 = 63488 <= 64512, the CTA pool at launch, 384 x 168)
 // TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D,256+2D);
 // bf16 P_t is written over S_t's first 64 columns (A operand from TMEM).
 // The two Q tiles ping-pong: while WG0 does softmax on S0(j+1) the tensor
@@ -35,7 +35,8 @@ struct FwdParams {
   float* lse;        // [B][Hq][N]
   __nv_bfloat16* o;  // [B][N][Hq][D]
   int B, Hq, Hkv, N;
-  int num_pairs;  // ceil(N / 256)
+  int num_pairs;  // ceil(N / 256): Q-tile pairs per head
+  int num_items;  // B * Hq * num_pairs work items
 };
 
 template <int D>
@@ -54,6 +55,44 @@ struct FwdCfg {
   static constexpr int EMU_OF_8 = (D == 128) ? HK_FWD_EMU128 : HK_FWD_EMU64;  // exps per 8 on the FMA pipe
 };
 
+// One work item = (b, h, pair of 128-row Q tiles). Items are numbered so that
+// the items of one (b, kvh) group (its G query heads x all pairs, which share
+// K and V) are consecutive, pairs fastest and heaviest first when causal; the
+// persistent CTAs take them in snake order (round r: CTA c gets item
+// r*G + c for even r, r*G + G-1-c for odd r), which pairs heavy with light
+// items across rounds and keeps the concurrently processed items on a few
+// K/V heads (L2 reuse).
+struct FwdItem {
+  int b, h, kvh, qt0, qt1, nkv0, nkv1, nkv;
+};
+
+template <bool CAUSAL>
+__device__ __forceinline__ int fwd_item_index(int round, int cta, int ctas) {
+  return round * ctas + ((round & 1) ? ctas - 1 - cta : cta);
+}
+
+template <bool CAUSAL>
+__device__ __forceinline__ FwdItem fwd_decode(const FwdParams& p, int item) {
+  const int G = p.Hq / p.Hkv;
+  const int pr = item % p.num_pairs;
+  int rest = item / p.num_pairs;
+  const int hg = rest % G;
+  rest /= G;
+  FwdItem it;
+  it.kvh = rest % p.Hkv;
+  it.b = rest / p.Hkv;
+  it.h = it.kvh * G + hg;
+  const int pair = CAUSAL ? (p.num_pairs - 1 - pr) : pr;
+  const int T = (p.N + 127) / 128;  // 128-row tiles along the sequence (last one may be ragged)
+  it.qt0 = 2 * pair;
+  it.qt1 = 2 * pair + 1;
+  const bool has1 = it.qt1 < T;
+  it.nkv0 = CAUSAL ? it.qt0 + 1 : T;
+  it.nkv1 = has1 ? (CAUSAL ? it.qt1 + 1 : T) : 0;
+  it.nkv = it.nkv1 > it.nkv0 ? it.nkv1 : it.nkv0;
+  return it;
+}
+
 template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(384, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
@@ -68,27 +107,18 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sK = smem + 2 * TB;  // NS tiles
   uint8_t* sV = sK + NS * TB;   // NS tiles
 
-  __shared__ uint64_t bar_q, bar_kfull[NS], bar_kempty[NS], bar_vfull[NS], bar_vempty[NS];
-  __shared__ uint64_t bar_s[2], bar_p[2], bar_o[2];
+  __shared__ uint64_t bar_q, bar_qfree, bar_kfull[NS], bar_kempty[NS], bar_vfull[NS], bar_vempty[NS];
+  __shared__ uint64_t bar_s[2], bar_p[2], bar_o[2], bar_oempty[2];
   __shared__ uint32_t tmem_base_s;
 
   const int warp = warp_id();
   const int lane = lane_id();
-
-  // ---- work decomposition: x = Q-tile pair (heaviest first when causal), y = head, z = batch
-  const int pair = CAUSAL ? (p.num_pairs - 1 - (int)blockIdx.x) : (int)blockIdx.x;
-  const int h = blockIdx.y;
-  const int b = blockIdx.z;
-  const int kvh = h / (p.Hq / p.Hkv);
-  const int T = (p.N + 127) / 128;     // 128-row tiles along the sequence (last one may be ragged)
-  const int qt0 = 2 * pair, qt1 = 2 * pair + 1;
-  const bool has1 = qt1 < T;
-  const int nkv0 = CAUSAL ? qt0 + 1 : T;
-  const int nkv1 = has1 ? (CAUSAL ? qt1 + 1 : T) : 0;
-  const int nkv = nkv1 > nkv0 ? nkv1 : nkv0;
+  const int cta = blockIdx.x, ctas = gridDim.x;
+  if (threadIdx.x == 0) hk_trace(30, 0, 0);  // CTA start
 
   if (threadIdx.x == 0) {
     mbar_init(&bar_q, 1);
+    mbar_init(&bar_qfree, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bar_kfull[s], 1);
       mbar_init(&bar_kempty[s], 1);
@@ -99,6 +129,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&bar_s[t], 1);
       mbar_init(&bar_p[t], 4);
       mbar_init(&bar_o[t], 1);
+      mbar_init(&bar_oempty[t], 4);
     }
     fence_barrier_init();
   }
@@ -113,32 +144,47 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_after();
   const uint32_t tbase = tmem_base_s;
 
+  // Every role walks the same item sequence; each barrier keeps its own phase
+  // counter, and barriers of a Q tile an item lacks (odd T, last pair) are
+  // skipped consistently by both sides.
   if (warp >= 8) {
-    reg_dealloc<72>();
+    reg_dealloc<112>();
     if (warp == 8 && lane == 0) {
       // ================= TMA producer =================
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
-      mbar_arrive_expect_tx(&bar_q, (has1 ? 2 : 1) * TB);
-      for (int pnl = 0; pnl < C::PANELS; ++pnl) {
-        tma_load_4d(&mapQ, &bar_q, sQ + pnl * 128 * 128, pnl * 64, h, qt0 * 128, b, pol_q);
-        if (has1) tma_load_4d(&mapQ, &bar_q, sQ + TB + pnl * 128 * 128, pnl * 64, h, qt1 * 128, b, pol_q);
-      }
       int s = 0;
-      uint32_t ph = 0;
-      for (int j = 0; j < nkv; ++j) {
+      uint32_t ph = 0, qf_ph = 0;
+      auto load_kv = [&](const FwdItem& it, int j) {
         mbar_wait(&bar_kempty[s], ph ^ 1);
         mbar_arrive_expect_tx(&bar_kfull[s], TB);
         for (int pnl = 0; pnl < C::PANELS; ++pnl)
-          tma_load_4d(&mapK, &bar_kfull[s], sK + s * TB + pnl * 128 * 128, pnl * 64, kvh, j * 128, b, pol_kv);
+          tma_load_4d(&mapK, &bar_kfull[s], sK + s * TB + pnl * 128 * 128, pnl * 64, it.kvh, j * 128, it.b, pol_kv);
         mbar_wait(&bar_vempty[s], ph ^ 1);
         mbar_arrive_expect_tx(&bar_vfull[s], TB);
         for (int pnl = 0; pnl < C::PANELS; ++pnl)
-          tma_load_4d(&mapV, &bar_vfull[s], sV + s * TB + pnl * 128 * 128, pnl * 64, kvh, j * 128, b, pol_kv);
+          tma_load_4d(&mapV, &bar_vfull[s], sV + s * TB + pnl * 128 * 128, pnl * 64, it.kvh, j * 128, it.b, pol_kv);
         if (++s == NS) {
           s = 0;
           ph ^= 1;
         }
+      };
+      for (int r = 0;; ++r) {
+        const int item = fwd_item_index<CAUSAL>(r, cta, ctas);
+        if (item >= p.num_items) break;
+        const FwdItem it = fwd_decode<CAUSAL>(p, item);
+        load_kv(it, 0);  // K/V of the next item stream in while the previous one finishes
+        if (r > 0) {     // Q buffer is free once the previous item's last S = Q K^T completed
+          mbar_wait(&bar_qfree, qf_ph);
+          qf_ph ^= 1;
+        }
+        const bool has1 = it.nkv1 > 0;
+        mbar_arrive_expect_tx(&bar_q, (has1 ? 2 : 1) * TB);
+        for (int pnl = 0; pnl < C::PANELS; ++pnl) {
+          tma_load_4d(&mapQ, &bar_q, sQ + pnl * 128 * 128, pnl * 64, it.h, it.qt0 * 128, it.b, pol_q);
+          if (has1) tma_load_4d(&mapQ, &bar_q, sQ + TB + pnl * 128 * 128, pnl * 64, it.h, it.qt1 * 128, it.b, pol_q);
+        }
+        for (int j = 1; j < it.nkv; ++j) load_kv(it, j);
       }
     } else if (warp == 9) {
       // ================= MMA issuer (whole warp, one elected lane issues) =================
@@ -165,64 +211,91 @@ __global__ void __launch_bounds__(384, 1)
           umma_ts_w(tbase + 256 + D * t, tbase + 128 * t + kk * 8, vd + ((kk * 16 * 128) >> 4), idesc_o,
                     (j > 0 || kk > 0) ? 1u : 0u);
       };
-      mbar_wait(&bar_q, 0);
-      mbar_wait(&bar_kfull[0], 0);
-      tc_fence_after();
-      issue_s(0, 0);
-      if (nkv1 > 0) issue_s(1, 0);
-      tc_commit_w(&bar_kempty[0]);
       int s = 0;
-      uint32_t ph = 0;
-      for (int j = 0; j < nkv; ++j) {
-        const int s1 = s + 1 == NS ? 0 : s + 1;
-        const uint32_t ph1 = s + 1 == NS ? ph ^ 1 : ph;
-        mbar_wait(&bar_vfull[s], ph);
-        bool k_next_waited = false;
+      uint32_t ph = 0, q_ph = 0;
+      uint32_t p_ph[2] = {0, 0}, oe_ph[2] = {0, 0};
+      bool o_used[2] = {false, false};  // O_t holds an earlier item's accumulator (wait for its epilogue)
+      for (int r = 0;; ++r) {
+        const int item = fwd_item_index<CAUSAL>(r, cta, ctas);
+        if (item >= p.num_items) break;
+        const FwdItem it = fwd_decode<CAUSAL>(p, item);
+        const bool last_item = fwd_item_index<CAUSAL>(r + 1, cta, ctas) >= p.num_items;
+        mbar_wait(&bar_q, q_ph);
+        q_ph ^= 1;
+        mbar_wait(&bar_kfull[s], ph);
+        tc_fence_after();
+        issue_s(0, s);
+        if (it.nkv1 > 0) issue_s(1, s);
+        tc_commit_w(&bar_kempty[s]);
+        if (it.nkv == 1 && !last_item) tc_commit_w(&bar_qfree);
+        for (int j = 0; j < it.nkv; ++j) {
+          const int s1 = s + 1 == NS ? 0 : s + 1;
+          const uint32_t ph1 = s + 1 == NS ? ph ^ 1 : ph;
+          mbar_wait(&bar_vfull[s], ph);
+          bool k_next_waited = false;
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const int nk = t == 0 ? nkv0 : nkv1;
-          if (j < nk) {
-            mbar_wait(&bar_p[t], j & 1);
-            tc_fence_after();
-            hk_trace(10 + t, j, 0);  // MMA: P_t(j) seen, PV issue
-            issue_pv(t, s, j);
-            if (j + 1 < nk) {
-              if (!k_next_waited) {
-                mbar_wait(&bar_kfull[s1], ph1);
-                tc_fence_after();
-                k_next_waited = true;
+          for (int t = 0; t < 2; ++t) {
+            const int nk = t == 0 ? it.nkv0 : it.nkv1;
+            if (j < nk) {
+              mbar_wait(&bar_p[t], p_ph[t]);
+              p_ph[t] ^= 1;
+              if (j == 0 && o_used[t]) {  // previous item's O_t must be read out before PV overwrites it
+                mbar_wait(&bar_oempty[t], oe_ph[t]);
+                oe_ph[t] ^= 1;
               }
-              issue_s(t, s1);
-            } else {
-              tc_commit_w(&bar_o[t]);
+              tc_fence_after();
+              hk_trace(10 + t, j, 0);  // MMA: P_t(j) seen, PV issue
+              issue_pv(t, s, j);
+              if (j + 1 < nk) {
+                if (!k_next_waited) {
+                  mbar_wait(&bar_kfull[s1], ph1);
+                  tc_fence_after();
+                  k_next_waited = true;
+                }
+                issue_s(t, s1);
+              } else {
+                tc_commit_w(&bar_o[t]);
+                o_used[t] = true;
+              }
             }
           }
+          // the CTA's very last V release is never waited for: skip it so no
+          // arrive can land after the CTA exits
+          if (!(last_item && j + 1 == it.nkv)) tc_commit_w(&bar_vempty[s]);
+          if (k_next_waited) tc_commit_w(&bar_kempty[s1]);
+          if (j + 2 == it.nkv && !last_item) tc_commit_w(&bar_qfree);  // every S of this item issued
+          s = s1;
+          ph = ph1;
         }
-        if (j + 1 < nkv) tc_commit_w(&bar_vempty[s]);
-        if (k_next_waited) tc_commit_w(&bar_kempty[s1]);
-        s = s1;
-        ph = ph1;
       }
     }
   } else {
     // ================= softmax warpgroups =================
-    reg_alloc<216>();
+    reg_alloc<192>();
     const int t = warp >> 2;  // Q tile of this warpgroup
-    const int nk = t == 0 ? nkv0 : nkv1;
     const uint32_t tS = tbase + 128 * t;
     const uint32_t tO = tbase + 256 + D * t;
-    if (nk > 0) {
-      const int qt = t == 0 ? qt0 : qt1;
-      const uint32_t lane_base = (warp & 3) * 32;
-      const int r = (warp & 3) * 32 + lane;  // row within the Q tile == TMEM lane
-      const float c = 1.4426950408889634f / sqrtf((float)D);  // (1/sqrt d) log2 e
+    const uint32_t lane_base = (warp & 3) * 32;
+    const int r = (warp & 3) * 32 + lane;  // row within the Q tile == TMEM lane
+    const float c = 1.4426950408889634f / sqrtf((float)D);  // (1/sqrt d) log2 e
+    const int T = (p.N + 127) / 128;
+    uint32_t s_ph = 0, o_ph = 0;
+    int step = 0;  // running KV-step count (trace index only)
+    for (int rr = 0;; ++rr) {
+      const int item = fwd_item_index<CAUSAL>(rr, cta, ctas);
+      if (item >= p.num_items) break;
+      const FwdItem it = fwd_decode<CAUSAL>(p, item);
+      const int nk = t == 0 ? it.nkv0 : it.nkv1;
+      if (nk == 0) continue;
+      const int qt = t == 0 ? it.qt0 : it.qt1;
       float m = -INFINITY;  // running max, log2-scaled units
       float l = 0.f;        // running row sum
-      for (int j = 0; j < nk; ++j) {
-        if (threadIdx.x % 128 == 0) hk_trace(1 + 4 * t, j, 0);  // softmax: start waiting for S_t(j)
-        mbar_wait(&bar_s[t], j & 1);
+      for (int j = 0; j < nk; ++j, ++step) {
+        if (threadIdx.x % 128 == 0) hk_trace(1 + 4 * t, step, 0);  // softmax: start waiting for S_t(j)
+        mbar_wait(&bar_s[t], s_ph);
+        s_ph ^= 1;
         tc_fence_after();
-        if (threadIdx.x % 128 == 0) hk_trace(2 + 4 * t, j, 0);  // S_t(j) ready
+        if (threadIdx.x % 128 == 0) hk_trace(2 + 4 * t, step, 0);  // S_t(j) ready
         const bool diag = CAUSAL && j == qt;
         // keys >= N (zero-filled by TMA) only need a mask when not causal: under the
         // causal mask they already lie beyond every valid query row
@@ -232,20 +305,26 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_p[t]);
-        if (threadIdx.x % 128 == 0) hk_trace(3 + 4 * t, j, 0);  // P_t(j) published
+        if (threadIdx.x % 128 == 0) hk_trace(3 + 4 * t, step, 0);  // P_t(j) published
       }
       // ---- epilogue: O = O_acc / l (bf16), LSE = (m + log2 l) ln 2
-      mbar_wait(&bar_o[t], 0);
+      mbar_wait(&bar_o[t], o_ph);
+      o_ph ^= 1;
       tc_fence_after();
       const float inv_l = 1.f / l;
       const int row = qt * 128 + r;
       const bool row_ok = row < p.N;  // rows of a ragged last tile beyond N are not stored
-      __nv_bfloat16* orow = p.o + (((size_t)b * p.N + (row_ok ? row : 0)) * p.Hq + h) * D;
+      __nv_bfloat16* orow = p.o + (((size_t)it.b * p.N + (row_ok ? row : 0)) * p.Hq + it.h) * D;
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t o[32];
         tmem_ld32(tmem_addr(tO, lane_base, c0), o);
         tmem_wait_ld();
+        if (c0 + 32 == D) {  // O_t fully read: the next item's P V may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_oempty[t]);
+        }
         uint4 v[4];
         uint32_t* vp = reinterpret_cast<uint32_t*>(v);
 #pragma unroll
@@ -257,7 +336,8 @@ __global__ void __launch_bounds__(384, 1)
           for (int q = 0; q < 4; ++q) dst[q] = v[q];
         }
       }
-      if (row_ok) p.lse[((size_t)b * p.Hq + h) * p.N + row] = (m + __log2f(l)) * 0.69314718055994531f;
+      if (row_ok) p.lse[((size_t)it.b * p.Hq + it.h) * p.N + row] = (m + __log2f(l)) * 0.69314718055994531f;
+      if (threadIdx.x % 128 == 0) hk_trace(31 + t, rr, 0);  // epilogue of tile t done
     }
   }
 

@@ -86,17 +86,20 @@ hk_status validate_common(int B, int Hq, int Hkv, int N, int d) {
   if (Hq % Hkv != 0) return fail(HK_ERR_INVALID_ARGUMENT, "Hq (%d) must be a multiple of Hkv (%d)", Hq, Hkv);
   if (d != 64 && d != 128) return fail(HK_ERR_UNSUPPORTED, "head dim d=%d unsupported (need 64 or 128)", d);
   if (Hq > 65535 || B > 65535) return fail(HK_ERR_UNSUPPORTED, "Hq and B must be <= 65535");
+  if ((long long)B * Hq * ((N + 127) / 128) > 0x7fffffffLL)
+    return fail(HK_ERR_UNSUPPORTED, "B * Hq * ceil(N/128) must fit in int32");
   return HK_OK;
 }
 
 template <int D, bool CAUSAL>
 hk_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const hk::FwdParams& p,
-                     cudaStream_t stream) {
+                     int num_sms, cudaStream_t stream) {
   using C = hk::FwdCfg<D>;
   auto* fn = hk::fwd_kernel<D, CAUSAL>;
   hk_status s = ensure_smem(fn, C::SMEM);
   if (s != HK_OK) return s;
-  dim3 grid(p.num_pairs, p.Hq, p.B);
+  // persistent: one CTA per SM (the SMEM footprint allows one), items in snake order
+  dim3 grid(p.num_items < num_sms ? p.num_items : num_sms);
   fn<<<grid, C::THREADS, C::SMEM, stream>>>(mq, mk, mv, p);
   return launched("hk_attn_fwd");
 }
@@ -168,7 +171,8 @@ hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, floa
       overlaps(LSE, lse_bytes, O, q_bytes) || overlaps(LSE, lse_bytes, Q, q_bytes) ||
       overlaps(LSE, lse_bytes, K, kv_bytes) || overlaps(LSE, lse_bytes, V, kv_bytes))
     return fail(HK_ERR_INVALID_ARGUMENT, "outputs O/LSE must not alias inputs or each other");
-  s = check_device(nullptr);
+  int num_sms = 0;
+  s = check_device(&num_sms);
   if (s != HK_OK) return s;
 
   CUtensorMap mq, mk, mv;
@@ -183,8 +187,12 @@ hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, floa
   p.Hkv = Hkv;
   p.N = N;
   p.num_pairs = ((N + 127) / 128 + 1) / 2;
-  if (d == 64) return causal ? launch_fwd<64, true>(mq, mk, mv, p, stream) : launch_fwd<64, false>(mq, mk, mv, p, stream);
-  return causal ? launch_fwd<128, true>(mq, mk, mv, p, stream) : launch_fwd<128, false>(mq, mk, mv, p, stream);
+  p.num_items = B * Hq * p.num_pairs;
+  if (d == 64)
+    return causal ? launch_fwd<64, true>(mq, mk, mv, p, num_sms, stream)
+                  : launch_fwd<64, false>(mq, mk, mv, p, num_sms, stream);
+  return causal ? launch_fwd<128, true>(mq, mk, mv, p, num_sms, stream)
+                : launch_fwd<128, false>(mq, mk, mv, p, num_sms, stream);
 }
 
 size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d) {

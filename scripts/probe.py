@@ -19,6 +19,12 @@ CONFIGS = {
     "C4-2048": (16, 2048, 32, 32, 64, True),
     "C5-4096-nc": (16, 4096, 64, 8, 128, False),
     "C5-4096-c": (16, 4096, 64, 8, 128, True),
+    "C5-1024-nc": (16, 1024, 64, 8, 128, False),
+    "C5-1024-c": (16, 1024, 64, 8, 128, True),
+    "C5-8192-nc": (16, 8192, 64, 8, 128, False),
+    "C5-16384-nc": (16, 16384, 64, 8, 128, False),
+    "C5-16384-c": (16, 16384, 64, 8, 128, True),
+    "C4-2048": (16, 2048, 32, 32, 64, True),
 }
 
 

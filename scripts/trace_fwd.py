@@ -17,6 +17,7 @@ from paper_2511_08083_b200.inputs import make_inputs  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2-nc"
 shapes = {"C2-nc": (16, 4096, 16, 16, 128, False), "C3": (16, 8192, 32, 8, 128, True),
+          "C5-1024-c": (16, 1024, 64, 8, 128, True), "C5-1024-nc": (16, 1024, 64, 8, 128, False),
           "C4-8192": (16, 8192, 32, 32, 64, True)}
 B, N, Hq, Hkv, d, causal = shapes[cfg]
 x = make_inputs(B, N, Hq, Hkv, d, seed=0, device="cuda")
@@ -45,4 +46,11 @@ for t in (0, 1):  # t = softmax warpgroup (column half)
     period = d([E(2, j) for j in js], [E(2, j + 1) for j in js])
     res[f"tile{t}"] = {"n": len(js), "wait_for_S": f(wait), "softmax_X": f(X), "P_to_nextS": f(chain),
                        "mma_lag_after_P": f(lag), "period": f(period)}
+t0c = ev.get((30, 0))
+if t0c:
+    firstS = min(v for (e, a), v in ev.items() if e in (2, 6) and a == 0)
+    lastP = max(v for (e, a), v in ev.items() if e in (3, 7))
+    end = max(ev.get((31, 0), 0), ev.get((32, 0), 0))
+    res["cta"] = {"start_to_first_S": firstS - t0c, "first_S_to_last_P": lastP - firstS,
+                  "last_P_to_epilogue_end": end - lastP, "total": end - t0c}
 print(json.dumps(res, indent=1))
