@@ -10,9 +10,9 @@ import os
 
 # HK_LIB=debug selects the -DHK_DEBUG_HANG build (barrier waits trap with a message).
 # HK_LIB=trace selects the -DHK_TRACE build (in-kernel event trace, hk_diag_trace_read).
+# Any other HK_LIB=<name> loads libhkattn_<name>.so (A/B timing of a saved build).
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
-                         {"debug": "libhkattn_debug.so", "trace": "libhkattn_trace.so"}.get(
-                             os.environ.get("HK_LIB", ""), "libhkattn.so"))
+                         f"libhkattn_{os.environ['HK_LIB']}.so" if os.environ.get("HK_LIB") else "libhkattn.so")
 _lib = None
 
 HK_STATUS = {0: "HK_OK", 1: "HK_ERR_INVALID_ARGUMENT", 2: "HK_ERR_UNSUPPORTED",

@@ -102,7 +102,7 @@ struct BwdCfg {
   static constexpr uint32_t BAR_BYTES = 256;
   static constexpr uint32_t SLACK1 = (D == 128) ? 0 : 1024;
   static constexpr uint32_t SMEM1 = 2 * T128 + NSA * T128 + NSB * SLOT_B1 + BAR_BYTES + SLACK1;
-  // B2: Q_i, dO_i resident; ring A = {K_j}, ring B = {V_j}
+  // B2: ring A = {K_j}, ring B = {Q_i, dO_i, V_j ...} (NSB + 2 slots)
   static constexpr uint32_t SMEM2 = 2 * T128 + (NSA + NSB) * T128 + 1024;
   static constexpr int THREADS = 320;  // 8 elementwise warps + TMA warp + MMA warp
 };
@@ -418,55 +418,75 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ---------------------------------------------------------------- B2: dQ
-// CTA = (query tile iq, h, b); loop over 128-key blocks j.
-// Q_i and dO_i are resident, so after they land (TMA) the elementwise warps
-// copy them into TMEM and S = Q_i K_j^T and dP = dO_i V_j^T run with A from
-// TMEM: per block the tensor core then reads only K_j (twice) and V_j from
-// SMEM (96 KB instead of 160 KB), which with the 64 KB of TMA traffic keeps
-// the pass under the 128 B/clk shared-memory bandwidth.
+// Persistent: one CTA per SM walks work items (query tile iq, h, b), numbered
+// like the forward's (the G heads x tiles of one (b, kvh) group consecutive,
+// tiles fastest, heaviest first when causal) and taken in snake order.
+// Per item, loop over 128-key blocks j. Q_i and dO_i land (TMA) in two staging
+// tiles and the elementwise warps copy them into TMEM, so S = Q_i K_j^T and
+// dP = dO_i V_j^T run with A from TMEM: per block the tensor core then reads
+// only K_j (twice) and V_j from SMEM (96 KB instead of 160 KB), which with the
+// 64 KB of TMA traffic keeps the pass under the 128 B/clk shared-memory
+// bandwidth. The staging tiles are free again right after the
+// copy, so the next item's Q/dO stream in during the current item, and at the
+// item boundary the copy for the next item is done between reading dQ out of
+// TMEM and storing it.
 // TMEM: dQ [0,D)  S [D,D+128)  dP [D+128,D+256)  Q_A [D+256,D+256+D/2)  dO_A [+D/2);
 // bf16 dS overwrites dP. S is single-buffered but released as soon as the
 // elementwise warps have loaded it (bar_sfree), so S(j+1) still overlaps the
 // exponentials of block j. MMA order: S(j+1), dQ(j) [needs dS(j)], dP(j+1).
+struct DqItem {
+  int iq, h, kvh, b, n_it;
+};
+__device__ __forceinline__ int snake_item(int round, int cta, int ctas) {
+  return round * ctas + ((round & 1) ? ctas - 1 - cta : cta);
+}
+template <bool CAUSAL>
+__device__ __forceinline__ DqItem dq_decode(const BwdParams& p, int item) {
+  const int T = p.Np / 128;
+  const int G = p.Hq / p.Hkv;
+  const int tr = item % T;
+  int rest = item / T;
+  const int hg = rest % G;
+  rest /= G;
+  DqItem it;
+  it.kvh = rest % p.Hkv;
+  it.b = rest / p.Hkv;
+  it.h = it.kvh * G + hg;
+  it.iq = CAUSAL ? T - 1 - tr : tr;  // heaviest first
+  it.n_it = CAUSAL ? it.iq + 1 : T;  // 128-key blocks
+  return it;
+}
+
 template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(320, 1)
     bwd_dq_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapdO,
                   const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                   const BwdParams p) {
   using C = BwdCfg<D>;
-  // V ring: NSB slots of its own + 2 that reuse the Q_i / dO_i staging area once
-  // those are copied into TMEM (slot 0.. of ring B first, then sQ, sdO).
-  constexpr int NSA = C::NSA, NSB = C::NSB + 2;
+  // ring A = K_j; ring B (NSB + 2 slots) carries, per item, Q_i, dO_i, then V_0 .. V_{n-1}:
+  // the Q_i/dO_i slots are released once copied into TMEM, so V keeps a deep ring
+  // and the next item's Q_i/dO_i queue behind the current item's last V blocks.
+  constexpr int NSA = C::NSA, NB = C::NSB + 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sdO = smem + C::T128;
-  uint8_t* sA = smem + 2 * C::T128;   // ring A slot s: K_j [T128]
-  uint8_t* sB = sA + NSA * C::T128;   // ring B slot s: V_j [T128]
+  uint8_t* sA = smem;                 // ring A slot s: K_j [T128]
+  uint8_t* sB = sA + NSA * C::T128;   // ring B slot s: Q_i | dO_i | V_j [T128]
 
-  auto vslot = [&](int it) -> uint8_t* {
-    const int s = it % NSB;
-    return s < C::NSB ? sB + s * C::T128 : smem + (s - C::NSB) * C::T128;
-  };
-  __shared__ uint64_t bar_q, bar_qa, fullA[NSA], emptyA[NSA], fullB[NSB], emptyB[NSB], bar_s, bar_sfree, bar_dp,
-      bar_ds, bar_acc;
+  __shared__ uint64_t bar_qa, fullA[NSA], emptyA[NSA], fullB[NB], emptyB[NB], bar_s, bar_sfree, bar_dp, bar_ds,
+      bar_acc;
   __shared__ uint32_t tmem_base_s;
 
   const int warp = warp_id(), lane = lane_id();
-  const int T = p.Np / 128;
-  const int iq = CAUSAL ? (T - 1 - (int)blockIdx.x) : (int)blockIdx.x;  // query tile (heaviest first)
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int kvh = h / (p.Hq / p.Hkv);
-  const int n_it = CAUSAL ? iq + 1 : T;  // 128-key blocks
+  const int cta = blockIdx.x, ctas = gridDim.x;
+  const int num_items = p.B * p.Hq * (p.Np / 128);
 
   if (threadIdx.x == 0) {
-    mbar_init(&bar_q, 1);
     mbar_init(&bar_qa, 8);
     for (int s = 0; s < NSA; ++s) {
       mbar_init(&fullA[s], 1);
       mbar_init(&emptyA[s], 1);
     }
-    for (int s = 0; s < NSB; ++s) {
+    for (int s = 0; s < NB; ++s) {
       mbar_init(&fullB[s], 1);
       mbar_init(&emptyB[s], 1);
     }
@@ -490,34 +510,40 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t tb = tmem_base_s;
   const uint32_t tdQ = tb, tS = tb + D, tP = tb + D + 128, tQa = tb + D + 256, tdOa = tQa + D / 2;
 
+  // All roles walk the same items; ring uses and barrier phases run on across items.
   if (warp == 8) {
     if (lane == 0) {
       const uint64_t pol_keep = policy_evict_last();
       const uint64_t pol_stream = policy_evict_normal();
-      mbar_arrive_expect_tx(&bar_q, 2 * C::T128);
-      for (int pn = 0; pn < C::PANELS; ++pn) {
-        tma_load_4d(&mapQ, &bar_q, sQ + pn * 128 * 128, pn * 64, h, iq * 128, b, pol_stream);
-        tma_load_4d(&mapdO, &bar_q, sdO + pn * 128 * 128, pn * 64, h, iq * 128, b, pol_stream);
-      }
-      // K (ring A, freed after dQ) for block it+1 goes out right after V (ring B,
-      // freed after dP) for block it, keeping K one block ahead.
-      mbar_arrive_expect_tx(&fullA[0], C::T128);
-      for (int pn = 0; pn < C::PANELS; ++pn)
-        tma_load_4d(&mapK, &fullA[0], sA + pn * 128 * 128, pn * 64, kvh, 0, b, pol_keep);
-      for (int it = 0; it < n_it; ++it) {
-        const int sb = it % NSB;
-        mbar_wait(&emptyB[sb], ((it / NSB) & 1) ^ 1);
-        if (it == C::NSB) mbar_wait(&bar_qa, 0);  // Q/dO staging copied to TMEM: reuse it for V
+      int ua = 0, ub = 0;  // ring A / ring B uses so far
+      auto load_k = [&](const DqItem& w, int j) {
+        const int sa = ua % NSA;
+        mbar_wait(&emptyA[sa], ((ua / NSA) & 1) ^ 1);
+        mbar_arrive_expect_tx(&fullA[sa], C::T128);
+        for (int pn = 0; pn < C::PANELS; ++pn)
+          tma_load_4d(&mapK, &fullA[sa], sA + sa * C::T128 + pn * 128 * 128, pn * 64, w.kvh, j * 128, w.b, pol_keep);
+        ++ua;
+      };
+      auto load_b = [&](const CUtensorMap* map, int head, int row0, int b, uint64_t pol) {
+        const int sb = ub % NB;
+        mbar_wait(&emptyB[sb], ((ub / NB) & 1) ^ 1);
         mbar_arrive_expect_tx(&fullB[sb], C::T128);
         for (int pn = 0; pn < C::PANELS; ++pn)
-          tma_load_4d(&mapV, &fullB[sb], vslot(it) + pn * 128 * 128, pn * 64, kvh, it * 128, b, pol_keep);
-        if (it + 1 < n_it) {
-          const int sa = (it + 1) % NSA;
-          mbar_wait(&emptyA[sa], (((it + 1) / NSA) & 1) ^ 1);
-          mbar_arrive_expect_tx(&fullA[sa], C::T128);
-          for (int pn = 0; pn < C::PANELS; ++pn)
-            tma_load_4d(&mapK, &fullA[sa], sA + sa * C::T128 + pn * 128 * 128, pn * 64, kvh, (it + 1) * 128, b,
-                        pol_keep);
+          tma_load_4d(map, &fullB[sb], sB + sb * C::T128 + pn * 128 * 128, pn * 64, head, row0, b, pol);
+        ++ub;
+      };
+      for (int r = 0;; ++r) {
+        const int item = snake_item(r, cta, ctas);
+        if (item >= num_items) break;
+        const DqItem w = dq_decode<CAUSAL>(p, item);
+        load_b(&mapQ, w.h, w.iq * 128, w.b, pol_stream);
+        load_b(&mapdO, w.h, w.iq * 128, w.b, pol_stream);
+        // K (ring A, freed after dQ) for block it+1 goes out right after V (ring B,
+        // freed after dP) for block it, keeping K one block ahead.
+        load_k(w, 0);
+        for (int it = 0; it < w.n_it; ++it) {
+          load_b(&mapV, w.kvh, it * 128, w.b, pol_keep);
+          if (it + 1 < w.n_it) load_k(w, it + 1);
         }
       }
     }
@@ -527,67 +553,88 @@ __global__ void __launch_bounds__(320, 1)
     constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);   // dQ += dS K_j: K_j MN-major
     constexpr uint64_t KMAJ = sdesc_sw128_const(16, 1024);
     constexpr uint64_t MNMAJ = sdesc_sw128_const(128 * 128, 1024);
-    const uint32_t aA = smem_u32(sA);
+    const uint32_t aA = smem_u32(sA), aB = smem_u32(sB);
     auto kmaj = [&](uint32_t base, int kk) { return KMAJ | ((base + (kk / 4) * 128 * 128 + (kk % 4) * 32) >> 4); };
     auto mnmaj = [&](uint32_t base, int kk) { return MNMAJ | ((base + kk * 16 * 128) >> 4); };
-    auto slotK = [&](int it) { return aA + (it % NSA) * C::T128; };
-    auto slotV = [&](int it) { return smem_u32(vslot(it)); };
-    auto issue_s = [&](int it) {
-      hk_trace(13, it, 1);  // MMA: S(it) issue
-      const uint32_t k = slotK(it);
+    int ua = 0, ub = 0;  // ring A / ring B uses so far
+    uint32_t g = 0;      // blocks so far (phase of bar_s, bar_sfree, bar_dp, bar_ds)
+    uint32_t qa_ph = 0;
+    auto issue_s = [&](int u) {
+      const uint32_t k = aA + (u % NSA) * C::T128;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) umma_ts_w(tS, tQa + kk * 8, kmaj(k, kk), idesc_sp, kk > 0);
       tc_commit_w(&bar_s);
     };
-    auto issue_dp = [&](int it) {
-      hk_trace(14, it, 1);  // MMA: dP(it) issue
-      const uint32_t v = slotV(it);
+    auto issue_dp = [&](int u, bool release) {
+      const uint32_t v = aB + (u % NB) * C::T128;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) umma_ts_w(tP, tdOa + kk * 8, kmaj(v, kk), idesc_sp, kk > 0);
       tc_commit_w(&bar_dp);
-      if (it + NSB < n_it) tc_commit_w(&emptyB[it % NSB]);  // V(it): dP(it) is its only use
+      if (release) tc_commit_w(&emptyB[u % NB]);  // V: dP is its only use
     };
-    mbar_wait(&bar_qa, 0);  // Q_A, dO_A written to TMEM by the elementwise warps
-    mbar_wait(&fullA[0], 0);
-    tc_fence_after();
-    issue_s(0);
-    mbar_wait(&fullB[0], 0);
-    tc_fence_after();
-    issue_dp(0);
-    for (int it = 0; it < n_it; ++it) {
-      const bool more = it + 1 < n_it;
-      if (more) {
-        mbar_wait(&bar_sfree, it & 1);  // S(it) loaded by the elementwise warps
-        mbar_wait(&fullA[(it + 1) % NSA], ((it + 1) / NSA) & 1);
-        tc_fence_after();
-        issue_s(it + 1);
+    for (int r = 0;; ++r) {
+      const int item = snake_item(r, cta, ctas);
+      if (item >= num_items) break;
+      const DqItem w = dq_decode<CAUSAL>(p, item);
+      // in the CTA's last item, releases nobody waits for are skipped (no arrive after exit)
+      const bool last_item = snake_item(r + 1, cta, ctas) >= num_items;
+      const int n = w.n_it;
+      const int a0 = ua, v0 = ub + 2;  // ring B: Q_i at ub, dO_i at ub + 1, V_j at v0 + j
+      mbar_wait(&bar_qa, qa_ph);        // Q_A, dO_A of this item in TMEM
+      qa_ph ^= 1;
+      if (lane == 0) {  // their staging slots are free
+        mbar_arrive(&emptyB[ub % NB]);
+        mbar_arrive(&emptyB[(ub + 1) % NB]);
       }
-      mbar_wait(&bar_ds, it & 1);
+      mbar_wait(&fullA[a0 % NSA], (a0 / NSA) & 1);
       tc_fence_after();
-      hk_trace(11, it, 1);  // MMA: dS(it) seen, dQ issue
-      {
-        const uint32_t k = slotK(it);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_ts_w(tdQ, tP + packed_col(kk), mnmaj(k, kk), idesc_acc, (it > 0 || kk > 0) ? 1u : 0u);
-      }
-      if (it + NSA < n_it) tc_commit_w(&emptyA[it % NSA]);  // K(it): last use dQ(it)
-      if (more) {  // dP(it+1) overwrites dS(it): after dQ(it) in issue order
-        mbar_wait(&fullB[(it + 1) % NSB], ((it + 1) / NSB) & 1);
+      issue_s(a0);
+      mbar_wait(&fullB[v0 % NB], (v0 / NB) & 1);
+      tc_fence_after();
+      issue_dp(v0, !last_item || NB - 2 < n);
+      for (int it = 0; it < n; ++it, ++g) {
+        const bool more = it + 1 < n;
+        mbar_wait(&bar_sfree, g & 1);  // S(it) loaded by the elementwise warps
+        if (more) {
+          const int u = a0 + it + 1;
+          mbar_wait(&fullA[u % NSA], (u / NSA) & 1);
+          tc_fence_after();
+          issue_s(u);
+        }
+        mbar_wait(&bar_ds, g & 1);
         tc_fence_after();
-        issue_dp(it + 1);
+        hk_trace(11, g, 1);  // MMA: dS(it) seen, dQ issue
+        {
+          const uint32_t k = aA + ((a0 + it) % NSA) * C::T128;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_ts_w(tdQ, tP + packed_col(kk), mnmaj(k, kk), idesc_acc, (it > 0 || kk > 0) ? 1u : 0u);
+        }
+        if (!last_item || it + NSA < n) tc_commit_w(&emptyA[(a0 + it) % NSA]);  // K(it): last use dQ(it)
+        if (more) {  // dP(it+1) overwrites dS(it): after dQ(it) in issue order
+          const int u = v0 + it + 1;
+          mbar_wait(&fullB[u % NB], (u / NB) & 1);
+          tc_fence_after();
+          issue_dp(u, !last_item || it + 1 + NB - 2 < n);
+        }
       }
+      tc_commit_w(&bar_acc);
+      ua += n;
+      ub += n + 2;
     }
-    tc_commit_w(&bar_acc);
   } else {
     const int wg = warp >> 2;              // key columns [64 wg, 64 wg + 64) of each block
     const uint32_t lb = (warp & 3) * 32;
     const int r = (warp & 3) * 32 + lane;  // query row within the tile
-    const int q = iq * 128 + r;
-    // ---- prologue: WG0 copies Q_i, WG1 dO_i from swizzled SMEM rows into TMEM (A operands)
-    mbar_wait(&bar_q, 0);
-    {
-      const uint8_t* src = wg == 0 ? sQ : sdO;
+    const float c = 1.4426950408889634f / sqrtf((float)D);
+    const uint32_t cP = tP + 64 * wg, cS = tS + 64 * wg;
+    uint32_t g = 0, acc_ph = 0;
+    int ub = 0;  // ring B uses so far (Q_i of the current item sits at ub, dO_i at ub + 1)
+    // WG0 copies Q_i, WG1 dO_i from swizzled SMEM rows into TMEM (A operands)
+    auto copy_in = [&]() {
+      const int u = ub + wg;
+      mbar_wait(&fullB[u % NB], (u / NB) & 1);
+      const uint8_t* src = sB + (u % NB) * C::T128;
       const uint32_t dst = wg == 0 ? tQa : tdOa;
 #pragma unroll
       for (int pn = 0; pn < C::PANELS; ++pn) {
@@ -605,71 +652,79 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_qa);
-    }
-    const float c = 1.4426950408889634f / sqrtf((float)D);
-    const size_t vrow = ((size_t)b * p.Hq + h) * p.Np + q;
-    const float l2 = p.lse2[vrow], Dq = p.Dv[vrow];
-    const uint32_t cP = tP + 64 * wg, cS = tS + 64 * wg;
-    for (int it = 0; it < n_it; ++it) {
-      float v[64];
-      if (threadIdx.x == 0) hk_trace(1, it, 1);
-      mbar_wait(&bar_s, it & 1);
-      tc_fence_after();
-      if (threadIdx.x == 0) hk_trace(2, it, 1);
-      tmem_ld64(tmem_addr(cS, lb, 0), v);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_sfree);  // S buffer free for S(it+1)
+    };
+    if (snake_item(0, cta, ctas) < num_items) copy_in();
+    for (int rr = 0;; ++rr) {
+      const int item = snake_item(rr, cta, ctas);
+      if (item >= num_items) break;
+      const DqItem w = dq_decode<CAUSAL>(p, item);
+      const int q = w.iq * 128 + r;
+      const size_t vrow = ((size_t)w.b * p.Hq + w.h) * p.Np + q;
+      const float l2 = p.lse2[vrow], Dq = p.Dv[vrow];
+      for (int it = 0; it < w.n_it; ++it, ++g) {
+        float v[64];
+        if (threadIdx.x == 0) hk_trace(1, g, 1);
+        mbar_wait(&bar_s, g & 1);
+        tc_fence_after();
+        if (threadIdx.x == 0) hk_trace(2, g, 1);
+        tmem_ld64(tmem_addr(cS, lb, 0), v);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_sfree);  // S buffer free for S(it+1)
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const float2 e = bwd_exp2_pair<BWD_EMU_OF_8>(
-            fma2(make_float2(v[2 * k], v[2 * k + 1]), make_float2(c, c), make_float2(-l2, -l2)), k);
-        v[2 * k] = e.x;
-        v[2 * k + 1] = e.y;
+        for (int k = 0; k < 32; ++k) {
+          const float2 e = bwd_exp2_pair<BWD_EMU_OF_8>(
+              fma2(make_float2(v[2 * k], v[2 * k + 1]), make_float2(c, c), make_float2(-l2, -l2)), k);
+          v[2 * k] = e.x;
+          v[2 * k + 1] = e.y;
+        }
+        if (CAUSAL && it == w.iq) {
+          const int k0 = it * 128 + 64 * wg;
+#pragma unroll
+          for (int cc = 0; cc < 64; ++cc)
+            if (k0 + cc > q) v[cc] = 0.f;
+        }
+        if (threadIdx.x == 0) hk_trace(3, g, 1);
+        mbar_wait(&bar_dp, g & 1);
+        tc_fence_after();
+        if (threadIdx.x == 0) hk_trace(4, g, 1);
+        float dp[64];
+        tmem_ld64(tmem_addr(cP, lb, 0), dp);
+        tmem_wait_ld();
+#pragma unroll
+        for (int cc = 0; cc < 64; ++cc) dp[cc] = v[cc] * (dp[cc] - Dq);
+        tmem_st_packed64(tmem_addr(cP, lb, 0), dp);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_ds);
+        if (threadIdx.x == 0) hk_trace(5, g, 1);
       }
-      if (CAUSAL && it == iq) {
-        const int k0 = it * 128 + 64 * wg;
-#pragma unroll
-        for (int cc = 0; cc < 64; ++cc)
-          if (k0 + cc > q) v[cc] = 0.f;
-      }
-      if (threadIdx.x == 0) hk_trace(3, it, 1);
-      mbar_wait(&bar_dp, it & 1);
+      ub += w.n_it + 2;
+      // ---- epilogue: dQ * (1/sqrt d); WG0 writes columns [0, D/2), WG1 [D/2, D)
+      mbar_wait(&bar_acc, acc_ph);
+      acc_ph ^= 1;
       tc_fence_after();
-      if (threadIdx.x == 0) hk_trace(4, it, 1);
-      float dp[64];
-      tmem_ld64(tmem_addr(cP, lb, 0), dp);
+      uint32_t o[D / 2];
+#pragma unroll
+      for (int c0 = 0; c0 < D / 2; c0 += 32)
+        tmem_ld32(tmem_addr(tdQ, lb, wg * (D / 2) + c0), *reinterpret_cast<uint32_t(*)[32]>(&o[c0]));
       tmem_wait_ld();
+      // the next item's Q/dO go into TMEM before dQ is stored: its S/dP start now.
+      // (Its dQ MMAs, which overwrite this accumulator, follow this WG's reads.)
+      if (snake_item(rr + 1, cta, ctas) < num_items) copy_in();
+      const float scale = rsqrtf((float)D);
+      const bool q_ok = q < p.N;  // query rows of a ragged last tile beyond N are not stored
+      __nv_bfloat16* out = p.dq + (((size_t)w.b * p.N + (q_ok ? q : 0)) * p.Hq + w.h) * D + wg * (D / 2);
 #pragma unroll
-      for (int cc = 0; cc < 64; ++cc) dp[cc] = v[cc] * (dp[cc] - Dq);
-      tmem_st_packed64(tmem_addr(cP, lb, 0), dp);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_ds);
-      if (threadIdx.x == 0) hk_trace(5, it, 1);
-    }
-    // ---- epilogue: dQ * (1/sqrt d); WG0 writes columns [0, D/2), WG1 [D/2, D)
-    mbar_wait(&bar_acc, 0);
-    tc_fence_after();
-    const float scale = rsqrtf((float)D);
-    const bool q_ok = q < p.N;  // query rows of a ragged last tile beyond N are not stored
-    __nv_bfloat16* out = p.dq + (((size_t)b * p.N + (q_ok ? q : 0)) * p.Hq + h) * D;
-#pragma unroll
-    for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
-      uint32_t o[32];
-      tmem_ld32(tmem_addr(tdQ, lb, c0), o);
-      tmem_wait_ld();
-      uint4 o4[4];
-      uint32_t* op = reinterpret_cast<uint32_t*>(o4);
-#pragma unroll
-      for (int k = 0; k < 16; ++k)
-        op[k] = pack_bf16(__uint_as_float(o[2 * k]) * scale, __uint_as_float(o[2 * k + 1]) * scale);
-      uint4* dst = reinterpret_cast<uint4*>(out + c0);
-      if (q_ok) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) dst[k] = o4[k];
+      for (int c0 = 0; c0 < D / 2; c0 += 8) {
+        uint4 o4;
+        o4.x = pack_bf16(__uint_as_float(o[c0 + 0]) * scale, __uint_as_float(o[c0 + 1]) * scale);
+        o4.y = pack_bf16(__uint_as_float(o[c0 + 2]) * scale, __uint_as_float(o[c0 + 3]) * scale);
+        o4.z = pack_bf16(__uint_as_float(o[c0 + 4]) * scale, __uint_as_float(o[c0 + 5]) * scale);
+        o4.w = pack_bf16(__uint_as_float(o[c0 + 6]) * scale, __uint_as_float(o[c0 + 7]) * scale);
+        if (q_ok) *reinterpret_cast<uint4*>(out + c0) = o4;
       }
     }
   }
@@ -688,7 +743,7 @@ inline bool set_smem(F* fn, uint32_t bytes) {
 template <int D, bool CAUSAL>
 hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,
                        void* dQ, void* dK, void* dV, float* ws, int B, int Hq, int Hkv, int N, cudaStream_t stream,
-                       char* err, size_t errlen, int phase) {
+                       char* err, size_t errlen, int phase, int num_sms) {
   using C = BwdCfg<D>;
   const int Np = (N + 127) / 128 * 128;  // workspace rows padded to whole tiles
   float* Dv = ws;
@@ -725,8 +780,10 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   // B1, B2
   if (phase < 0 || phase == 1)
     bwd_dkdv_kernel<D, CAUSAL><<<dim3(Np / 128, Hkv, B), C::THREADS, C::SMEM1, stream>>>(mQ, mdO, mK, mV, p);
-  if (phase < 0 || phase == 2)
-    bwd_dq_kernel<D, CAUSAL><<<dim3(Np / 128, Hq, B), C::THREADS, C::SMEM2, stream>>>(mQ, mdO, mK, mV, p);
+  if (phase < 0 || phase == 2) {
+    const int items = B * Hq * (Np / 128);  // persistent: one CTA per SM
+    bwd_dq_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS, C::SMEM2, stream>>>(mQ, mdO, mK, mV, p);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(err, errlen, "hk_attn_bwd launch failed: %s", cudaGetErrorString(e));
@@ -737,12 +794,13 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
 
 inline hk_status launch_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                             const void* dO, void* dQ, void* dK, void* dV, float* ws, int B, int Hq, int Hkv, int N,
-                            int d, bool causal, cudaStream_t stream, char* err, size_t errlen, int phase) {
+                            int d, bool causal, cudaStream_t stream, char* err, size_t errlen, int phase,
+                            int num_sms) {
   if (d == 64)
-    return causal ? launch_bwd_t<64, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase)
-                  : launch_bwd_t<64, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase);
-  return causal ? launch_bwd_t<128, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase)
-                : launch_bwd_t<128, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase);
+    return causal ? launch_bwd_t<64, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase, num_sms)
+                  : launch_bwd_t<64, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase, num_sms);
+  return causal ? launch_bwd_t<128, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase, num_sms)
+                : launch_bwd_t<128, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase, num_sms);
 }
 
 }  // namespace hk

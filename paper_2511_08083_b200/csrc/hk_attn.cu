@@ -134,10 +134,11 @@ static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V
       if (overlaps(outs[i], out_sz[i], outs[k], out_sz[k]))
         return fail(HK_ERR_INVALID_ARGUMENT, "outputs/workspace must not alias each other");
   }
-  s = check_device(nullptr);
+  int num_sms = 0;
+  s = check_device(&num_sms);
   if (s != HK_OK) return s;
   return hk::launch_bwd(Q, K, V, O, LSE, dO, dQ, dK, dV, reinterpret_cast<float*>(workspace), B, Hq, Hkv, N, d,
-                        causal != 0, stream, g_err, sizeof(g_err), phase);
+                        causal != 0, stream, g_err, sizeof(g_err), phase, num_sms);
 }
 
 extern "C" {

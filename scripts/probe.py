@@ -46,6 +46,7 @@ def main():
     ap.add_argument("--configs", default="C2-nc,C2-c,C3,C4-8192")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--bwd", action="store_true")
+    ap.add_argument("--phases", action="store_true", help="time bwd pre / dkdv / dq separately")
     a = ap.parse_args()
     for name in a.configs.split(","):
         B, N, Hq, Hkv, d, causal = CONFIGS[name]
@@ -59,6 +60,22 @@ def main():
             ms_b = timeit(lambda: attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, dq=dq, dk=dk, dv=dv),
                           a.iters, 3)
             rec.update(bwd_ms=round(ms_b, 4), bwd_tflops=round(2.5 * flops / ms_b / 1e9, 1))
+            if a.phases:
+                import ctypes
+                from paper_2511_08083_b200 import _lib
+                from paper_2511_08083_b200.api import bwd_workspace_bytes
+                L = _lib.lib()
+                ws = torch.empty(bwd_workspace_bytes(B, Hq, Hkv, N, d) // 4, device="cuda", dtype=torch.float32)
+                P = lambda t: ctypes.c_void_p(t.data_ptr())
+                sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+                for ph, name, fl in ((0, "pre", 0), (1, "dkdv", 2.0), (2, "dq", 1.5)):
+                    f = lambda: _lib.check(L.hk_diag_bwd_phase(ph, P(x["Q"]), P(x["K"]), P(x["V"]), P(o), P(lse),
+                                                               P(x["dO"]), P(dq), P(dk), P(dv), P(ws), ws.numel() * 4,
+                                                               B, Hq, Hkv, N, d, int(causal), sp))
+                    t = timeit(f, a.iters, 2)
+                    rec[name + "_ms"] = round(t, 4)
+                    if fl:
+                        rec[name + "_tflops"] = round(fl * flops / t / 1e9, 1)
         print(json.dumps(rec), flush=True)
         del x
 
