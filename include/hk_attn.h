@@ -52,8 +52,11 @@ typedef enum {
 hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, float* LSE, int B, int Hq,
                       int Hkv, int N, int d, int causal, cudaStream_t stream);
 
-/* Bytes of fp32 workspace hk_attn_bwd needs: D = rowsum(dO * O) and LSE*log2(e),
- * each [B][Hq][Np] fp32 with Np = N rounded up to a multiple of 128, i.e. 2*B*Hq*Np*4. */
+/* Bytes of workspace hk_attn_bwd needs: D = rowsum(dO * O) and LSE*log2(e),
+ * each [B][Hq][Np] fp32 with Np = N rounded up to a multiple of 128, then 256 bytes
+ * of work counters for the persistent kernels: 2*B*Hq*Np*4 + 256. The call
+ * initialises all of it (no zeroing needed); calls sharing one workspace must be
+ * stream-ordered. */
 size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d);
 
 /* Backward: given Q, K, V, the forward's O and LSE, and dO, writes dQ, dK, dV

@@ -30,7 +30,9 @@ template <int D>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ O,
                                                       const __nv_bfloat16* __restrict__ dO,
                                                       const float* __restrict__ lse, float* __restrict__ Dout,
-                                                      float* __restrict__ lse2, int B, int N, int H, int Np) {
+                                                      float* __restrict__ lse2, int B, int N, int H, int Np,
+                                                      unsigned* __restrict__ sched) {
+  if (blockIdx.x == 0 && threadIdx.x < 4) sched[threadIdx.x] = 0u;
   constexpr int LPR = D / 8;  // lanes per row
   constexpr int RPW = 32 / LPR;
   const size_t rows = (size_t)B * N * H;
@@ -80,8 +82,63 @@ struct BwdParams {
   __nv_bfloat16* dq;  // [B][N][Hq][D]
   __nv_bfloat16* dk;  // [B][N][Hkv][D]
   __nv_bfloat16* dv;  // [B][N][Hkv][D]
+  unsigned* sched;    // [4] work counters in the workspace: dK/dV draw, done; dQ draw, done
   int B, Hq, Hkv, N, Np;
 };
+
+// Dynamic work distribution for the persistent backward kernels: the TMA lane
+// draws item indices from a global counter (so the CTAs work through one
+// contiguous, heaviest-first window of items: balanced, and the items in
+// flight share their Q/dO or K/V in L2) and hands each draw to the MMA warp and
+// the 8 elementwise warps through a 2-entry ring in shared memory. A draw
+// >= the item count ends every role. The CTA that finishes last resets the
+// counters for the next launch; the pre-kernel zeroes them too.
+constexpr int SCHED_NQ = 2;
+struct Sched {
+  uint64_t full[SCHED_NQ], empty[SCHED_NQ];
+  int item[SCHED_NQ];
+};
+__device__ __forceinline__ void sched_init(Sched& q) {
+  for (int i = 0; i < SCHED_NQ; ++i) {
+    mbar_init(&q.full[i], 1);
+    mbar_init(&q.empty[i], 9);  // the MMA warp + 8 elementwise warps
+  }
+}
+// producer lane: draw number k
+__device__ __forceinline__ int sched_publish(Sched& q, unsigned* ctr, int k) {
+  const int i = k % SCHED_NQ;
+  mbar_wait(&q.empty[i], ((k / SCHED_NQ) & 1) ^ 1);
+  const int item = (int)atomicAdd(ctr, 1u);
+  *reinterpret_cast<volatile int*>(&q.item[i]) = item;
+  mbar_arrive(&q.full[i]);
+  return item;
+}
+// consumer (whole warp): draw number k
+__device__ __forceinline__ int sched_take(Sched& q, int k) {
+  const int i = k % SCHED_NQ;
+  mbar_wait(&q.full[i], (k / SCHED_NQ) & 1);
+  // lane 0's copy via shfl: ptxas then treats the index (and everything the MMA
+  // warp derives from it) as warp-uniform, keeping descriptors in uniform registers
+  const int item = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile int*>(&q.item[i]), 0);
+  if (lane_id() == 0) mbar_arrive(&q.empty[i]);
+  return item;
+}
+// last CTA out resets the draw counter (ctr[0]) and the exit counter (ctr[1])
+__device__ __forceinline__ void sched_exit(unsigned* ctr) {
+  __threadfence();
+  if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+    atomicExch(ctr, 0u);
+    atomicExch(ctr + 1, 0u);
+  }
+}
+// Wait until the last release committed on each slot of a ring (U uses so far)
+// has landed, so no asynchronous arrive is still in flight when the CTA exits.
+__device__ __forceinline__ void drain_ring(uint64_t* empty, int ns, int U) {
+  for (int s = 0; s < ns && s < U; ++s) {
+    const int last = U - 1 - ((U - 1 - s) % ns);
+    mbar_wait(&empty[s], (last / ns) & 1);
+  }
+}
 
 // 128 x 128 tiles throughout: tcgen05.mma with N=64 paces at 48 cycles per
 // K=16 step instead of 32 (measured, scripts/rates.py), N=128 at full rate.
@@ -147,12 +204,36 @@ __device__ __forceinline__ void tmem_st_packed64(uint32_t taddr, const float (&v
 }
 
 // ---------------------------------------------------------------- B1: dK, dV
-// CTA = (key tile jt, kvh, b); loop h in the GQA group x 128-row query blocks qi.
+// Persistent: one CTA per SM draws work items (key tile jt, kvh, b) from the
+// dynamic scheduler (items numbered tiles fastest, heaviest first when causal;
+// consecutive items share the Q/dO of their (b, kvh) group in L2). Per item: loop h in the GQA group x
+// 128-row query blocks qi. K_j, V_j are resident; once the item's last S^T and
+// dP^T completed (bar_kvfree) the next item's K, V load into the same tiles
+// while this item finishes; the Q and dO rings run on across items.
 // TMEM: dV [0,D)  dK [D,2D)  S^T [2D,2D+128)  dP^T [2D+128,2D+256); bf16 P^T / dS^T
 // overwrite the first half of each warpgroup's columns of S^T / dP^T.
 // MMA order per block: dV(i) [needs P^T(i)], S^T(i+1), dK(i) [needs dS^T(i)],
 // dP^T(i+1): the exponentials of block i+1 overlap dK(i)/dP^T(i+1) and the dS
-// work overlaps dV(i+1)/S^T(i+2).
+// work overlaps dV(i+1)/S^T(i+2). The next item's first dV/dK (which overwrite
+// the accumulators) need its first P^T/dS^T, which the elementwise warps
+// publish only after reading this item's dV/dK out.
+struct KvItem {
+  int jt, kvh, b, i0, n_it;
+};
+template <bool CAUSAL>
+__device__ __forceinline__ KvItem kv_decode(const BwdParams& p, int item) {
+  const int T = p.Np / 128;
+  const int tr = item % T;
+  const int rest = item / T;
+  KvItem it;
+  it.kvh = rest % p.Hkv;
+  it.b = rest / p.Hkv;
+  it.jt = CAUSAL ? T - 1 - tr : tr;  // heaviest first
+  it.i0 = CAUSAL ? it.jt : 0;        // first query block that sees key tile jt
+  it.n_it = (p.Hq / p.Hkv) * (T - it.i0);
+  return it;
+}
+
 template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(320, 1)
     bwd_dkdv_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapdO,
@@ -178,20 +259,20 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t& bar_p = emptyB[NSB + 3];
   uint64_t& bar_ds = emptyB[NSB + 4];
   uint64_t& bar_acc = emptyB[NSB + 5];
-  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(emptyB + NSB + 6);
-  static_assert((2 * NSA + 2 * NSB + 7) * 8 <= C::BAR_BYTES, "barrier area");
+  uint64_t& bar_kvfree = emptyB[NSB + 6];
+  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(emptyB + NSB + 7);
+  Sched& sched = *reinterpret_cast<Sched*>(emptyB + NSB + 8);
+  static_assert((2 * NSA + 2 * NSB + 8) * 8 + sizeof(Sched) <= C::BAR_BYTES, "barrier area");
 
   const int warp = warp_id(), lane = lane_id();
   const int T = p.Np / 128;
-  const int jt = CAUSAL ? (T - 1 - (int)blockIdx.x) : (int)blockIdx.x;  // key tile (heaviest first)
-  const int kvh = blockIdx.y, b = blockIdx.z;
   const int G = p.Hq / p.Hkv;
-  const int i0 = CAUSAL ? jt : 0;  // first query block that sees key tile jt
-  const int per_h = T - i0;
-  const int n_it = G * per_h;
+  const int num_items = p.B * p.Hkv * T;
 
   if (threadIdx.x == 0) {
+    sched_init(sched);
     mbar_init(&bar_kv, 1);
+    mbar_init(&bar_kvfree, 1);
     for (int s = 0; s < NSA; ++s) {
       mbar_init(&fullA[s], 1);
       mbar_init(&emptyA[s], 1);
@@ -217,40 +298,52 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tb = tmem_base_s;
+  const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base_s, 0);  // warp-uniform for ptxas (UR operands)
   const uint32_t tdV = tb, tdK = tb + D, tS = tb + 2 * D, tP = tb + 2 * D + 128;
 
+  // All roles walk the same items; ring uses and barrier phases run on across items.
   if (warp == 8) {
     // ================= TMA producer =================
     if (lane == 0) {
       const uint64_t pol_keep = policy_evict_last();
       const uint64_t pol_stream = policy_evict_normal();
-      mbar_arrive_expect_tx(&bar_kv, 2 * C::T128);
-      for (int pn = 0; pn < C::PANELS; ++pn) {
-        tma_load_4d(&mapK, &bar_kv, sK + pn * 128 * 128, pn * 64, kvh, jt * 128, b, pol_stream);
-        tma_load_4d(&mapV, &bar_kv, sV + pn * 128 * 128, pn * 64, kvh, jt * 128, b, pol_stream);
-      }
-      // blocking waits (the hardware suspends the warp: no issue slots taken
-      // from the elementwise warps sharing its SM sub-partition)
-      int h = kvh * G, qi = i0;
-      for (int it = 0; it < n_it; ++it) {
-        const int sa = it % NSA, sb = it % NSB;
-        mbar_wait(&emptyA[sa], ((it / NSA) & 1) ^ 1);
-        hk_trace(20, it, 0);  // producer: ring A slot free, loads for it issued
-        mbar_arrive_expect_tx(&fullA[sa], C::T128);
-        for (int pn = 0; pn < C::PANELS; ++pn)
-          tma_load_4d(&mapQ, &fullA[sa], sA + sa * C::T128 + pn * 128 * 128, pn * 64, h, qi * 128, b, pol_keep);
-        mbar_wait(&emptyB[sb], ((it / NSB) & 1) ^ 1);
-        uint8_t* st = sB + sb * C::SLOT_B1;
-        mbar_arrive_expect_tx(&fullB[sb], C::T128 + 1024);
-        for (int pn = 0; pn < C::PANELS; ++pn)
-          tma_load_4d(&mapdO, &fullB[sb], st + pn * 128 * 128, pn * 64, h, qi * 128, b, pol_keep);
-        const size_t off = ((size_t)b * p.Hq + h) * p.Np + (size_t)qi * 128;
-        bulk_load(st + C::T128, p.lse2 + off, 512, &fullB[sb]);
-        bulk_load(st + C::T128 + 512, p.Dv + off, 512, &fullB[sb]);
-        if (++qi == T) {
-          qi = i0;
-          ++h;
+      int u = 0;  // ring uses so far (rings A and B advance together, one use per block)
+      uint32_t kvf_ph = 0;
+      for (int r = 0;; ++r) {
+        const int item = sched_publish(sched, p.sched, r);
+        if (item >= num_items) break;
+        const KvItem w = kv_decode<CAUSAL>(p, item);
+        if (r > 0) {  // K, V tiles free once the previous item's last S^T / dP^T completed
+          mbar_wait(&bar_kvfree, kvf_ph);
+          kvf_ph ^= 1;
+        }
+        mbar_arrive_expect_tx(&bar_kv, 2 * C::T128);
+        for (int pn = 0; pn < C::PANELS; ++pn) {
+          tma_load_4d(&mapK, &bar_kv, sK + pn * 128 * 128, pn * 64, w.kvh, w.jt * 128, w.b, pol_stream);
+          tma_load_4d(&mapV, &bar_kv, sV + pn * 128 * 128, pn * 64, w.kvh, w.jt * 128, w.b, pol_stream);
+        }
+        // blocking waits (the hardware suspends the warp: no issue slots taken
+        // from the elementwise warps sharing its SM sub-partition)
+        int h = w.kvh * G, qi = w.i0;
+        for (int it = 0; it < w.n_it; ++it, ++u) {
+          const int sa = u % NSA, sb = u % NSB;
+          mbar_wait(&emptyA[sa], ((u / NSA) & 1) ^ 1);
+          hk_trace(20, u, 0);  // producer: ring A slot free, loads for it issued
+          mbar_arrive_expect_tx(&fullA[sa], C::T128);
+          for (int pn = 0; pn < C::PANELS; ++pn)
+            tma_load_4d(&mapQ, &fullA[sa], sA + sa * C::T128 + pn * 128 * 128, pn * 64, h, qi * 128, w.b, pol_keep);
+          mbar_wait(&emptyB[sb], ((u / NSB) & 1) ^ 1);
+          uint8_t* st = sB + sb * C::SLOT_B1;
+          mbar_arrive_expect_tx(&fullB[sb], C::T128 + 1024);
+          for (int pn = 0; pn < C::PANELS; ++pn)
+            tma_load_4d(&mapdO, &fullB[sb], st + pn * 128 * 128, pn * 64, h, qi * 128, w.b, pol_keep);
+          const size_t off = ((size_t)w.b * p.Hq + h) * p.Np + (size_t)qi * 128;
+          bulk_load(st + C::T128, p.lse2 + off, 512, &fullB[sb]);
+          bulk_load(st + C::T128 + 512, p.Dv + off, 512, &fullB[sb]);
+          if (++qi == T) {
+            qi = w.i0;
+            ++h;
+          }
         }
       }
     }
@@ -263,164 +356,184 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aA = smem_u32(sA), aB = smem_u32(sB);
     auto kmaj = [&](uint32_t base, int kk) { return KMAJ | ((base + (kk / 4) * 128 * 128 + (kk % 4) * 32) >> 4); };
     auto mnmaj = [&](uint32_t base, int kk) { return MNMAJ | ((base + kk * 16 * 128) >> 4); };
-    auto slotQ = [&](int it) { return aA + (it % NSA) * C::T128; };
-    auto slotO = [&](int it) { return aB + (it % NSB) * C::SLOT_B1; };
-    auto issue_s = [&](int it) {
-      const uint32_t q = slotQ(it);
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) umma_ss_w(tS, kmaj(aK, kk), kmaj(q, kk), idesc_sp, kk > 0);
+    auto slotQ = [&](int u) { return aA + (u % NSA) * C::T128; };
+    auto slotO = [&](int u) { return aB + (u % NSB) * C::SLOT_B1; };
+    auto issue_s = [&](int u) {
+      gemm_ss_kk<D / 16>(tS, kmaj(aK, 0), kmaj(slotQ(u), 0), idesc_sp, 0u);
       tc_commit_w(&bar_s);
     };
-    auto issue_dp = [&](int it) {
-      hk_trace(14, it, 0);  // MMA: dP^T(it) issue
-      const uint32_t dO = slotO(it);
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) umma_ss_w(tP, kmaj(aV, kk), kmaj(dO, kk), idesc_sp, kk > 0);
+    auto issue_dp = [&](int u) {
+      hk_trace(14, u, 0);  // MMA: dP^T(u) issue
+      gemm_ss_kk<D / 16>(tP, kmaj(aV, 0), kmaj(slotO(u), 0), idesc_sp, 0u);
       tc_commit_w(&bar_dp);
     };
-    mbar_wait(&bar_kv, 0);
-    mbar_wait(&fullA[0], 0);
-    tc_fence_after();
-    issue_s(0);
-    mbar_wait(&fullB[0], 0);
-    tc_fence_after();
-    issue_dp(0);
-    for (int it = 0; it < n_it; ++it) {
-      const uint32_t q = slotQ(it), dO = slotO(it);
-      const uint32_t acc = it > 0 ? 1u : 0u;
-      const bool more = it + 1 < n_it;
-      mbar_wait(&bar_p, it & 1);
+    int u0 = 0;  // ring uses before this item == blocks before this item
+    uint32_t kv_ph = 0;
+    int r = 0;
+    for (;; ++r) {
+      const int item = sched_take(sched, r);
+      if (item >= num_items) break;
+      const KvItem w = kv_decode<CAUSAL>(p, item);
+      const int n = w.n_it;
+      mbar_wait(&bar_kv, kv_ph);
+      kv_ph ^= 1;
+      mbar_wait(&fullA[u0 % NSA], (u0 / NSA) & 1);
       tc_fence_after();
-      hk_trace(10, it, 0);  // MMA: P^T(it) seen, dV issue
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        umma_ts_w(tdV, tS + packed_col(kk), mnmaj(dO, kk), idesc_acc, (acc | kk) ? 1u : 0u);
-      if (more) {
-        mbar_wait(&fullA[(it + 1) % NSA], ((it + 1) / NSA) & 1);
-        tc_fence_after();
-        hk_trace(13, it + 1, 0);  // ring A slot it+1 landed, S^T issue
-        issue_s(it + 1);
-      }
-      mbar_wait(&bar_ds, it & 1);
+      issue_s(u0);
+      mbar_wait(&fullB[u0 % NSB], (u0 / NSB) & 1);
       tc_fence_after();
-      hk_trace(11, it, 0);  // MMA: dS^T(it) seen, dK issue
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        umma_ts_w(tdK, tP + packed_col(kk), mnmaj(q, kk), idesc_acc, (acc | kk) ? 1u : 0u);
-      // Q(it) (last use dK) and dO/lse2/D(it) (last uses dV, the dS phase): free both
-      if (it + NSA < n_it) tc_commit_w(&emptyA[it % NSA]);
-      if (it + NSB < n_it) tc_commit_w(&emptyB[it % NSB]);
-      if (more) {  // dP^T(it+1) overwrites dS^T(it): after dK(it) in issue order
-        mbar_wait(&fullB[(it + 1) % NSB], ((it + 1) / NSB) & 1);
+      issue_dp(u0);
+      if (n == 1) tc_commit_w(&bar_kvfree);
+      for (int it = 0; it < n; ++it) {
+        const int u = u0 + it;
+        const uint32_t q = slotQ(u), dO = slotO(u);
+        const uint32_t acc = it > 0 ? 1u : 0u;
+        const bool more = it + 1 < n;
+        mbar_wait(&bar_p, u & 1);
         tc_fence_after();
-        issue_dp(it + 1);
+        hk_trace(10, u, 0);  // MMA: P^T(it) seen, dV issue
+        gemm_tsp_mn(tdV, tS, mnmaj(dO, 0), idesc_acc, acc);
+        if (more) {
+          mbar_wait(&fullA[(u + 1) % NSA], ((u + 1) / NSA) & 1);
+          tc_fence_after();
+          hk_trace(13, u + 1, 0);  // ring A slot u+1 landed, S^T issue
+          issue_s(u + 1);
+        }
+        mbar_wait(&bar_ds, u & 1);
+        tc_fence_after();
+        hk_trace(11, u, 0);  // MMA: dS^T(it) seen, dK issue
+        gemm_tsp_mn(tdK, tP, mnmaj(q, 0), idesc_acc, acc);
+        // Q(it) (last use dK) and dO/lse2/D(it) (last uses dV, the dS phase): free both
+        tc_commit_w(&emptyA[u % NSA]);
+        tc_commit_w(&emptyB[u % NSB]);
+        if (more) {  // dP^T(it+1) overwrites dS^T(it): after dK(it) in issue order
+          mbar_wait(&fullB[(u + 1) % NSB], ((u + 1) / NSB) & 1);
+          tc_fence_after();
+          issue_dp(u + 1);
+          if (it + 2 == n) tc_commit_w(&bar_kvfree);  // last S^T and dP^T issued
+        }
       }
+      tc_commit_w(&bar_acc);
+      u0 += n;
     }
-    tc_commit_w(&bar_acc);
+    // the releases of the final uses are never waited for by the producer: let them land
+    drain_ring(emptyA, NSA, u0);
+    drain_ring(emptyB, NSB, u0);
+    if (r > 0) mbar_wait(&bar_kvfree, (r - 1) & 1);
   } else {
     // ================= elementwise warpgroups (warps 0-7) =================
     const int wg = warp >> 2;              // query columns [64 wg, 64 wg + 64) of each block
     const uint32_t lb = (warp & 3) * 32;   // TMEM lane base
     const int r = (warp & 3) * 32 + lane;  // key row within the tile
-    const int key = jt * 128 + r;
     const float c = 1.4426950408889634f / sqrtf((float)D);
     const uint32_t cS = tS + 64 * wg, cP = tP + 64 * wg;
-    int qi = i0, s = 0;
-    for (int it = 0; it < n_it; ++it) {
-      const uint8_t* vec = sB + s * C::SLOT_B1 + C::T128;  // lse2 [128], then D [128]
-      const uint32_t par = it & 1;
-      float v[64];
-      // ---- phase 1: P^T = exp2(c S^T - LSE2) (masked), bf16 into TMEM for dV += P^T dO
-      if (threadIdx.x == 0) hk_trace(1, it, 0);
-      mbar_wait(&fullB[s], (it / NSB) & 1);  // lse2/D ride with dO in ring B: landed?
-      mbar_wait(&bar_s, par);
+    int u = 0, s = 0;  // blocks so far; ring B slot of block u
+    uint32_t acc_ph = 0;
+    for (int rr = 0;; ++rr) {
+      const int item = sched_take(sched, rr);
+      if (item >= num_items) break;
+      const KvItem w = kv_decode<CAUSAL>(p, item);
+      const int key = w.jt * 128 + r;
+      int qi = w.i0;
+      for (int it = 0; it < w.n_it; ++it, ++u) {
+        const uint8_t* vec = sB + s * C::SLOT_B1 + C::T128;  // lse2 [128], then D [128]
+        const uint32_t par = u & 1;
+        float v[64];
+        // ---- phase 1: P^T = exp2(c S^T - LSE2) (masked), bf16 into TMEM for dV += P^T dO
+        if (threadIdx.x == 0) hk_trace(1, u, 0);
+        mbar_wait(&fullB[s], (u / NSB) & 1);  // lse2/D ride with dO in ring B: landed?
+        mbar_wait(&bar_s, par);
+        tc_fence_after();
+        if (threadIdx.x == 0) hk_trace(2, u, 0);
+        tmem_ld64(tmem_addr(cS, lb, 0), v);
+        tmem_wait_ld();
+        const int q0 = qi * 128 + 64 * wg;
+#pragma unroll
+        for (int c4 = 0; c4 < 64; c4 += 4) {
+          float l0, l1, l2, l3;
+          lds_v4(vec + 4 * (64 * wg + c4), l0, l1, l2, l3);
+          const float2 xa = fma2(make_float2(v[c4], v[c4 + 1]), make_float2(c, c), make_float2(-l0, -l1));
+          const float2 xb = fma2(make_float2(v[c4 + 2], v[c4 + 3]), make_float2(c, c), make_float2(-l2, -l3));
+          const float2 ea = bwd_exp2_pair<BWD_EMU_OF_8>(xa, c4 / 2);
+          const float2 eb = bwd_exp2_pair<BWD_EMU_OF_8>(xb, c4 / 2 + 1);
+          v[c4] = ea.x;
+          v[c4 + 1] = ea.y;
+          v[c4 + 2] = eb.x;
+          v[c4 + 3] = eb.y;
+        }
+        if (CAUSAL && qi == w.jt) {
+#pragma unroll
+          for (int cc = 0; cc < 64; ++cc)
+            if (q0 + cc < key) v[cc] = 0.f;  // query < key is masked
+        }
+        tmem_st_packed64(tmem_addr(cS, lb, 0), v);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_p);
+        if (threadIdx.x == 0) hk_trace(3, u, 0);
+        // ---- phase 2: dS^T = P^T (dP^T - D), bf16 into TMEM for dK += dS^T Q
+        mbar_wait(&bar_dp, par);
+        tc_fence_after();
+        if (threadIdx.x == 0) hk_trace(4, u, 0);
+        float dp[64];
+        tmem_ld64(tmem_addr(cP, lb, 0), dp);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c4 = 0; c4 < 64; c4 += 4) {
+          float d0, d1, d2, d3;
+          lds_v4(vec + 512 + 4 * (64 * wg + c4), d0, d1, d2, d3);
+          dp[c4 + 0] = v[c4 + 0] * (dp[c4 + 0] - d0);
+          dp[c4 + 1] = v[c4 + 1] * (dp[c4 + 1] - d1);
+          dp[c4 + 2] = v[c4 + 2] * (dp[c4 + 2] - d2);
+          dp[c4 + 3] = v[c4 + 3] * (dp[c4 + 3] - d3);
+        }
+        tmem_st_packed64(tmem_addr(cP, lb, 0), dp);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_ds);
+        if (threadIdx.x == 0) hk_trace(5, u, 0);
+        if (++qi == T) qi = w.i0;
+        if (++s == NSB) s = 0;
+      }
+      // ---- epilogue: WG0 writes dV, WG1 writes dK * (1/sqrt d)
+      mbar_wait(&bar_acc, acc_ph);
+      acc_ph ^= 1;
       tc_fence_after();
-      if (threadIdx.x == 0) hk_trace(2, it, 0);
-      tmem_ld64(tmem_addr(cS, lb, 0), v);
-      tmem_wait_ld();
-      const int q0 = qi * 128 + 64 * wg;
+      const float scale = wg == 0 ? 1.f : rsqrtf((float)D);
+      const uint32_t tacc = wg == 0 ? tdV : tdK;
+      const bool key_ok = key < p.N;  // key rows of a ragged last tile beyond N are not stored
+      __nv_bfloat16* out =
+          (wg == 0 ? p.dv : p.dk) + (((size_t)w.b * p.N + (key_ok ? key : 0)) * p.Hkv + w.kvh) * D;
 #pragma unroll
-      for (int c4 = 0; c4 < 64; c4 += 4) {
-        float l0, l1, l2, l3;
-        lds_v4(vec + 4 * (64 * wg + c4), l0, l1, l2, l3);
-        const float2 xa = fma2(make_float2(v[c4], v[c4 + 1]), make_float2(c, c), make_float2(-l0, -l1));
-        const float2 xb = fma2(make_float2(v[c4 + 2], v[c4 + 3]), make_float2(c, c), make_float2(-l2, -l3));
-        const float2 ea = bwd_exp2_pair<BWD_EMU_OF_8>(xa, c4 / 2);
-        const float2 eb = bwd_exp2_pair<BWD_EMU_OF_8>(xb, c4 / 2 + 1);
-        v[c4] = ea.x;
-        v[c4 + 1] = ea.y;
-        v[c4 + 2] = eb.x;
-        v[c4 + 3] = eb.y;
-      }
-      if (CAUSAL && qi == jt) {
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t o[32];
+        tmem_ld32(tmem_addr(tacc, lb, c0), o);
+        tmem_wait_ld();
+        uint4 o4[4];
+        uint32_t* op = reinterpret_cast<uint32_t*>(o4);
 #pragma unroll
-        for (int cc = 0; cc < 64; ++cc)
-          if (q0 + cc < key) v[cc] = 0.f;  // query < key is masked
-      }
-      tmem_st_packed64(tmem_addr(cS, lb, 0), v);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_p);
-      if (threadIdx.x == 0) hk_trace(3, it, 0);
-      // ---- phase 2: dS^T = P^T (dP^T - D), bf16 into TMEM for dK += dS^T Q
-      mbar_wait(&bar_dp, par);
-      tc_fence_after();
-      if (threadIdx.x == 0) hk_trace(4, it, 0);
-      float dp[64];
-      tmem_ld64(tmem_addr(cP, lb, 0), dp);
-      tmem_wait_ld();
+        for (int k = 0; k < 16; ++k)
+          op[k] = pack_bf16(__uint_as_float(o[2 * k]) * scale, __uint_as_float(o[2 * k + 1]) * scale);
+        uint4* dst = reinterpret_cast<uint4*>(out + c0);
+        if (key_ok) {
 #pragma unroll
-      for (int c4 = 0; c4 < 64; c4 += 4) {
-        float d0, d1, d2, d3;
-        lds_v4(vec + 512 + 4 * (64 * wg + c4), d0, d1, d2, d3);
-        dp[c4 + 0] = v[c4 + 0] * (dp[c4 + 0] - d0);
-        dp[c4 + 1] = v[c4 + 1] * (dp[c4 + 1] - d1);
-        dp[c4 + 2] = v[c4 + 2] * (dp[c4 + 2] - d2);
-        dp[c4 + 3] = v[c4 + 3] * (dp[c4 + 3] - d3);
-      }
-      tmem_st_packed64(tmem_addr(cP, lb, 0), dp);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_ds);
-      if (threadIdx.x == 0) hk_trace(5, it, 0);
-      if (++qi == T) qi = i0;
-      if (++s == NSB) s = 0;
-    }
-    // ---- epilogue: WG0 writes dV, WG1 writes dK * (1/sqrt d)
-    mbar_wait(&bar_acc, 0);
-    tc_fence_after();
-    const float scale = wg == 0 ? 1.f : rsqrtf((float)D);
-    const uint32_t tacc = wg == 0 ? tdV : tdK;
-    const bool key_ok = key < p.N;  // key rows of a ragged last tile beyond N are not stored
-    __nv_bfloat16* out = (wg == 0 ? p.dv : p.dk) + (((size_t)b * p.N + (key_ok ? key : 0)) * p.Hkv + kvh) * D;
-#pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 32) {
-      uint32_t o[32];
-      tmem_ld32(tmem_addr(tacc, lb, c0), o);
-      tmem_wait_ld();
-      uint4 o4[4];
-      uint32_t* op = reinterpret_cast<uint32_t*>(o4);
-#pragma unroll
-      for (int k = 0; k < 16; ++k)
-        op[k] = pack_bf16(__uint_as_float(o[2 * k]) * scale, __uint_as_float(o[2 * k + 1]) * scale);
-      uint4* dst = reinterpret_cast<uint4*>(out + c0);
-      if (key_ok) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) dst[k] = o4[k];
+          for (int k = 0; k < 4; ++k) dst[k] = o4[k];
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc<512>(tb);
+  if (threadIdx.x == 0) sched_exit(p.sched);
 }
 
 // ---------------------------------------------------------------- B2: dQ
-// Persistent: one CTA per SM walks work items (query tile iq, h, b), numbered
-// like the forward's (the G heads x tiles of one (b, kvh) group consecutive,
-// tiles fastest, heaviest first when causal) and taken in snake order.
+// Persistent: one CTA per SM draws work items (query tile iq, h, b) from the
+// dynamic scheduler, numbered like the forward's (the G heads x tiles of one
+// (b, kvh) group consecutive, tiles fastest, heaviest first when causal).
 // Per item, loop over 128-key blocks j. Q_i and dO_i land (TMA) in two staging
 // tiles and the elementwise warps copy them into TMEM, so S = Q_i K_j^T and
 // dP = dO_i V_j^T run with A from TMEM: per block the tensor core then reads
@@ -437,9 +550,6 @@ __global__ void __launch_bounds__(320, 1)
 struct DqItem {
   int iq, h, kvh, b, n_it;
 };
-__device__ __forceinline__ int snake_item(int round, int cta, int ctas) {
-  return round * ctas + ((round & 1) ? ctas - 1 - cta : cta);
-}
 template <bool CAUSAL>
 __device__ __forceinline__ DqItem dq_decode(const BwdParams& p, int item) {
   const int T = p.Np / 128;
@@ -474,13 +584,15 @@ __global__ void __launch_bounds__(320, 1)
 
   __shared__ uint64_t bar_qa, fullA[NSA], emptyA[NSA], fullB[NB], emptyB[NB], bar_s, bar_sfree, bar_dp, bar_ds,
       bar_acc;
+  __shared__ Sched sched;
   __shared__ uint32_t tmem_base_s;
 
   const int warp = warp_id(), lane = lane_id();
-  const int cta = blockIdx.x, ctas = gridDim.x;
   const int num_items = p.B * p.Hq * (p.Np / 128);
+  unsigned* const ctr = p.sched + 2;
 
   if (threadIdx.x == 0) {
+    sched_init(sched);
     mbar_init(&bar_qa, 8);
     for (int s = 0; s < NSA; ++s) {
       mbar_init(&fullA[s], 1);
@@ -507,7 +619,7 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tb = tmem_base_s;
+  const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base_s, 0);  // warp-uniform for ptxas (UR operands)
   const uint32_t tdQ = tb, tS = tb + D, tP = tb + D + 128, tQa = tb + D + 256, tdOa = tQa + D / 2;
 
   // All roles walk the same items; ring uses and barrier phases run on across items.
@@ -533,7 +645,7 @@ __global__ void __launch_bounds__(320, 1)
         ++ub;
       };
       for (int r = 0;; ++r) {
-        const int item = snake_item(r, cta, ctas);
+        const int item = sched_publish(sched, ctr, r);
         if (item >= num_items) break;
         const DqItem w = dq_decode<CAUSAL>(p, item);
         load_b(&mapQ, w.h, w.iq * 128, w.b, pol_stream);
@@ -560,24 +672,18 @@ __global__ void __launch_bounds__(320, 1)
     uint32_t g = 0;      // blocks so far (phase of bar_s, bar_sfree, bar_dp, bar_ds)
     uint32_t qa_ph = 0;
     auto issue_s = [&](int u) {
-      const uint32_t k = aA + (u % NSA) * C::T128;
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) umma_ts_w(tS, tQa + kk * 8, kmaj(k, kk), idesc_sp, kk > 0);
+      gemm_ts_kk<D / 16>(tS, tQa, kmaj(aA + (u % NSA) * C::T128, 0), idesc_sp, 0u);
       tc_commit_w(&bar_s);
     };
-    auto issue_dp = [&](int u, bool release) {
-      const uint32_t v = aB + (u % NB) * C::T128;
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) umma_ts_w(tP, tdOa + kk * 8, kmaj(v, kk), idesc_sp, kk > 0);
+    auto issue_dp = [&](int u) {
+      gemm_ts_kk<D / 16>(tP, tdOa, kmaj(aB + (u % NB) * C::T128, 0), idesc_sp, 0u);
       tc_commit_w(&bar_dp);
-      if (release) tc_commit_w(&emptyB[u % NB]);  // V: dP is its only use
+      tc_commit_w(&emptyB[u % NB]);  // V: dP is its only use
     };
     for (int r = 0;; ++r) {
-      const int item = snake_item(r, cta, ctas);
+      const int item = sched_take(sched, r);
       if (item >= num_items) break;
       const DqItem w = dq_decode<CAUSAL>(p, item);
-      // in the CTA's last item, releases nobody waits for are skipped (no arrive after exit)
-      const bool last_item = snake_item(r + 1, cta, ctas) >= num_items;
       const int n = w.n_it;
       const int a0 = ua, v0 = ub + 2;  // ring B: Q_i at ub, dO_i at ub + 1, V_j at v0 + j
       mbar_wait(&bar_qa, qa_ph);        // Q_A, dO_A of this item in TMEM
@@ -591,7 +697,7 @@ __global__ void __launch_bounds__(320, 1)
       issue_s(a0);
       mbar_wait(&fullB[v0 % NB], (v0 / NB) & 1);
       tc_fence_after();
-      issue_dp(v0, !last_item || NB - 2 < n);
+      issue_dp(v0);
       for (int it = 0; it < n; ++it, ++g) {
         const bool more = it + 1 < n;
         mbar_wait(&bar_sfree, g & 1);  // S(it) loaded by the elementwise warps
@@ -604,24 +710,22 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&bar_ds, g & 1);
         tc_fence_after();
         hk_trace(11, g, 1);  // MMA: dS(it) seen, dQ issue
-        {
-          const uint32_t k = aA + ((a0 + it) % NSA) * C::T128;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_ts_w(tdQ, tP + packed_col(kk), mnmaj(k, kk), idesc_acc, (it > 0 || kk > 0) ? 1u : 0u);
-        }
-        if (!last_item || it + NSA < n) tc_commit_w(&emptyA[(a0 + it) % NSA]);  // K(it): last use dQ(it)
+        gemm_tsp_mn(tdQ, tP, mnmaj(aA + ((a0 + it) % NSA) * C::T128, 0), idesc_acc, it > 0 ? 1u : 0u);
+        tc_commit_w(&emptyA[(a0 + it) % NSA]);  // K(it): last use dQ(it)
         if (more) {  // dP(it+1) overwrites dS(it): after dQ(it) in issue order
           const int u = v0 + it + 1;
           mbar_wait(&fullB[u % NB], (u / NB) & 1);
           tc_fence_after();
-          issue_dp(u, !last_item || it + 1 + NB - 2 < n);
+          issue_dp(u);
         }
       }
       tc_commit_w(&bar_acc);
       ua += n;
       ub += n + 2;
     }
+    // the releases of the final uses are never waited for by the producer: let them land
+    drain_ring(emptyA, NSA, ua);
+    drain_ring(emptyB, NB, ub);
   } else {
     const int wg = warp >> 2;              // key columns [64 wg, 64 wg + 64) of each block
     const uint32_t lb = (warp & 3) * 32;
@@ -653,10 +757,9 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_qa);
     };
-    if (snake_item(0, cta, ctas) < num_items) copy_in();
-    for (int rr = 0;; ++rr) {
-      const int item = snake_item(rr, cta, ctas);
-      if (item >= num_items) break;
+    int item = sched_take(sched, 0);
+    if (item < num_items) copy_in();
+    for (int rr = 1; item < num_items; ++rr) {
       const DqItem w = dq_decode<CAUSAL>(p, item);
       const int q = w.iq * 128 + r;
       const size_t vrow = ((size_t)w.b * p.Hq + w.h) * p.Np + q;
@@ -713,7 +816,8 @@ __global__ void __launch_bounds__(320, 1)
       tmem_wait_ld();
       // the next item's Q/dO go into TMEM before dQ is stored: its S/dP start now.
       // (Its dQ MMAs, which overwrite this accumulator, follow this WG's reads.)
-      if (snake_item(rr + 1, cta, ctas) < num_items) copy_in();
+      item = sched_take(sched, rr);  // look ahead: is there a next item?
+      if (item < num_items) copy_in();
       const float scale = rsqrtf((float)D);
       const bool q_ok = q < p.N;  // query rows of a ragged last tile beyond N are not stored
       __nv_bfloat16* out = p.dq + (((size_t)w.b * p.N + (q_ok ? q : 0)) * p.Hq + w.h) * D + wg * (D / 2);
@@ -731,6 +835,7 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc<512>(tb);
+  if (threadIdx.x == 0) sched_exit(ctr);
 }
 
 // ---------------------------------------------------------------- host launch
@@ -766,8 +871,18 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     }
     if (dev < 64) attr_done[dev] = true;
   }
-  BwdParams p{Dv, lse2, reinterpret_cast<__nv_bfloat16*>(dQ), reinterpret_cast<__nv_bfloat16*>(dK),
-              reinterpret_cast<__nv_bfloat16*>(dV), B, Hq, Hkv, N, Np};
+  unsigned* sched = reinterpret_cast<unsigned*>(ws + (size_t)2 * B * Hq * Np);  // 4 counters after D, LSE2
+  BwdParams p{Dv,
+              lse2,
+              reinterpret_cast<__nv_bfloat16*>(dQ),
+              reinterpret_cast<__nv_bfloat16*>(dK),
+              reinterpret_cast<__nv_bfloat16*>(dV),
+              sched,
+              B,
+              Hq,
+              Hkv,
+              N,
+              Np};
   // B0
   const size_t rows = (size_t)B * N * Hq;
   const size_t warps_needed = (rows + (32 / (D / 8)) - 1) / (32 / (D / 8));
@@ -776,10 +891,13 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   if (phase < 0 || phase == 0)
     bwd_pre_kernel<D><<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(O),
                                                               reinterpret_cast<const __nv_bfloat16*>(dO), LSE, Dv,
-                                                              lse2, B, N, Hq, Np);
+                                                              lse2, B, N, Hq, Np, sched);
   // B1, B2
-  if (phase < 0 || phase == 1)
-    bwd_dkdv_kernel<D, CAUSAL><<<dim3(Np / 128, Hkv, B), C::THREADS, C::SMEM1, stream>>>(mQ, mdO, mK, mV, p);
+  if (phase < 0 || phase == 1) {
+    const int items = B * Hkv * (Np / 128);  // persistent: one CTA per SM
+    bwd_dkdv_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS, C::SMEM1, stream>>>(mQ, mdO, mK,
+                                                                                                    mV, p);
+  }
   if (phase < 0 || phase == 2) {
     const int items = B * Hq * (Np / 128);  // persistent: one CTA per SM
     bwd_dq_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS, C::SMEM2, stream>>>(mQ, mdO, mK, mV, p);

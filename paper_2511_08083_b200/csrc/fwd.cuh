@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = tmem_base_s;
+  const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base_s, 0);  // warp-uniform for ptxas (UR operands)
 
   // Every role walks the same item sequence; each barrier keeps its own phase
   // counter, and barriers of a Q tile an item lacks (odd T, last pair) are
@@ -196,20 +196,11 @@ __global__ void __launch_bounds__(384, 1)
       const uint64_t dk0 = KMAJ | (smem_u32(sK) >> 4);
       const uint64_t dv0 = VMN | (smem_u32(sV) >> 4);
       auto issue_s = [&](int t, int s) {
-        const uint64_t qd = dq0 + ((t * TB) >> 4), kd = dk0 + ((s * TB) >> 4);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = ((kk / 4) * 128 * 128 + (kk % 4) * 32) >> 4;
-          umma_ss_w(tbase + 128 * t, qd + off, kd + off, idesc_s, kk > 0);
-        }
+        gemm_ss_kk<D / 16>(tbase + 128 * t, dq0 + ((t * TB) >> 4), dk0 + ((s * TB) >> 4), idesc_s, 0u);
         tc_commit_w(&bar_s[t]);
       };
       auto issue_pv = [&](int t, int s, int j) {
-        const uint64_t vd = dv0 + ((s * TB) >> 4);
-#pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk)
-          umma_ts_w(tbase + 256 + D * t, tbase + 128 * t + kk * 8, vd + ((kk * 16 * 128) >> 4), idesc_o,
-                    (j > 0 || kk > 0) ? 1u : 0u);
+        gemm_ts_mn(tbase + 256 + D * t, tbase + 128 * t, dv0 + ((s * TB) >> 4), idesc_o, j > 0 ? 1u : 0u);
       };
       int s = 0;
       uint32_t ph = 0, q_ph = 0;

@@ -201,7 +201,7 @@ size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d) {
   (void)d;
   if (B <= 0 || Hq <= 0 || N <= 0) return 0;
   const size_t Np = ((size_t)N + 127) / 128 * 128;  // rows padded to whole 128-row tiles
-  return (size_t)2 * B * Hq * Np * sizeof(float);
+  return (size_t)2 * B * Hq * Np * sizeof(float) + 256;  // + the persistent kernels' work counters
 }
 
 hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,

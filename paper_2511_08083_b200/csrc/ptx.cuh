@@ -330,6 +330,75 @@ __device__ __forceinline__ void umma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// ---- whole-GEMM issue: one elect.sync, then the NK k-steps of one 128 x N x 16NK
+// GEMM with the operand descriptors / TMEM columns advanced by immediates inside
+// the asm (one instruction each instead of per-step descriptor math + elect).
+// Offsets in 16-byte units (descriptor start-address field) or TMEM columns:
+//   K-major SW128, 128-row tile: k-step kk at (kk/4)*1024 + (kk%4)*2
+//   MN-major SW128:              k-step kk at kk*128 (16 rows of 128 B)
+//   TMEM A, contiguous bf16:     kk*8 columns;  packed by two warpgroups: packed_col(kk)
+#define HK_MMA_HEAD                                   \
+  "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a, b;\n\t"  \
+  ".reg .b32 ta;\n\t"                                  \
+  "setp.ne.b32 p, %4, 0;\n\t"                          \
+  "setp.eq.b32 t, %4, %4;\n\t"                         \
+  "elect.sync _|e, 0xffffffff;\n\t"
+#define HK_SS_FIRST "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+#define HK_SS_STEP(AO, BO)                                          \
+  "add.s64 a, %1, " #AO ";\n\tadd.s64 b, %2, " #BO ";\n\t"          \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+#define HK_TS_FIRST "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+#define HK_TS_STEP(AO, BO)                                          \
+  "add.s32 ta, %1, " #AO ";\n\tadd.s64 b, %2, " #BO ";\n\t"         \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, t;\n\t"
+
+// A, B both K-major SW128 128-row tiles (S = Q K^T, S^T = K Q^T, dP^T = V dO^T)
+template <int NK>
+__device__ __forceinline__ void gemm_ss_kk(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  static_assert(NK == 4 || NK == 8, "k-steps");
+  if constexpr (NK == 4) {
+    asm volatile(HK_MMA_HEAD HK_SS_FIRST HK_SS_STEP(2, 2) HK_SS_STEP(4, 4) HK_SS_STEP(6, 6) "}" ::"r"(d), "l"(a),
+                 "l"(b), "r"(idesc), "r"(acc)
+                 : "memory");
+  } else {
+    asm volatile(HK_MMA_HEAD HK_SS_FIRST HK_SS_STEP(2, 2) HK_SS_STEP(4, 4) HK_SS_STEP(6, 6) HK_SS_STEP(1024, 1024)
+                     HK_SS_STEP(1026, 1026) HK_SS_STEP(1028, 1028) HK_SS_STEP(1030, 1030) "}" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc)
+                 : "memory");
+  }
+}
+// A from TMEM (contiguous bf16 columns), B K-major SW128 (dQ pass: S = Q_A K^T, dP = dO_A V^T)
+template <int NK>
+__device__ __forceinline__ void gemm_ts_kk(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  static_assert(NK == 4 || NK == 8, "k-steps");
+  if constexpr (NK == 4) {
+    asm volatile(HK_MMA_HEAD HK_TS_FIRST HK_TS_STEP(8, 2) HK_TS_STEP(16, 4) HK_TS_STEP(24, 6) "}" ::"r"(d),
+                 "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+                 : "memory");
+  } else {
+    asm volatile(HK_MMA_HEAD HK_TS_FIRST HK_TS_STEP(8, 2) HK_TS_STEP(16, 4) HK_TS_STEP(24, 6) HK_TS_STEP(32, 1024)
+                     HK_TS_STEP(40, 1026) HK_TS_STEP(48, 1028) HK_TS_STEP(56, 1030) "}" ::"r"(d),
+                 "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+                 : "memory");
+  }
+}
+// A from TMEM (contiguous bf16 columns), B MN-major SW128, K = 128 (forward O += P V)
+__device__ __forceinline__ void gemm_ts_mn(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(HK_MMA_HEAD HK_TS_FIRST HK_TS_STEP(8, 128) HK_TS_STEP(16, 256) HK_TS_STEP(24, 384)
+                   HK_TS_STEP(32, 512) HK_TS_STEP(40, 640) HK_TS_STEP(48, 768) HK_TS_STEP(56, 896) "}" ::"r"(d),
+               "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+               : "memory");
+}
+// A from TMEM packed by two warpgroups (columns 16kk.. at kk*8 for kk<4, 64+(kk-4)*8 after),
+// B MN-major SW128, K = 128 (dV += P^T dO, dK += dS^T Q, dQ += dS K)
+__device__ __forceinline__ void gemm_tsp_mn(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(HK_MMA_HEAD HK_TS_FIRST HK_TS_STEP(8, 128) HK_TS_STEP(16, 256) HK_TS_STEP(24, 384)
+                   HK_TS_STEP(64, 512) HK_TS_STEP(72, 640) HK_TS_STEP(80, 768) HK_TS_STEP(88, 896) "}" ::"r"(d),
+               "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+               : "memory");
+}
+
 __device__ __forceinline__ void tc_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

@@ -48,11 +48,11 @@ def test_host_only_validation(lib):
     L = _lib.lib()
     assert L.hk_attn_abi_version() == 1
     assert L.hk_status_string(2) == b"HK_ERR_UNSUPPORTED"
-    assert L.hk_attn_bwd_workspace_bytes(2, 4, 2, 256, 64) == 2 * 2 * 4 * 256 * 4
+    assert L.hk_attn_bwd_workspace_bytes(2, 4, 2, 256, 64) == 2 * 2 * 4 * 256 * 4 + 256
     p = ctypes.c_void_p(16)
     assert L.hk_attn_fwd(p, p, p, p, p, 1, 2, 2, 128, 96, 0, None) == 2   # d = 96
     assert L.hk_attn_fwd(p, p, p, p, p, 1, 2, 2, 0, 64, 0, None) == 1     # N = 0
-    assert L.hk_attn_bwd_workspace_bytes(1, 2, 2, 200, 64) == 2 * 2 * 256 * 4  # rows padded to 128
+    assert L.hk_attn_bwd_workspace_bytes(1, 2, 2, 200, 64) == 2 * 2 * 256 * 4 + 256  # rows padded to 128
     assert L.hk_attn_fwd(p, p, p, p, p, 1, 3, 2, 128, 64, 0, None) == 1   # Hq % Hkv
     assert b"multiple" in L.hk_attn_last_error()
     assert L.hk_attn_fwd(p, p, p, p, p, 0, 2, 2, 128, 64, 0, None) == 1   # B = 0

@@ -30,7 +30,7 @@ def run(B, N, Hq, Hkv, d, causal, seed, std_qk=None):
     x = gen(B, N, Hq, Hkv, d, seed=seed, std_qk=std_qk)
     o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
     Np = (N + 127) // 128 * 128
-    ws = torch.empty(2 * B * Hq * Np, dtype=torch.float32, device="cuda")
+    ws = torch.empty(2 * B * Hq * Np + 64, dtype=torch.float32, device="cuda")  # + scheduler counters
     dq, dk, dv = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, workspace=ws)
     torch.cuda.synchronize()
     ref = oracle.attn_fwd_bwd(np64(x["Q"]), np64(x["K"]), np64(x["V"]), np64(x["dO"]), causal)
