@@ -206,6 +206,9 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t ph = 0, q_ph = 0;
       uint32_t p_ph[2] = {0, 0}, oe_ph[2] = {0, 0};
       bool o_used[2] = {false, false};  // O_t holds an earlier item's accumulator (wait for its epilogue)
+#ifdef HK_TRACE
+      uint32_t tstep[2] = {0, 0};
+#endif
       for (int r = 0;; ++r) {
         const int item = fwd_item_index<CAUSAL>(r, cta, ctas);
         if (item >= p.num_items) break;
@@ -235,7 +238,9 @@ __global__ void __launch_bounds__(384, 1)
                 oe_ph[t] ^= 1;
               }
               tc_fence_after();
-              hk_trace(10 + t, j, 0);  // MMA: P_t(j) seen, PV issue
+#ifdef HK_TRACE
+              hk_trace(10 + t, tstep[t]++, 0);  // MMA: P_t seen, PV issue (running step of tile t)
+#endif
               issue_pv(t, s, j);
               if (j + 1 < nk) {
                 if (!k_next_waited) {
@@ -291,8 +296,9 @@ __global__ void __launch_bounds__(384, 1)
         // keys >= N (zero-filled by TMA) only need a mask when not causal: under the
         // causal mask they already lie beyond every valid query row
         const int kvalid = (!CAUSAL && j == T - 1) ? p.N - j * 128 : 128;
-        softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, diag, j > 0, kvalid);
+        softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, diag, j > 0, kvalid, 40 + 4 * t, step);
         tmem_wait_st();
+        if (threadIdx.x % 128 == 0) hk_trace(43 + 4 * t, step, 0);  // P stores complete
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_p[t]);

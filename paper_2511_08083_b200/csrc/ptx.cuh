@@ -27,16 +27,16 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 // ------------------------------------------------------------------ tracing (HK_TRACE builds only)
-// hk_trace(ev, a, b): one traced CTA stores clock64 at slot (ev, a mod 1024)
-// of a device table (a plain store: no atomics on the hot path) read back by
-// hk_diag_trace_read (include/hk_attn_diag.h). `b` is unused (kept for call sites).
+// hk_trace(ev, a, b): one traced CTA stores clock64 at slot (ev, a) of a device
+// table, a < 1024 (later indices are dropped; a plain store: no atomics on the hot
+// path), read back by hk_diag_trace_read (include/hk_attn_diag.h). `b` is unused.
 #ifdef HK_TRACE
 __device__ unsigned long long g_hk_trace[64 * 1024];
 __device__ __forceinline__ bool hk_trace_cta() {
   return blockIdx.x == gridDim.x / 2 && blockIdx.y == 0 && blockIdx.z == 0;
 }
 __device__ __forceinline__ void hk_trace(uint32_t ev, uint32_t a, uint32_t) {
-  if (hk_trace_cta()) g_hk_trace[(ev & 63) * 1024 + (a & 1023)] = (unsigned long long)clock64();
+  if (hk_trace_cta() && a < 1024) g_hk_trace[(ev & 63) * 1024 + a] = (unsigned long long)clock64();
 }
 #else
 __device__ __forceinline__ void hk_trace(uint32_t, uint32_t, uint32_t) {}

@@ -52,12 +52,21 @@ __device__ __forceinline__ void softmax_chunk32(const float* s, float c, float m
 // masked P is exactly 0. `o_live`: O already holds earlier P V products.
 template <int D, int EMU_OF_8>
 __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t lane_base, int r, float c,
-                                             float& m, float& l, bool diag, bool o_live, int kvalid = 128) {
+                                             float& m, float& l, bool diag, bool o_live, int kvalid = 128,
+                                             int trace_ev = -1, uint32_t trace_idx = 0) {
+#ifdef HK_TRACE
+  const bool tr = trace_ev >= 0 && (threadIdx.x % 128) == 0;
+#define HK_SM_TRACE(k) \
+  if (tr) hk_trace(trace_ev + (k), trace_idx, 0);
+#else
+#define HK_SM_TRACE(k)
+#endif
   float s[128];
 #pragma unroll
   for (int c0 = 0; c0 < 128; c0 += 32)
     tmem_ld32(tmem_addr(tS, lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(&s[c0]));
   tmem_wait_ld();
+  HK_SM_TRACE(0)  // S in registers
   const bool masked = diag || kvalid < 128;
   if (masked) {
     const int lim = diag ? (r + 1 < kvalid ? r + 1 : kvalid) : kvalid;  // keys [0, lim) visible
@@ -81,6 +90,7 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
     alpha = ex2(m - m_use);
   }
   const float smin = (m_use - 125.f) / c;
+  HK_SM_TRACE(1)  // row max done
   float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int c0 = 0; c0 < 128; c0 += 32) {
@@ -91,6 +101,7 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
       softmax_chunk32<true, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);
     tmem_st16(tmem_addr(tS, lane_base, c0 / 2), pk);
   }
+  HK_SM_TRACE(2)  // exps done, P stores issued
   const float2 rs2 = add2(acc[0], acc[1]);
   l = l * alpha + (rs2.x + rs2.y);
   // O holds P(j-1) V_{j-1}, complete: the S barrier tracked every earlier MMA.
@@ -110,6 +121,7 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
     }
   }
   m = m_use;
+#undef HK_SM_TRACE
 }
 
 }  // namespace hk

@@ -44,8 +44,15 @@ for t in (0, 1):  # t = softmax warpgroup (column half)
     chain = d([E(3, j) for j in js], [E(2, j + 1) for j in js])
     lag = d([E(3, j) for j in js], [ev.get((10, j)) for j in js])
     period = d([E(2, j) for j in js], [E(2, j + 1) for j in js])
+    sub = {}
+    marks = [(2 + 4 * t, "S_ready"), (40 + 4 * t, "S_loaded"), (41 + 4 * t, "max_done"), (42 + 4 * t, "exps_done"),
+             (43 + 4 * t, "st_done"), (3 + 4 * t, "P_pub")]
+    for (e1, n1), (e2, n2) in zip(marks, marks[1:]):
+        v = d([ev.get((e1, j)) for j in js], [ev.get((e2, j)) for j in js])
+        if v:
+            sub[f"{n1}->{n2}"] = f(v)
     res[f"tile{t}"] = {"n": len(js), "wait_for_S": f(wait), "softmax_X": f(X), "P_to_nextS": f(chain),
-                       "mma_lag_after_P": f(lag), "period": f(period)}
+                       "mma_lag_after_P": f(lag), "period": f(period), "softmax_parts": sub}
 t0c = ev.get((30, 0))
 if t0c:
     firstS = min(v for (e, a), v in ev.items() if e in (2, 6) and a == 0)
