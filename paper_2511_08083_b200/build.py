@@ -14,7 +14,7 @@ LIB_TRACE = os.path.join(PKG, "libhkattn_trace.so")  # -DHK_TRACE: in-kernel clo
 SOURCES = [os.path.join(CSRC, "hk_attn.cu")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
-         "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include")]
+         "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden", "-I", os.path.join(ROOT, "include")]
 
 
 def _deps():
@@ -31,9 +31,13 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False, trace: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False, trace: bool = False,
+          variant: str = "") -> str:
+    """variant: build libhkattn_<variant>.so instead (A/B experiments with HK_EXTRA flags)."""
     lib = LIB_DEBUG if debug else LIB_TRACE if trace else LIB
-    if not force and not (debug or trace) and not needs_build():
+    if variant:
+        lib = os.path.join(PKG, f"libhkattn_{variant}.so")
+    if not force and not (debug or trace or variant) and not needs_build():
         return LIB
     tmp = lib + ".tmp"
     extra = (["-DHK_DEBUG_HANG"] if debug else []) + (["-DHK_TRACE"] if trace else [])
@@ -45,7 +49,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False, trace
         raise RuntimeError("nvcc failed building libhkattn.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    if not (debug or trace):
+    if not (debug or trace or variant):
         with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
             f.write(r.stderr)
     os.replace(tmp, lib)
@@ -53,4 +57,6 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False, trace
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv, trace="--trace" in sys.argv))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv, trace="--trace" in sys.argv,
+                variant=var))

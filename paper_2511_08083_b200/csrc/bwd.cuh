@@ -180,7 +180,10 @@ __device__ __forceinline__ uint32_t packed_col(int kk) { return kk < 4 ? kk * 8 
 // P = 2^x for a pair of backward scores (x = c s - LSE2 <= ~0): BWD_EMU_OF_8
 // of every 8 pairs on the FMA pipe (ex2_poly2), the rest on the MUFU, which
 // otherwise needs 1024 of each block's 1536-2048 tensor cycles.
-constexpr int BWD_EMU_OF_8 = 3;
+#ifndef HK_BWD_EMU
+#define HK_BWD_EMU 3
+#endif
+constexpr int BWD_EMU_OF_8 = HK_BWD_EMU;
 template <int EMU_OF_8>
 __device__ __forceinline__ float2 bwd_exp2_pair(float2 x, int k) {
   if ((k % 8) < EMU_OF_8) return ex2_poly2(x);

@@ -12,8 +12,13 @@
 #include <set>
 #include <utility>
 
+// Built with -fvisibility=hidden: only the C ABI below is exported. (Template
+// statics such as per-kernel "attribute set" flags would otherwise become
+// process-wide GNU-unique symbols shared between two loaded copies of the library.)
+#pragma GCC visibility push(default)
 #include "../../include/hk_attn.h"
 #include "../../include/hk_attn_diag.h"
+#pragma GCC visibility pop
 #include "bwd.cuh"
 #include "fwd.cuh"
 #include "tma_host.h"
