@@ -1,4 +1,5 @@
-"""fp64 CPU oracle for fused attention forward/backward (HipKittens, arXiv 2511.08083).
+"""fp64 CPU oracles for fused attention forward/backward and the BF16 GEMM
+(HipKittens, arXiv 2511.08083).
 
 TEST INFRASTRUCTURE ONLY. Only `tests/`, `__graft_entry__.smoke()` and the
 `cpu_baseline` / `--impl reference` legs of `bench.py` may import this package.
@@ -19,3 +20,4 @@ from .attention import (  # noqa: F401
     attn_key_rows,
     softmax_scale,
 )
+from .gemm import gemm_abt, gemm_abt_rows, gemm_loops  # noqa: F401,E402

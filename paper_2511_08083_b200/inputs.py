@@ -81,3 +81,10 @@ def sample_rows(N: int, count: int, seed: int, diag_tile: int = 128):
     while len(rows) < min(count, N):
         rows.add(int(torch.randint(0, N, (1,), generator=g)))
     return sorted(rows)
+
+
+def make_gemm_inputs(M: int, N: int, K: int, seed: int = 0, device="cpu", std: float = 1.0):
+    """A [M, K] and B [N, K] bf16, i.i.d. N(0, std^2) rounded to bf16 -- the paper's
+    GEMM inputs (N(0, 1)). Each operand has its own splitmix64 stream."""
+    return {"A": _block((M, K), splitmix64(seed, 11), device, std),
+            "B": _block((N, K), splitmix64(seed, 12), device, std)}
