@@ -30,6 +30,7 @@ SIGNATURES = {
     "hk_diag_umma": (_I, [_P, _P, _P, _I, _I, _I, _I, _P]),
     "hk_diag_rates": (_I, [_I, _I, _I, _P, _P]),
     "hk_diag_trace_read": (_I, [_P, _Z, _I]),
+    "hk_gemm_bf16": (_I, [_P, _P, _P, _I, _I, _I, _P]),
     "hk_diag_bwd_phase": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _I, _I, _I, _I, _I, _I, _P]),
 }
 

@@ -77,6 +77,22 @@ def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None,
     return dq, dk, dv
 
 
+def gemm(a, b, out=None):
+    """C = a @ b.T (bf16 in, fp32 accumulate, bf16 out) on the tcgen05 CTA-pair
+    GEMM (include/hk_gemm.h). a [M, K], b [N, K] bf16 CUDA, contiguous;
+    M, N multiples of 256 and K of 64."""
+    _check_tensor("a", a)
+    _check_tensor("b", b)
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[1]:
+        raise ValueError(f"need a [M, K] and b [N, K]; got {tuple(a.shape)} and {tuple(b.shape)}")
+    M, K = a.shape
+    N = b.shape[0]
+    c = torch.empty((M, N), dtype=torch.bfloat16, device=a.device) if out is None else out
+    _check_tensor("out", c)
+    check(lib().hk_gemm_bf16(_ptr(a), _ptr(b), _ptr(c), M, N, K, _stream()))
+    return c
+
+
 class Attention(torch.autograd.Function):
     """autograd wrapper: Attention.apply(q, k, v, causal) -> o."""
 

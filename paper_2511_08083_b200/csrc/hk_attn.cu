@@ -18,9 +18,11 @@
 #pragma GCC visibility push(default)
 #include "../../include/hk_attn.h"
 #include "../../include/hk_attn_diag.h"
+#include "../../include/hk_gemm.h"
 #pragma GCC visibility pop
 #include "bwd.cuh"
 #include "fwd.cuh"
+#include "gemm.cuh"
 #include "tma_host.h"
 #include "rates_diag.cuh"
 #include "umma_diag.cuh"
@@ -341,6 +343,38 @@ hk_status hk_diag_rates(int kind, int param, int iters, float* out, cudaStream_t
   HK_RATE(2, 64) HK_RATE(2, 128) HK_RATE(2, 256)
 #undef HK_RATE
   return fail(HK_ERR_UNSUPPORTED, "unknown mma mode");
+}
+
+hk_status hk_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, cudaStream_t stream) {
+  g_err[0] = 0;
+  if (M <= 0 || N <= 0 || K <= 0) return fail(HK_ERR_INVALID_ARGUMENT, "M, N, K must be positive (%d, %d, %d)", M, N, K);
+  if (!A || !B || !C) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (!aligned16(A) || !aligned16(B) || !aligned16(C))
+    return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  if (M % 256 || N % 256 || K % 64)
+    return fail(HK_ERR_UNSUPPORTED, "need M %% 256 == 0, N %% 256 == 0, K %% 64 == 0 (got %d, %d, %d)", M, N, K);
+  const size_t a_bytes = (size_t)M * K * 2, b_bytes = (size_t)N * K * 2, c_bytes = (size_t)M * N * 2;
+  if (overlaps(C, c_bytes, A, a_bytes) || overlaps(C, c_bytes, B, b_bytes))
+    return fail(HK_ERR_INVALID_ARGUMENT, "C must not overlap A or B");
+  int num_sms = 0;
+  hk_status s = check_device(&num_sms);
+  if (s != HK_OK) return s;
+  CUtensorMap ma, mb;
+  if (!hk::encode_rowmajor(&ma, A, M, K, 128) || !hk::encode_rowmajor(&mb, B, N, K, 128))
+    return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (CUresult %d)", hk::last_encode_result());
+  s = ensure_smem(hk::gemm_bf16_kernel, hk::GEMM_SMEM);
+  if (s != HK_OK) return s;
+  hk::GemmParams p;
+  p.c = reinterpret_cast<__nv_bfloat16*>(C);
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.tiles_m = M / 256;
+  p.tiles_n = N / 256;
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;  // persistent: one CTA pair per TPC
+  hk::gemm_bf16_kernel<<<2 * pairs, hk::GEMM_THREADS, hk::GEMM_SMEM, stream>>>(ma, mb, p);
+  return launched("hk_gemm_bf16");
 }
 
 hk_status hk_diag_trace_read(void* dst, size_t bytes, int reset) {

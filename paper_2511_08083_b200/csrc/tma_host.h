@@ -48,4 +48,23 @@ inline bool encode_bnhd(CUtensorMap* map, const void* base, int B, int N, int H,
   return r == CUDA_SUCCESS;
 }
 
+// A row-major bf16 matrix [rows][cols] viewed as the 2-D map (cols, rows), box
+// (64, box_rows), 128-byte swizzle (K-major operand tiles for tcgen05).
+inline bool encode_rowmajor(CUtensorMap* map, const void* base, int rows, int cols, int box_rows) {
+  auto fn = get_encode_fn();
+  if (!fn) {
+    last_encode_result() = -1;
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  last_encode_result() = (int)r;
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace hk
