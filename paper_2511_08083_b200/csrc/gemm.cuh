@@ -25,15 +25,24 @@ namespace hk {
 struct GemmParams {
   __nv_bfloat16* c;  // [M][N] row-major
   int M, N, K;
-  int tiles_m, tiles_n;  // M / 256, N / 256
+  int tiles_m, tiles_n;  // M / 256, N / BNP
 };
 
 constexpr int GEMM_BK = 64;                           // K per stage: one 128-B swizzle panel
-constexpr int GEMM_STAGES = 6;
 constexpr uint32_t GEMM_HALF = 128 * GEMM_BK * 2;     // 16 KB: 128 rows x 64 bf16
-constexpr uint32_t GEMM_STAGE = 2 * GEMM_HALF;        // this CTA's A half + B half
-constexpr uint32_t GEMM_SMEM = GEMM_STAGES * GEMM_STAGE + 1024;
 constexpr int GEMM_THREADS = 192;
+// BNP = N extent of a pair tile: 256 (one 256-column accumulator per CTA, two
+// buffers) or 512 (two 256-column accumulators per CTA covering N = 512: each
+// stage moves A-half + 2 B-halves = 48 KB per CTA for twice the MMA work, 25%
+// fewer operand bytes per FLOP through L2 -- the kernel is power-capped and
+// that traffic costs clock).
+template <int BNP>
+struct GemmCfg {
+  static constexpr int NB = BNP / 256;                         // B halves per CTA per stage
+  static constexpr uint32_t STAGE = (1 + NB) * GEMM_HALF;      // A half + NB B halves
+  static constexpr int STAGES = BNP == 256 ? 6 : 4;
+  static constexpr uint32_t SMEM = STAGES * STAGE + 1024;
+};
 constexpr int GEMM_GROUP_M = 8;                       // tile raster: 8 M-tiles share B tiles in L2
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -113,11 +122,19 @@ __device__ __forceinline__ void gemm_tile_coords(const GemmParams& p, int t, int
   nt = r / gsz;
 }
 
+template <int BNP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                      const GemmParams p) {
+  using C = GemmCfg<BNP>;
+  constexpr int GEMM_STAGES = C::STAGES;
+  constexpr uint32_t GEMM_STAGE = C::STAGE;
+  constexpr int NB = C::NB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // tfull: accumulator(s) of a tile complete; tempty[a]: TMEM columns [256a, 256a+256)
+  // free again (BNP = 256: two alternating accumulators; BNP = 512: the two halves
+  // of one accumulator, released half by half by the epilogue)
   __shared__ uint64_t full[GEMM_STAGES], empty[GEMM_STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_s;
 
@@ -163,7 +180,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * GEMM_STAGE);  // both CTAs' halves
           uint8_t* st = smem + s * GEMM_STAGE;
           tma_load_2d_pair(&mapA, full_leader + 8 * s, st, kt * GEMM_BK, mt * 256 + rank * 128, pol);
-          tma_load_2d_pair(&mapB, full_leader + 8 * s, st + GEMM_HALF, kt * GEMM_BK, nt * 256 + rank * 128, pol);
+#pragma unroll
+          for (int h = 0; h < NB; ++h)  // B rows [256h + 128 rank, +128) of this tile's BNP
+            tma_load_2d_pair(&mapB, full_leader + 8 * s, st + (1 + h) * GEMM_HALF, kt * GEMM_BK,
+                             nt * BNP + 256 * h + rank * 128, pol);
         }
       }
       // let the final (never awaited) stage releases land before exit
@@ -180,16 +200,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t a0 = smem_u32(smem);
       int it = 0, tc = 0;
       for (int t = pair; t < ntiles; t += npairs, ++tc) {
-        const int acc = tc & 1;
-        mbar_wait(&tempty[acc], ((tc >> 1) & 1) ^ 1);  // both epilogues done with this accumulator
-        tc_fence_after();
-        const uint32_t d = tbase + acc * 256;
+        const int acc = NB == 1 ? (tc & 1) : 0;
+        // both epilogues done with the TMEM columns this tile accumulates into
+        const uint32_t te_ph = NB == 1 ? (((tc >> 1) & 1) ^ 1) : ((tc & 1) ^ 1);
         for (int kt = 0; kt < ktiles; ++kt, ++it) {
           const int s = it % GEMM_STAGES;
           mbar_wait(&full[s], (it / GEMM_STAGES) & 1);
-          tc_fence_after();
           const uint32_t sa = a0 + s * GEMM_STAGE;
-          gemm_pair_stage(d, KMAJ | (sa >> 4), KMAJ | ((sa + GEMM_HALF) >> 4), idesc, kt > 0 ? 1u : 0u);
+#pragma unroll
+          for (int h = 0; h < NB; ++h) {
+            if (kt == 0) mbar_wait(&tempty[NB == 1 ? acc : h], te_ph);
+            tc_fence_after();
+            gemm_pair_stage(tbase + (NB == 1 ? acc : h) * 256, KMAJ | (sa >> 4),
+                            KMAJ | ((sa + (1 + h) * GEMM_HALF) >> 4), idesc, kt > 0 ? 1u : 0u);
+          }
           tc_commit_pair_w(&empty[s]);
         }
         tc_commit_pair_w(&tfull[acc]);
@@ -204,20 +228,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     for (int t = pair; t < ntiles; t += npairs, ++tc) {
       int mt, nt;
       gemm_tile_coords(p, t, mt, nt);
-      const int acc = tc & 1;
-      mbar_wait(&tfull[acc], (tc >> 1) & 1);
+      const int acc = NB == 1 ? (tc & 1) : 0;
+      mbar_wait(&tfull[acc], NB == 1 ? ((tc >> 1) & 1) : (tc & 1));
       tc_fence_after();
       const int row = mt * 256 + rank * 128 + r;
-      __nv_bfloat16* crow = p.c + (size_t)row * p.N + nt * 256;
+      __nv_bfloat16* crow = p.c + (size_t)row * p.N + nt * BNP;
 #pragma unroll 1
-      for (int c0 = 0; c0 < 256; c0 += 32) {
+      for (int c0 = 0; c0 < BNP; c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tmem_addr(tbase + acc * 256, lane_base, c0), v);
         tmem_wait_ld();
-        if (c0 == 256 - 32) {  // accumulator fully read: the MMA may reuse it
+        if ((c0 & 255) == 256 - 32) {  // 256 columns fully read: the MMA may reuse them
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tempty_leader + 8 * acc);
+          if (lane == 0) mbar_arrive_cluster(tempty_leader + 8 * (NB == 1 ? acc : c0 / 256));
         }
         uint4 o[4];
         uint32_t* op = reinterpret_cast<uint32_t*>(o);

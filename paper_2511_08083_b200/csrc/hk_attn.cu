@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -362,18 +363,25 @@ hk_status hk_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int 
   CUtensorMap ma, mb;
   if (!hk::encode_rowmajor(&ma, A, M, K, 128) || !hk::encode_rowmajor(&mb, B, N, K, 128))
     return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (CUresult %d)", hk::last_encode_result());
-  s = ensure_smem(hk::gemm_bf16_kernel, hk::GEMM_SMEM);
-  if (s != HK_OK) return s;
   hk::GemmParams p;
   p.c = reinterpret_cast<__nv_bfloat16*>(C);
   p.M = M;
   p.N = N;
   p.K = K;
   p.tiles_m = M / 256;
-  p.tiles_n = N / 256;
+  const bool wide = N % 512 == 0 && getenv("HK_GEMM_NARROW") == nullptr;  // 256x512 pair tiles when N allows
+  p.tiles_n = wide ? N / 512 : N / 256;
   const int tiles = p.tiles_m * p.tiles_n;
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;  // persistent: one CTA pair per TPC
-  hk::gemm_bf16_kernel<<<2 * pairs, hk::GEMM_THREADS, hk::GEMM_SMEM, stream>>>(ma, mb, p);
+  if (wide) {
+    s = ensure_smem(hk::gemm_bf16_kernel<512>, hk::GemmCfg<512>::SMEM);
+    if (s != HK_OK) return s;
+    hk::gemm_bf16_kernel<512><<<2 * pairs, hk::GEMM_THREADS, hk::GemmCfg<512>::SMEM, stream>>>(ma, mb, p);
+  } else {
+    s = ensure_smem(hk::gemm_bf16_kernel<256>, hk::GemmCfg<256>::SMEM);
+    if (s != HK_OK) return s;
+    hk::gemm_bf16_kernel<256><<<2 * pairs, hk::GEMM_THREADS, hk::GemmCfg<256>::SMEM, stream>>>(ma, mb, p);
+  }
   return launched("hk_gemm_bf16");
 }
 
