@@ -117,9 +117,13 @@ __device__ __forceinline__ int sched_publish(Sched& q, unsigned* ctr, int k) {
 __device__ __forceinline__ int sched_take(Sched& q, int k) {
   const int i = k % SCHED_NQ;
   mbar_wait(&q.full[i], (k / SCHED_NQ) & 1);
-  // lane 0's copy via shfl: ptxas then treats the index (and everything the MMA
-  // warp derives from it) as warp-uniform, keeping descriptors in uniform registers
-  const int item = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile int*>(&q.item[i]), 0);
+  // Lane 0 alone reads the slot and releases it (its arrive orders its own read
+  // before the producer's next write); the other lanes get the value by shfl,
+  // which also makes the index (and everything the MMA warp derives from it)
+  // warp-uniform for ptxas, keeping descriptors in uniform registers.
+  int v = 0;
+  if (lane_id() == 0) v = *reinterpret_cast<volatile int*>(&q.item[i]);
+  const int item = __shfl_sync(0xffffffffu, v, 0);
   if (lane_id() == 0) mbar_arrive(&q.empty[i]);
   return item;
 }

@@ -1,6 +1,10 @@
 #!/bin/bash
-# compute-sanitizer passes on a tiny fwd+bwd (GPU box). Usage: bash scripts/sanitize.sh
+# compute-sanitizer passes on small fwd+bwd+GEMM runs that hand several items to
+# every persistent CTA (GPU box). Usage: bash scripts/sanitize.sh
 for tool in memcheck racecheck synccheck initcheck; do
   echo "== $tool"
-  timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool $tool python scripts/tiny_fwd_bwd.py 2>&1 | grep -E "ERROR SUMMARY|ran|not supported|Error" | head -5
+  timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool $tool python scripts/tiny_fwd_bwd.py > /tmp/san_$tool.txt 2>&1
+  grep -E "ERROR SUMMARY|RACECHECK SUMMARY|ran$|not supported" /tmp/san_$tool.txt | head -5
+  # distinct reported race sites (racecheck), with counts
+  grep -E "Race reported" /tmp/san_$tool.txt | sed 's/+0x[0-9a-f]*//' | sort | uniq -c | head -10
 done
