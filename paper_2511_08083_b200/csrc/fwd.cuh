@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sV = sK + NS * TB;   // NS tiles
 
   __shared__ uint64_t bar_q, bar_qfree, bar_kfull[NS], bar_kempty[NS], bar_vfull[NS], bar_vempty[NS];
-  __shared__ uint64_t bar_s[2], bar_p[2], bar_o[2], bar_oempty[2];
+  __shared__ uint64_t bar_s[2], bar_p[2], bar_pl[2], bar_o[2], bar_oempty[2];
   __shared__ uint32_t tmem_base_s;
 
   const int warp = warp_id();
@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bar_s[t], 1);
       mbar_init(&bar_p[t], 4);
+      mbar_init(&bar_pl[t], 4);  // first half of P_t (keys [0, 64)) published
       mbar_init(&bar_o[t], 1);
       mbar_init(&bar_oempty[t], 4);
     }
@@ -199,12 +200,10 @@ __global__ void __launch_bounds__(384, 1)
         gemm_ss_kk<D / 16>(tbase + 128 * t, dq0 + ((t * TB) >> 4), dk0 + ((s * TB) >> 4), idesc_s, 0u);
         tc_commit_w(&bar_s[t]);
       };
-      auto issue_pv = [&](int t, int s, int j) {
-        gemm_ts_mn(tbase + 256 + D * t, tbase + 128 * t, dv0 + ((s * TB) >> 4), idesc_o, j > 0 ? 1u : 0u);
-      };
+
       int s = 0;
       uint32_t ph = 0, q_ph = 0;
-      uint32_t p_ph[2] = {0, 0}, oe_ph[2] = {0, 0};
+      uint32_t p_ph[2] = {0, 0}, oe_ph[2] = {0, 0};  // bar_pl and bar_p complete in lockstep
       bool o_used[2] = {false, false};  // O_t holds an earlier item's accumulator (wait for its epilogue)
 #ifdef HK_TRACE
       uint32_t tstep[2] = {0, 0};
@@ -231,8 +230,7 @@ __global__ void __launch_bounds__(384, 1)
           for (int t = 0; t < 2; ++t) {
             const int nk = t == 0 ? it.nkv0 : it.nkv1;
             if (j < nk) {
-              mbar_wait(&bar_p[t], p_ph[t]);
-              p_ph[t] ^= 1;
+              mbar_wait(&bar_pl[t], p_ph[t]);
               if (j == 0 && o_used[t]) {  // previous item's O_t must be read out before PV overwrites it
                 mbar_wait(&bar_oempty[t], oe_ph[t]);
                 oe_ph[t] ^= 1;
@@ -241,7 +239,12 @@ __global__ void __launch_bounds__(384, 1)
 #ifdef HK_TRACE
               hk_trace(10 + t, tstep[t]++, 0);  // MMA: P_t seen, PV issue (running step of tile t)
 #endif
-              issue_pv(t, s, j);
+              const uint64_t vd = dv0 + ((s * TB) >> 4);
+              gemm_ts_mn_lo(tbase + 256 + D * t, tbase + 128 * t, vd, idesc_o, j > 0 ? 1u : 0u);
+              mbar_wait(&bar_p[t], p_ph[t]);
+              p_ph[t] ^= 1;
+              tc_fence_after();
+              gemm_ts_mn_hi(tbase + 256 + D * t, tbase + 128 * t, vd, idesc_o);
               if (j + 1 < nk) {
                 if (!k_next_waited) {
                   mbar_wait(&bar_kfull[s1], ph1);
@@ -296,7 +299,8 @@ __global__ void __launch_bounds__(384, 1)
         // keys >= N (zero-filled by TMA) only need a mask when not causal: under the
         // causal mask they already lie beyond every valid query row
         const int kvalid = (!CAUSAL && j == T - 1) ? p.N - j * 128 : 128;
-        softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, diag, j > 0, kvalid, 40 + 4 * t, step);
+        softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, diag, j > 0, kvalid, 40 + 4 * t, step,
+                                     &bar_pl[t]);
         tmem_wait_st();
         if (threadIdx.x % 128 == 0) hk_trace(43 + 4 * t, step, 0);  // P stores complete
         tc_fence_before();

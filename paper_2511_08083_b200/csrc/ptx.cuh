@@ -389,6 +389,19 @@ __device__ __forceinline__ void gemm_ts_mn(uint32_t d, uint32_t a_tmem, uint64_t
                "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
                : "memory");
 }
+// The two K halves of gemm_ts_mn (keys [0,64) then [64,128)): the forward publishes P
+// in two halves so the first half of O += P V overlaps the second half's exponentials.
+__device__ __forceinline__ void gemm_ts_mn_lo(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(HK_MMA_HEAD HK_TS_FIRST HK_TS_STEP(8, 128) HK_TS_STEP(16, 256) HK_TS_STEP(24, 384) "}" ::"r"(d),
+               "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+               : "memory");
+}
+__device__ __forceinline__ void gemm_ts_mn_hi(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc) {
+  asm volatile(HK_MMA_HEAD HK_TS_FIRST HK_TS_STEP(8, 128) HK_TS_STEP(16, 256) HK_TS_STEP(24, 384) "}" ::"r"(d),
+               "r"(a_tmem + 32), "l"(b + 512), "r"(idesc), "r"(1u)
+               : "memory");
+}
 // A from TMEM packed by two warpgroups (columns 16kk.. at kk*8 for kk<4, 64+(kk-4)*8 after),
 // B MN-major SW128, K = 128 (dV += P^T dO, dK += dS^T Q, dQ += dS K)
 __device__ __forceinline__ void gemm_tsp_mn(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,

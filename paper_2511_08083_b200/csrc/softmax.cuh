@@ -53,7 +53,7 @@ __device__ __forceinline__ void softmax_chunk32(const float* s, float c, float m
 template <int D, int EMU_OF_8>
 __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t lane_base, int r, float c,
                                              float& m, float& l, bool diag, bool o_live, int kvalid = 128,
-                                             int trace_ev = -1, uint32_t trace_idx = 0) {
+                                             int trace_ev = -1, uint32_t trace_idx = 0, uint64_t* bar_lo = nullptr) {
 #ifdef HK_TRACE
   const bool tr = trace_ev >= 0 && (threadIdx.x % 128) == 0;
 #define HK_SM_TRACE(k) \
@@ -91,6 +91,25 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
   }
   const float smin = (m_use - 125.f) / c;
   HK_SM_TRACE(1)  // row max done
+  // O holds P(j-1) V_{j-1}, complete: the S barrier tracked every earlier MMA. The
+  // rescale comes before any part of P(j) is published (P V(j) accumulates onto it).
+  if (o_live && __any_sync(0xffffffffu, alpha != 1.f)) {
+    // 16 columns at a time: the 128 scores are still live here
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 16) {
+      float o[16];
+      tmem_ld16(tmem_addr(tO, lane_base, c0), reinterpret_cast<uint32_t*>(o));
+      tmem_wait_ld();
+#pragma unroll
+      for (int cc = 0; cc < 16; cc += 2) {
+        const float2 v = mul2(make_float2(o[cc], o[cc + 1]), make_float2(alpha, alpha));
+        o[cc] = v.x;
+        o[cc + 1] = v.y;
+      }
+      tmem_st16(tmem_addr(tO, lane_base, c0), reinterpret_cast<const uint32_t*>(o));
+    }
+    tmem_wait_st();
+  }
   float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int c0 = 0; c0 < 128; c0 += 32) {
@@ -100,26 +119,16 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
     else
       softmax_chunk32<true, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);
     tmem_st16(tmem_addr(tS, lane_base, c0 / 2), pk);
+    if (bar_lo != nullptr && c0 == 32) {  // P of keys [0, 64) (and the O rescale) in TMEM:
+      tmem_wait_st();                     // the first half of P V may start
+      tc_fence_before();
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(bar_lo);
+    }
   }
   HK_SM_TRACE(2)  // exps done, P stores issued
   const float2 rs2 = add2(acc[0], acc[1]);
   l = l * alpha + (rs2.x + rs2.y);
-  // O holds P(j-1) V_{j-1}, complete: the S barrier tracked every earlier MMA.
-  if (o_live && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 32) {
-      float o[32];
-      tmem_ld32(tmem_addr(tO, lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(o));
-      tmem_wait_ld();
-#pragma unroll
-      for (int cc = 0; cc < 32; cc += 2) {
-        const float2 v = mul2(make_float2(o[cc], o[cc + 1]), make_float2(alpha, alpha));
-        o[cc] = v.x;
-        o[cc + 1] = v.y;
-      }
-      tmem_st32(tmem_addr(tO, lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(o));
-    }
-  }
   m = m_use;
 #undef HK_SM_TRACE
 }
