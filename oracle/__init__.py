@@ -1,5 +1,5 @@
-"""fp64 CPU oracles for fused attention forward/backward and the BF16 GEMM
-(HipKittens, arXiv 2511.08083).
+"""fp64 CPU oracles for fused attention forward/backward, the BF16 GEMM and the
+memory-bound dropout-residual-LayerNorm and rotary kernels (HipKittens, arXiv 2511.08083).
 
 TEST INFRASTRUCTURE ONLY. Only `tests/`, `__graft_entry__.smoke()` and the
 `cpu_baseline` / `--impl reference` legs of `bench.py` may import this package.
@@ -21,3 +21,4 @@ from .attention import (  # noqa: F401
     softmax_scale,
 )
 from .gemm import gemm_abt, gemm_abt_rows, gemm_loops  # noqa: F401,E402
+from .membound import dropout_keep, layernorm_dropout_residual, rope, rope_tables  # noqa: F401,E402

@@ -88,3 +88,17 @@ def make_gemm_inputs(M: int, N: int, K: int, seed: int = 0, device="cpu", std: f
     GEMM inputs (N(0, 1)). Each operand has its own splitmix64 stream."""
     return {"A": _block((M, K), splitmix64(seed, 11), device, std),
             "B": _block((N, K), splitmix64(seed, 12), device, std)}
+
+
+def make_ln_inputs(rows: int, D: int, seed: int = 0, device="cpu"):
+    """x, residual [rows, D] bf16 N(0,1); weight ~ 1 + 0.1 N(0,1), bias ~ 0.1 N(0,1) bf16."""
+    w = _block((D,), splitmix64(seed, 23), device, 0.1).float() + 1.0
+    return {"x": _block((rows, D), splitmix64(seed, 21), device, 1.0),
+            "residual": _block((rows, D), splitmix64(seed, 22), device, 1.0),
+            "weight": w.to(torch.bfloat16),
+            "bias": _block((D,), splitmix64(seed, 24), device, 0.1)}
+
+
+def make_rope_inputs(B: int, N: int, H: int, d: int, seed: int = 0, device="cpu"):
+    """x [B, N, H, d] bf16 N(0,1) (the Q or K tensor a rotary step transforms)."""
+    return {"x": _block((B, N, H, d), splitmix64(seed, 31), device, 1.0)}
