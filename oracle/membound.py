@@ -14,9 +14,10 @@ the CUDA path (same counter-based generator, reading #20).
    eps = 1e-5. The listing keeps mean/var in bf16; the oracle is
    exact (fp64) and takes r after the bf16 rounding of the stored o_resid,
    as the product path does (reading #20).
-   keep(i) for flat element index i = row * D + col: u32(i, seed) >= floor(p * 2^32)
-   with u32 the top 32 bits of the splitmix64 finaliser of
-   (seed * 0x9E3779B97F4A7C15 + i + 1) mod 2^64.
+   keep(i) for flat element index i = row * D + col (< 2^32):
+   h(i) >= floor(p * 2^32), h = the "lowbias32" integer hash of
+   (i * 0x9E3779B9 + seed) mod 2^32:
+       x ^= x >> 16; x *= 0x7feb352d; x ^= x >> 15; x *= 0x846ca68b; x ^= x >> 16.
 
 2. Rotary positional encoding (B=16, H=16, d=128), rotate-half
    form (reading #21): for x [B, N, H, d], cos/sin [N, d/2],
@@ -28,21 +29,18 @@ from __future__ import annotations
 
 import numpy as np
 
-_GOLD = np.uint64(0x9E3779B97F4A7C15)
-
-
 def dropout_keep(n_elems: int, p: float, seed: int, offset: int = 0) -> np.ndarray:
-    """Boolean keep mask for flat indices offset .. offset+n_elems-1."""
+    """Boolean keep mask for flat indices offset .. offset+n_elems-1 (uint32 arithmetic)."""
     if p <= 0.0:
         return np.ones(n_elems, dtype=bool)
-    with np.errstate(over="ignore"):
-        z = np.uint64(seed) * _GOLD + (np.arange(offset, offset + n_elems, dtype=np.uint64) + np.uint64(1))
-        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
-        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
-        z = z ^ (z >> np.uint64(31))
-    u32 = (z >> np.uint64(32)).astype(np.uint64)
-    thresh = np.uint64(int(p * 4294967296.0))
-    return u32 >= thresh
+    i = np.arange(offset, offset + n_elems, dtype=np.uint64)
+    x = (i * np.uint64(0x9E3779B9) + np.uint64(seed & 0xFFFFFFFF)) & np.uint64(0xFFFFFFFF)
+    x ^= x >> np.uint64(16)
+    x = (x * np.uint64(0x7FEB352D)) & np.uint64(0xFFFFFFFF)
+    x ^= x >> np.uint64(15)
+    x = (x * np.uint64(0x846CA68B)) & np.uint64(0xFFFFFFFF)
+    x ^= x >> np.uint64(16)
+    return x >= np.uint64(int(p * 4294967296.0))
 
 
 def _bf16_round(a: np.ndarray) -> np.ndarray:

@@ -31,6 +31,8 @@ SIGNATURES = {
     "hk_diag_rates": (_I, [_I, _I, _I, _P, _P]),
     "hk_diag_trace_read": (_I, [_P, _Z, _I]),
     "hk_gemm_bf16": (_I, [_P, _P, _P, _I, _I, _I, _P]),
+    "hk_ln_dropout_residual": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, ctypes.c_float, ctypes.c_uint, ctypes.c_float, _P]),
+    "hk_rope": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _P]),
     "hk_diag_bwd_phase": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _I, _I, _I, _I, _I, _I, _P]),
 }
 

@@ -93,6 +93,37 @@ def gemm(a, b, out=None):
     return c
 
 
+def ln_dropout_residual(x, residual, weight, bias, p: float = 0.0, seed: int = 0, eps: float = 1e-5,
+                        out=None, out_resid=None):
+    """Fused dropout + residual + LayerNorm (include/hk_membound.h). x, residual [..., D]
+    bf16 CUDA contiguous; weight, bias [D] bf16. Returns (out, out_resid) bf16."""
+    for n, t in (("x", x), ("residual", residual), ("weight", weight), ("bias", bias)):
+        _check_tensor(n, t)
+    if x.shape != residual.shape or weight.shape != (x.shape[-1],) or bias.shape != (x.shape[-1],):
+        raise ValueError("x and residual must match, weight and bias must be [D]")
+    D = x.shape[-1]
+    rows = x.numel() // D
+    o = torch.empty_like(x) if out is None else out
+    r = torch.empty_like(x) if out_resid is None else out_resid
+    check(lib().hk_ln_dropout_residual(_ptr(x), _ptr(residual), _ptr(weight), _ptr(bias), _ptr(o), _ptr(r), rows, D,
+                                       float(p), int(seed) & 0xFFFFFFFF, float(eps), _stream()))
+    return o, r
+
+
+def rope(x, cos, sin, out=None):
+    """Rotary embedding (rotate-half) of x [B, N, H, d] bf16 with cos/sin [N, d/2] fp32
+    (include/hk_membound.h). `out` may be `x` (in place)."""
+    _check_tensor("x", x)
+    _check_tensor("cos", cos, torch.float32)
+    _check_tensor("sin", sin, torch.float32)
+    B, N, H, d = x.shape
+    if cos.shape != (N, d // 2) or sin.shape != (N, d // 2):
+        raise ValueError("cos and sin must be [N, d/2]")
+    o = torch.empty_like(x) if out is None else out
+    check(lib().hk_rope(_ptr(x), _ptr(cos), _ptr(sin), _ptr(o), B, N, H, d, _stream()))
+    return o
+
+
 class Attention(torch.autograd.Function):
     """autograd wrapper: Attention.apply(q, k, v, causal) -> o."""
 

@@ -20,10 +20,12 @@
 #include "../../include/hk_attn.h"
 #include "../../include/hk_attn_diag.h"
 #include "../../include/hk_gemm.h"
+#include "../../include/hk_membound.h"
 #pragma GCC visibility pop
 #include "bwd.cuh"
 #include "fwd.cuh"
 #include "gemm.cuh"
+#include "membound.cuh"
 #include "tma_host.h"
 #include "rates_diag.cuh"
 #include "umma_diag.cuh"
@@ -383,6 +385,83 @@ hk_status hk_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int 
     hk::gemm_bf16_kernel<256><<<2 * pairs, hk::GEMM_THREADS, hk::GemmCfg<256>::SMEM, stream>>>(ma, mb, p);
   }
   return launched("hk_gemm_bf16");
+}
+
+hk_status hk_ln_dropout_residual(const void* x, const void* residual, const void* weight, const void* bias, void* out,
+                                 void* out_resid, int rows, int D, float p, unsigned int seed, float eps,
+                                 cudaStream_t stream) {
+  g_err[0] = 0;
+  if (rows <= 0 || D <= 0) return fail(HK_ERR_INVALID_ARGUMENT, "rows and D must be positive (%d, %d)", rows, D);
+  if (!x || !residual || !weight || !bias || !out || !out_resid)
+    return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (!aligned16(x) || !aligned16(residual) || !aligned16(weight) || !aligned16(bias) || !aligned16(out) ||
+      !aligned16(out_resid))
+    return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  if (!(p >= 0.f && p < 1.f) || !(eps > 0.f)) return fail(HK_ERR_INVALID_ARGUMENT, "need 0 <= p < 1 and eps > 0");
+  if (D % 8 || D > 8192) return fail(HK_ERR_UNSUPPORTED, "need D %% 8 == 0 and D <= 8192 (got %d)", D);
+  if ((long long)rows * D >= (1ll << 32)) return fail(HK_ERR_UNSUPPORTED, "rows * D must be < 2^32");
+  const size_t bytes = (size_t)rows * D * 2;
+  if (overlaps(out, bytes, out_resid, bytes) || overlaps(out, bytes, x, bytes) ||
+      overlaps(out, bytes, residual, bytes) || overlaps(out_resid, bytes, x, bytes) ||
+      overlaps(out_resid, bytes, residual, bytes))
+    return fail(HK_ERR_INVALID_ARGUMENT, "outputs must not overlap each other or the inputs");
+  int num_sms = 0;
+  hk_status s = check_device(&num_sms);
+  if (s != HK_OK) return s;
+  hk::LnParams q;
+  q.x = reinterpret_cast<const __nv_bfloat16*>(x);
+  q.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
+  q.weight = reinterpret_cast<const __nv_bfloat16*>(weight);
+  q.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
+  q.out = reinterpret_cast<__nv_bfloat16*>(out);
+  q.out_resid = reinterpret_cast<__nv_bfloat16*>(out_resid);
+  q.rows = rows;
+  q.D = D;
+  q.thresh = p > 0.f ? (uint32_t)fmin((double)p * 4294967296.0, 4294967295.0) : 0u;
+  q.seed = seed;
+  q.scale = 1.f / (1.f - p);
+  q.eps = eps;
+  const int warps = 8, blocks_needed = (rows + warps - 1) / warps;
+  const int blocks = blocks_needed < num_sms * 8 ? blocks_needed : num_sms * 8;
+  const int vpl = (D / 8 + 31) / 32;  // 8-element vectors per lane
+#define HK_LN(V) hk::ln_dropout_residual_kernel<V><<<blocks, 256, 0, stream>>>(q)
+  if (vpl <= 1) HK_LN(1);
+  else if (vpl <= 2) HK_LN(2);
+  else if (vpl <= 4) HK_LN(4);
+  else if (vpl <= 8) HK_LN(8);
+  else if (vpl <= 16) HK_LN(16);
+  else HK_LN(32);
+#undef HK_LN
+  return launched("hk_ln_dropout_residual");
+}
+
+hk_status hk_rope(const void* x, const float* cos, const float* sin, void* out, int B, int N, int H, int d,
+                  cudaStream_t stream) {
+  g_err[0] = 0;
+  if (B <= 0 || N <= 0 || H <= 0 || d <= 0) return fail(HK_ERR_INVALID_ARGUMENT, "B, N, H, d must be positive");
+  if (!x || !cos || !sin || !out) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (!aligned16(x) || !aligned16(cos) || !aligned16(sin) || !aligned16(out))
+    return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  if (d % 16 || d > 512) return fail(HK_ERR_UNSUPPORTED, "need d %% 16 == 0 and d <= 512 (got %d)", d);
+  const size_t bytes = (size_t)B * N * H * d * 2;
+  if (out != x && overlaps(out, bytes, x, bytes)) return fail(HK_ERR_INVALID_ARGUMENT, "out partially overlaps x");
+  int num_sms = 0;
+  hk_status s = check_device(&num_sms);
+  if (s != HK_OK) return s;
+  hk::RopeParams q;
+  q.x = reinterpret_cast<const __nv_bfloat16*>(x);
+  q.cos = cos;
+  q.sin = sin;
+  q.out = reinterpret_cast<__nv_bfloat16*>(out);
+  q.rows = (size_t)B * N * H;
+  q.N = N;
+  q.H = H;
+  q.d = d;
+  const size_t threads = q.rows * (d / 16);
+  size_t blocks = (threads + 255) / 256;
+  if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
+  hk::rope_kernel<<<(unsigned)blocks, 256, 0, stream>>>(q);
+  return launched("hk_rope");
 }
 
 hk_status hk_diag_trace_read(void* dst, size_t bytes, int reset) {

@@ -1,0 +1,168 @@
+// The paper's memory-bound kernels (PAPER.md P:554-562,
+// P:583): fused dropout + residual + LayerNorm (listing P:1214-1267) and rotary
+// positional encoding. Both are HBM-roofline kernels on B200: 16-byte vector
+// loads/stores, one pass over HBM, statistics in fp32 registers.
+#pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+
+namespace hk {
+
+// ---------------------------------------------------------------- dropout hash
+// keep(i) = lowbias32(i * 0x9E3779B9 + seed) >= thresh, thresh = floor(p * 2^32)
+// (reading #20; the oracle implements the same counter-based hash).
+__device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 t = __bfloat1622float2(h[k]);
+    f[2 * k] = t.x;
+    f[2 * k + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(f[2 * k], f[2 * k + 1]);
+  return v;
+}
+
+// ---------------------------------------------------------------- LayerNorm
+struct LnParams {
+  const __nv_bfloat16* x;         // [rows][D]
+  const __nv_bfloat16* residual;  // [rows][D]
+  const __nv_bfloat16* weight;    // [D]
+  const __nv_bfloat16* bias;      // [D]
+  __nv_bfloat16* out;             // [rows][D]
+  __nv_bfloat16* out_resid;       // [rows][D]
+  int rows, D;
+  uint32_t thresh;  // dropout keep threshold (0 = no dropout)
+  uint32_t seed;
+  float scale;      // 1 / (1 - p)
+  float eps;
+};
+
+// One warp per row (rows grid-strided over warps). Lane l owns the 8-element
+// vectors l, l+32, ... of its row (VPL = vectors per lane, compile-time max).
+// r = bf16(residual + dropout(x)) is kept packed in registers (it is stored
+// rounded anyway) for the two-pass mean / centred variance.
+template <int VPL>
+__global__ void __launch_bounds__(256) ln_dropout_residual_kernel(const LnParams p) {
+  const int lane = threadIdx.x & 31;
+  const int nv = p.D / 8;
+  const size_t gwarp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const size_t nwarps = (size_t)gridDim.x * blockDim.x / 32;
+  const float inv_d = 1.f / (float)p.D;
+  for (size_t row = gwarp; row < (size_t)p.rows; row += nwarps) {
+    const uint4* xr = reinterpret_cast<const uint4*>(p.x + row * p.D);
+    const uint4* rr = reinterpret_cast<const uint4*>(p.residual + row * p.D);
+    uint4 rv[VPL];
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int v = lane + 32 * k;
+      if (v < nv) {
+        float xf[8], rf[8];
+        unpack8(__ldcs(xr + v), xf);  // streamed once: evict-first
+        unpack8(__ldcs(rr + v), rf);
+        const uint32_t base = (uint32_t)(row * p.D + (size_t)v * 8);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float xt = xf[e];
+          if (p.thresh) xt = lowbias32((base + e) * 0x9E3779B9u + p.seed) >= p.thresh ? xt * p.scale : 0.f;
+          rf[e] += xt;
+        }
+        rv[k] = pack8(rf);
+        float q[8];
+        unpack8(rv[k], q);  // the stored (rounded) values feed the statistics
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sum += q[e];
+        __stcs(reinterpret_cast<uint4*>(p.out_resid + row * p.D) + v, rv[k]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum * inv_d;
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      if (lane + 32 * k < nv) {
+        float q[8];
+        unpack8(rv[k], q);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float c = q[e] - mean;
+          ss = fmaf(c, c, ss);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float rstd = rsqrtf(ss * inv_d + p.eps);
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int v = lane + 32 * k;
+      if (v < nv) {
+        float q[8], w[8], b[8];
+        unpack8(rv[k], q);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(p.weight) + v), w);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(p.bias) + v), b);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) q[e] = fmaf((q[e] - mean) * rstd, w[e], b[e]);
+        __stcs(reinterpret_cast<uint4*>(p.out + row * p.D) + v, pack8(q));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- rotary
+struct RopeParams {
+  const __nv_bfloat16* x;  // [B][N][H][d]
+  const float* cos;        // [N][d/2]
+  const float* sin;        // [N][d/2]
+  __nv_bfloat16* out;      // [B][N][H][d]
+  size_t rows;             // B * N * H
+  int N, H, d;
+};
+
+// One thread per (row, 8-wide chunk of the first half): it loads the matching
+// chunks of both halves (16 B each) and the 8 cos/sin values of its position.
+__global__ void __launch_bounds__(256) rope_kernel(const RopeParams p) {
+  const int half = p.d / 2, cpr = half / 8;  // chunks per row
+  const size_t total = p.rows * cpr;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = t / cpr;
+    const int ch = (int)(t % cpr);
+    const int n = (int)((row / p.H) % p.N);
+    const __nv_bfloat16* xr = p.x + row * p.d;
+    float a[8], b[8], c[8], s[8];
+    unpack8(__ldcs(reinterpret_cast<const uint4*>(xr) + ch), a);
+    unpack8(__ldcs(reinterpret_cast<const uint4*>(xr + half) + ch), b);
+    const float4* cp = reinterpret_cast<const float4*>(p.cos + (size_t)n * half + ch * 8);
+    const float4* sp = reinterpret_cast<const float4*>(p.sin + (size_t)n * half + ch * 8);
+    const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
+    c[0] = c0.x, c[1] = c0.y, c[2] = c0.z, c[3] = c0.w, c[4] = c1.x, c[5] = c1.y, c[6] = c1.z, c[7] = c1.w;
+    s[0] = s0.x, s[1] = s0.y, s[2] = s0.z, s[3] = s0.w, s[4] = s1.x, s[5] = s1.y, s[6] = s1.z, s[7] = s1.w;
+    float lo[8], hi[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      lo[e] = fmaf(a[e], c[e], -b[e] * s[e]);
+      hi[e] = fmaf(b[e], c[e], a[e] * s[e]);
+    }
+    __nv_bfloat16* orow = p.out + row * p.d;
+    __stcs(reinterpret_cast<uint4*>(orow) + ch, pack8(lo));
+    __stcs(reinterpret_cast<uint4*>(orow + half) + ch, pack8(hi));
+  }
+}
+
+}  // namespace hk

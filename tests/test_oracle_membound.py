@@ -45,15 +45,17 @@ def test_dropout_keep_rate_and_determinism():
 
 
 def test_dropout_hash_brute_force():
-    """The vectorised hash equals a plain-integer splitmix64 finaliser, element by element."""
-    M = (1 << 64) - 1
+    """The vectorised hash equals the plain-integer lowbias32 hash, element by element."""
+    M = (1 << 32) - 1
 
     def keep1(i, p, seed):
-        z = (seed * 0x9E3779B97F4A7C15 + i + 1) & M
-        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
-        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
-        z ^= z >> 31
-        return (z >> 32) >= int(p * 2 ** 32)
+        x = (i * 0x9E3779B9 + seed) & M
+        x ^= x >> 16
+        x = (x * 0x7FEB352D) & M
+        x ^= x >> 15
+        x = (x * 0x846CA68B) & M
+        x ^= x >> 16
+        return x >= int(p * 2 ** 32)
 
     k = dropout_keep(300, 0.4, seed=123)
     assert all(k[i] == keep1(i, 0.4, 123) for i in range(300))
