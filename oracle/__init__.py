@@ -16,6 +16,7 @@ from .attention import (  # noqa: F401
     attn_fwd,
     attn_fwd_bwd,
     attn_naive,
+    attn_varlen_fwd_bwd,
     attn_rows,
     attn_key_rows,
     softmax_scale,

@@ -29,11 +29,19 @@ Sources:
     P:1313; L indexed {batch, head, 0, seq}: P:1500.
   * Causal: key j visible to query i iff j <= i (reading #3; P:571 names
     causal attention without fixing alignment; Nq == Nk so it is unique).
+    With Nq != Nk the mask is bottom-right aligned:
+    key j visible to query i iff j <= i + (Nk - Nq) (reading #22).
+    A query row that sees no key has O = 0, LSE = -inf (the logsumexp of an
+    empty set), D = 0 and dQ = 0; it adds nothing to dK, dV (reading #22).
   * Backward: the analytic gradient of the forward (reading #11); the paper
     gives no algorithm.
 
 Layout conventions (all numpy, any float dtype accepted, converted to fp64):
-  Q, dO: [B, N, Hq, d]   K, V: [B, N, Hkv, d]   LSE, D: [B, Hq, N]
+  Q, dO: [B, Nq, Hq, d]   K, V: [B, Nk, Hkv, d]   LSE, D: [B, Hq, Nq]
+  (Nq == Nk == N for the paper's problem; Nq != Nk is NEXT #4.)
+Packed variable-length batches (NEXT #4, `attn_varlen_fwd_bwd`):
+  Q, dO: [total_q, Hq, d]   K, V: [total_k, Hkv, d]   LSE, D: [Hq, total_q]
+  sequence b = rows cu_q[b]..cu_q[b+1]-1 of Q and cu_k[b]..cu_k[b+1]-1 of K.
 """
 from __future__ import annotations
 
@@ -54,34 +62,47 @@ def softmax_scale(d: int) -> float:
 
 
 def _check(Q, K, V):
+    """Shapes; returns B, Nq, Hq, Hkv, d, G (K, V may have Nk != Nq rows)."""
     B, N, Hq, d = Q.shape
     Bk, Nk, Hkv, dk = K.shape
-    if K.shape != V.shape or (Bk, Nk, dk) != (B, N, d):
-        raise ValueError("K, V must be [B, N, Hkv, d] matching Q [B, N, Hq, d]")
+    if K.shape != V.shape or (Bk, dk) != (B, d):
+        raise ValueError("K, V must be [B, Nk, Hkv, d] matching Q [B, Nq, Hq, d]")
     if Hq % Hkv != 0:
         raise ValueError("Hq must be a multiple of Hkv (P:1287 GROUP_SIZE)")
     return B, N, Hq, Hkv, d, Hq // Hkv
 
 
-def _allowed(rows: np.ndarray, N: int, causal: bool) -> np.ndarray:
-    """Boolean mask [len(rows), N]: key j visible to query i (reading #3)."""
-    cols = np.arange(N)
+def _allowed(rows: np.ndarray, Nq: int, Nk: int, causal: bool) -> np.ndarray:
+    """Boolean mask [len(rows), Nk]: key j visible to query i (readings #3, #22:
+    j <= i + Nk - Nq, which is j <= i when Nq == Nk)."""
+    cols = np.arange(Nk)
     if causal:
-        return cols[None, :] <= rows[:, None]
-    return np.ones((len(rows), N), dtype=bool)
+        return cols[None, :] <= rows[:, None] + (Nk - Nq)
+    return np.ones((len(rows), Nk), dtype=bool)
 
 
-def _scores(q_rows, k, rows, causal, scale):
-    """S = scale * q k^T with -inf outside A(i). q_rows [r, d], k [N, d]."""
+def _scores(q_rows, k, rows, Nq, causal, scale):
+    """S = scale * q k^T with -inf outside A(i). q_rows [r, d], k [Nk, d]."""
     S = (q_rows @ k.T) * scale
-    S[~_allowed(rows, k.shape[0], causal)] = -np.inf
+    S[~_allowed(rows, Nq, k.shape[0], causal)] = -np.inf
     return S
 
 
 def _lse(S):
-    """Stable natural-log logsumexp per row: m + ln sum exp(S - m)."""
-    m = S.max(axis=1, keepdims=True)
-    return (m + np.log(np.exp(S - m).sum(axis=1, keepdims=True)))[:, 0]
+    """Stable natural-log logsumexp per row: m + ln sum exp(S - m); -inf for a
+    row with no visible key (reading #22)."""
+    m = S.max(axis=1, keepdims=True) if S.shape[1] else np.full((S.shape[0], 1), -np.inf)
+    empty = ~np.isfinite(m)
+    m0 = np.where(empty, 0.0, m)
+    with np.errstate(divide="ignore"):
+        out = m0 + np.log(np.exp(S - m0).sum(axis=1, keepdims=True))
+    return np.where(empty, -np.inf, out)[:, 0]
+
+
+def _probs(S, lse):
+    """P_ij = exp(S_ij - LSE_i); 0 on a row with no visible key (reading #22)."""
+    live = np.isfinite(lse)
+    return np.exp(S - np.where(live, lse, 0.0)[:, None]) * live[:, None]
 
 
 def attn_fwd(Q, K, V, causal: bool):
@@ -99,9 +120,9 @@ def attn_fwd(Q, K, V, causal: bool):
             k, v = K[b, :, kvh, :], V[b, :, kvh, :]
             for r0 in range(0, N, _ROW_BLOCK):
                 rows = np.arange(r0, min(N, r0 + _ROW_BLOCK))
-                S = _scores(Q[b, rows, h, :], k, rows, causal, scale)
+                S = _scores(Q[b, rows, h, :], k, rows, N, causal, scale)
                 lse = _lse(S)
-                P = np.exp(S - lse[:, None])
+                P = _probs(S, lse)
                 O[b, rows, h, :] = P @ v
                 LSE[b, h, rows] = lse
     return O, LSE
@@ -124,9 +145,10 @@ def attn_fwd_bwd(Q, K, V, dO, causal: bool):
     O = np.zeros((B, N, Hq, d))
     LSE = np.zeros((B, Hq, N))
     Dv = np.zeros((B, Hq, N))
+    Nk = K.shape[1]
     dQ = np.zeros((B, N, Hq, d))
-    dK = np.zeros((B, N, Hkv, d))
-    dV = np.zeros((B, N, Hkv, d))
+    dK = np.zeros((B, Nk, Hkv, d))
+    dV = np.zeros((B, Nk, Hkv, d))
     for b in range(B):
         for h in range(Hq):
             kvh = h // G
@@ -135,9 +157,9 @@ def attn_fwd_bwd(Q, K, V, dO, causal: bool):
                 rows = np.arange(r0, min(N, r0 + _ROW_BLOCK))
                 q = Q[b, rows, h, :]
                 do = dO[b, rows, h, :]
-                S = _scores(q, k, rows, causal, scale)
+                S = _scores(q, k, rows, N, causal, scale)
                 lse = _lse(S)
-                P = np.exp(S - lse[:, None])
+                P = _probs(S, lse)
                 o = P @ v
                 D = (do * o).sum(axis=1)
                 dP = do @ v.T
@@ -166,9 +188,9 @@ def attn_rows(Q, K, V, dO, causal: bool, b: int, h: int, rows):
     v = np.asarray(V[b, :, kvh, :], dtype=np.float64)
     do = np.asarray(dO[b, rows, h, :], dtype=np.float64)
     scale = softmax_scale(k.shape[1])
-    S = _scores(q, k, rows, causal, scale)
+    S = _scores(q, k, rows, np.shape(Q)[1], causal, scale)
     lse = _lse(S)
-    P = np.exp(S - lse[:, None])
+    P = _probs(S, lse)
     o = P @ v
     D = (do * o).sum(axis=1)
     dP = do @ v.T
@@ -185,7 +207,7 @@ def attn_key_rows(Q, K, V, dO, causal: bool, b: int, kvh: int, keys, LSE, D):
     """
     keys = np.asarray(keys)
     B, N, Hq, d = np.shape(Q)
-    Hkv = K.shape[2]
+    Nk, Hkv = K.shape[1], K.shape[2]
     G = Hq // Hkv
     scale = softmax_scale(d)
     kj = np.asarray(K[b, keys, kvh, :], dtype=np.float64)  # [r, d]
@@ -198,9 +220,9 @@ def attn_key_rows(Q, K, V, dO, causal: bool, b: int, kvh: int, keys, LSE, D):
         do = np.asarray(dO[b, :, h, :], dtype=np.float64)
         # S^T for the sampled keys: [r, N] = scale * k_j q_i
         ST = (kj @ q.T) * scale
-        mask = _allowed(rows, N, causal)[:, keys].T           # [r, N]: query i sees key j
+        mask = _allowed(rows, N, Nk, causal)[:, keys].T       # [r, N]: query i sees key j
         ST[~mask] = -np.inf
-        PT = np.exp(ST - np.asarray(LSE[b, h], dtype=np.float64)[None, :])
+        PT = _probs(ST.T, np.asarray(LSE[b, h], dtype=np.float64)).T
         dPT = vj @ do.T
         dST = PT * (dPT - np.asarray(D[b, h], dtype=np.float64)[None, :])
         dV += PT @ do
@@ -216,18 +238,22 @@ def attn_naive(Q, K, V, dO, causal: bool):
     V = np.asarray(V, dtype=np.float64)
     dO = np.asarray(dO, dtype=np.float64)
     B, N, Hq, Hkv, d, G = _check(Q, K, V)
+    Nk = K.shape[1]
     scale = softmax_scale(d)
     O = np.zeros((B, N, Hq, d))
     LSE = np.zeros((B, Hq, N))
     Dv = np.zeros((B, Hq, N))
     dQ = np.zeros((B, N, Hq, d))
-    dK = np.zeros((B, N, Hkv, d))
-    dV = np.zeros((B, N, Hkv, d))
+    dK = np.zeros((B, Nk, Hkv, d))
+    dV = np.zeros((B, Nk, Hkv, d))
     for b in range(B):
         for h in range(Hq):
             kvh = h // G
             for i in range(N):
-                js = [j for j in range(N) if (not causal) or j <= i]
+                js = [j for j in range(Nk) if (not causal) or j <= i + (Nk - N)]
+                if not js:  # no visible key: O = 0, LSE = -inf, no gradient (reading #22)
+                    LSE[b, h, i] = -math.inf
+                    continue
                 s = {j: scale * sum(Q[b, i, h, x] * K[b, j, kvh, x] for x in range(d)) for j in js}
                 mx = max(s.values())
                 lse = mx + math.log(sum(math.exp(s[j] - mx) for j in js))
@@ -245,3 +271,42 @@ def attn_naive(Q, K, V, dO, causal: bool):
                         dK[b, j, kvh, x] += scale * ds * Q[b, i, h, x]
                         dV[b, j, kvh, x] += p[j] * dO[b, i, h, x]
     return {"O": O, "LSE": LSE, "D": Dv, "dQ": dQ, "dK": dK, "dV": dV}
+
+
+def attn_varlen_fwd_bwd(Q, K, V, dO, cu_q, cu_k, causal: bool):
+    """Packed variable-length batch (NEXT #4): sequence b is the dense problem
+    on Q rows cu_q[b]:cu_q[b+1] and K/V rows cu_k[b]:cu_k[b+1] (lengths may
+    differ; causal is bottom-right aligned per sequence, reading #22).
+
+    Q, dO [total_q, Hq, d]; K, V [total_k, Hkv, d]. Returns O, dQ like Q,
+    dK, dV like K, LSE and D [Hq, total_q]; a sequence with no keys gives
+    O = 0, LSE = -inf, dQ = 0.
+    """
+    Q = np.asarray(Q, dtype=np.float64)
+    K = np.asarray(K, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    dO = np.asarray(dO, dtype=np.float64)
+    cu_q = [int(x) for x in cu_q]
+    cu_k = [int(x) for x in cu_k]
+    if len(cu_q) != len(cu_k) or cu_q[0] != 0 or cu_k[0] != 0 or cu_q[-1] != Q.shape[0] \
+            or cu_k[-1] != K.shape[0] or any(b < a for a, b in zip(cu_q, cu_q[1:])) \
+            or any(b < a for a, b in zip(cu_k, cu_k[1:])):
+        raise ValueError("cu_q / cu_k must be monotone offsets from 0 to total_q / total_k")
+    Hq, d = Q.shape[1], Q.shape[2]
+    out = {"O": np.zeros_like(Q), "dQ": np.zeros_like(Q), "dK": np.zeros_like(K), "dV": np.zeros_like(K),
+           "LSE": np.zeros((Hq, Q.shape[0])), "D": np.zeros((Hq, Q.shape[0]))}
+    for b in range(len(cu_q) - 1):
+        qs, ks = slice(cu_q[b], cu_q[b + 1]), slice(cu_k[b], cu_k[b + 1])
+        if cu_q[b + 1] == cu_q[b]:
+            continue  # no queries: nothing to compute, dK = dV = 0 for this sequence
+        if cu_k[b + 1] == cu_k[b]:  # no keys: every row sees nothing (reading #22)
+            out["LSE"][:, qs] = -np.inf
+            continue
+        r = attn_fwd_bwd(Q[None, qs], K[None, ks], V[None, ks], dO[None, qs], causal)
+        for k in ("O", "dQ"):
+            out[k][qs] = r[k][0]
+        for k in ("dK", "dV"):
+            out[k][ks] = r[k][0]
+        for k in ("LSE", "D"):
+            out[k][:, qs] = r[k][0]
+    return out
