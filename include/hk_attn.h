@@ -66,6 +66,51 @@ hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O
                       const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
                       int B, int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream);
 
+/* ---- Sequence-length variants (reading #22).
+ * The paper's problem has Nq == Nk (P:1292 `num_tiles = ATTN_N / KV_BLOCK_SIZE`);
+ * these entry points take the baselines' API features (AITER flash_attn_func /
+ * varlen; SDPA) with the same kernels.
+ * Mask: key j is visible to query i iff j < Nk and, when causal,
+ *   j <= i + (Nk - Nq)         (bottom-right aligned; j <= i when Nq == Nk).
+ * A query row that sees no key (causal with Nq > Nk, or a varlen sequence with
+ * no keys) gets O = 0 and LSE = -inf, and adds nothing to the gradients
+ * (its dQ row is 0). */
+
+/* Dense, Nq != Nk. Q, O, dO, dQ: [B][Nq][Hq][d]; K, V, dK, dV: [B][Nk][Hkv][d];
+ * LSE: [B][Hq][Nq] fp32. Nq, Nk >= 1. Errors and ownership as above. */
+hk_status hk_attn_fwd_qk(const void* Q, const void* K, const void* V, void* O, float* LSE, int B, int Hq,
+                         int Hkv, int Nq, int Nk, int d, int causal, cudaStream_t stream);
+/* = 2*B*Hq*Nqp*4 + 256, Nqp = Nq rounded up to a multiple of 128. */
+size_t hk_attn_bwd_qk_workspace_bytes(int B, int Hq, int Hkv, int Nq, int Nk, int d);
+hk_status hk_attn_bwd_qk(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                         const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
+                         int B, int Hq, int Hkv, int Nq, int Nk, int d, int causal, cudaStream_t stream);
+
+/* Packed variable-length batch of B sequences.
+ *   Q, O, dO, dQ : [total_q][Hq][d] bf16;  K, V, dK, dV : [total_k][Hkv][d] bf16
+ *   LSE          : [Hq][total_q] fp32
+ *   cu_seqlens_q, cu_seqlens_k : DEVICE int32 [B+1], cu[0] = 0, non-decreasing,
+ *     cu_q[B] = total_q, cu_k[B] = total_k; sequence b is Q rows
+ *     cu_q[b] .. cu_q[b+1]-1 against K/V rows cu_k[b] .. cu_k[b+1]-1
+ *     (lengths may differ per sequence and between Q and K, and may be 0).
+ *   max_seqlen_q / max_seqlen_k : >= every sequence's length (sizes the grid).
+ * total_q, total_k, max_seqlen_* >= 1. The cu_seqlens contents live on the
+ * device and are NOT validated (that would need a host sync): offsets that
+ * break the contract give undefined results, and rows beyond a sequence's
+ * max_seqlen are not computed. A query sequence with no keys gets O = 0,
+ * LSE = -inf, dQ = 0; keys no query sees get dK = dV = 0. */
+hk_status hk_attn_fwd_varlen(const void* Q, const void* K, const void* V, void* O, float* LSE,
+                             const int* cu_seqlens_q, const int* cu_seqlens_k, int B, int Hq, int Hkv,
+                             int total_q, int total_k, int max_seqlen_q, int max_seqlen_k, int d, int causal,
+                             cudaStream_t stream);
+/* = 2*B*Hq*Mp*4 + 256, Mp = max_seqlen_q rounded up to a multiple of 128. */
+size_t hk_attn_bwd_varlen_workspace_bytes(int B, int Hq, int Hkv, int max_seqlen_q, int max_seqlen_k, int d);
+hk_status hk_attn_bwd_varlen(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                             const void* dO, void* dQ, void* dK, void* dV, void* workspace,
+                             size_t workspace_bytes, const int* cu_seqlens_q, const int* cu_seqlens_k, int B,
+                             int Hq, int Hkv, int total_q, int total_k, int max_seqlen_q, int max_seqlen_k, int d,
+                             int causal, cudaStream_t stream);
+
 const char* hk_attn_last_error(void);
 const char* hk_status_string(hk_status s);
 int hk_attn_abi_version(void);

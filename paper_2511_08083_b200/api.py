@@ -32,31 +32,39 @@ def _check_tensor(name, t, dtype=torch.bfloat16):
 
 
 def _shapes(q, k, v):
+    """Returns B, Nq, Nk, Hq, Hkv, d (Nq != Nk allowed: bottom-right causal, hk_attn.h)."""
     if q.dim() != 4 or k.dim() != 4 or v.shape != k.shape:
-        raise ValueError("q must be [B,N,Hq,d]; k, v [B,N,Hkv,d]")
+        raise ValueError("q must be [B,Nq,Hq,d]; k, v [B,Nk,Hkv,d]")
     B, N, Hq, d = q.shape
-    if k.shape[0] != B or k.shape[1] != N or k.shape[3] != d:
+    if k.shape[0] != B or k.shape[3] != d:
         raise ValueError("k/v shape mismatch with q")
-    return B, N, Hq, k.shape[2], d
+    return B, N, k.shape[1], Hq, k.shape[2], d
 
 
 def attn_fwd(q, k, v, causal: bool = False, out=None, lse=None):
-    """O, LSE = attention(q, k, v). q [B,N,Hq,d], k/v [B,N,Hkv,d] bf16 CUDA.
-    Returns (o [B,N,Hq,d] bf16, lse [B,Hq,N] fp32, natural log)."""
+    """O, LSE = attention(q, k, v). q [B,Nq,Hq,d], k/v [B,Nk,Hkv,d] bf16 CUDA.
+    Returns (o [B,Nq,Hq,d] bf16, lse [B,Hq,Nq] fp32, natural log). Nq != Nk
+    uses hk_attn_fwd_qk (causal mask bottom-right aligned)."""
     for n, t in (("q", q), ("k", k), ("v", v)):
         _check_tensor(n, t)
-    B, N, Hq, Hkv, d = _shapes(q, k, v)
+    B, N, Nk, Hq, Hkv, d = _shapes(q, k, v)
     o = torch.empty_like(q) if out is None else out
     L = torch.empty((B, Hq, N), dtype=torch.float32, device=q.device) if lse is None else lse
     _check_tensor("out", o)
     _check_tensor("lse", L, torch.float32)
-    check(lib().hk_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, Hq, Hkv, N, d, int(bool(causal)),
-                            _stream()))
+    if N == Nk:
+        check(lib().hk_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, Hq, Hkv, N, d, int(bool(causal)),
+                                _stream()))
+    else:
+        check(lib().hk_attn_fwd_qk(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, Hq, Hkv, N, Nk, d,
+                                   int(bool(causal)), _stream()))
     return o, L
 
 
-def bwd_workspace_bytes(B, Hq, Hkv, N, d) -> int:
-    return int(lib().hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d))
+def bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk=None) -> int:
+    if Nk is None or Nk == N:
+        return int(lib().hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d))
+    return int(lib().hk_attn_bwd_qk_workspace_bytes(B, Hq, Hkv, N, Nk, d))
 
 
 def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None, dk=None, dv=None):
@@ -65,15 +73,67 @@ def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None,
     for n, t in (("q", q), ("k", k), ("v", v), ("o", o), ("do", do)):
         _check_tensor(n, t)
     _check_tensor("lse", lse, torch.float32)
-    B, N, Hq, Hkv, d = _shapes(q, k, v)
+    B, N, Nk, Hq, Hkv, d = _shapes(q, k, v)
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
-    nbytes = bwd_workspace_bytes(B, Hq, Hkv, N, d)
+    nbytes = bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk)
     ws = torch.empty(nbytes // 4, dtype=torch.float32, device=q.device) if workspace is None else workspace
-    check(lib().hk_attn_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
-                            _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), B, Hq, Hkv, N, d,
-                            int(bool(causal)), _stream()))
+    if N == Nk:
+        check(lib().hk_attn_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
+                                _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), B, Hq, Hkv, N, d,
+                                int(bool(causal)), _stream()))
+    else:
+        check(lib().hk_attn_bwd_qk(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
+                                   _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), B, Hq, Hkv, N, Nk, d,
+                                   int(bool(causal)), _stream()))
+    return dq, dk, dv
+
+
+def _varlen_args(q, k, v, cu_seqlens_q, cu_seqlens_k):
+    for n, t in (("q", q), ("k", k), ("v", v)):
+        _check_tensor(n, t)
+    _check_tensor("cu_seqlens_q", cu_seqlens_q, torch.int32)
+    _check_tensor("cu_seqlens_k", cu_seqlens_k, torch.int32)
+    if q.dim() != 3 or k.dim() != 3 or v.shape != k.shape or k.shape[2] != q.shape[2]:
+        raise ValueError("q must be [total_q,Hq,d]; k, v [total_k,Hkv,d]")
+    if cu_seqlens_q.dim() != 1 or cu_seqlens_q.shape != cu_seqlens_k.shape or cu_seqlens_q.numel() < 2:
+        raise ValueError("cu_seqlens_q / cu_seqlens_k must be int32 [B+1]")
+    return cu_seqlens_q.numel() - 1, q.shape[0], k.shape[0], q.shape[1], k.shape[1], q.shape[2]
+
+
+def attn_fwd_varlen(q, k, v, cu_seqlens_q, cu_seqlens_k, max_seqlen_q: int, max_seqlen_k: int,
+                    causal: bool = False, out=None, lse=None):
+    """Packed variable-length attention (hk_attn_fwd_varlen). q [total_q,Hq,d],
+    k/v [total_k,Hkv,d] bf16; cu_seqlens_* int32 [B+1] on the device (not
+    validated: see hk_attn.h). Returns (o [total_q,Hq,d], lse [Hq,total_q] fp32)."""
+    B, tq, tk, Hq, Hkv, d = _varlen_args(q, k, v, cu_seqlens_q, cu_seqlens_k)
+    o = torch.empty_like(q) if out is None else out
+    L = torch.empty((Hq, tq), dtype=torch.float32, device=q.device) if lse is None else lse
+    _check_tensor("out", o)
+    _check_tensor("lse", L, torch.float32)
+    check(lib().hk_attn_fwd_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), _ptr(cu_seqlens_q),
+                                   _ptr(cu_seqlens_k), B, Hq, Hkv, tq, tk, int(max_seqlen_q), int(max_seqlen_k), d,
+                                   int(bool(causal)), _stream()))
+    return o, L
+
+
+def attn_bwd_varlen(q, k, v, o, lse, do, cu_seqlens_q, cu_seqlens_k, max_seqlen_q: int, max_seqlen_k: int,
+                    causal: bool = False, workspace=None, dq=None, dk=None, dv=None):
+    """Backward of attn_fwd_varlen (hk_attn_bwd_varlen). Returns (dq, dk, dv) bf16."""
+    B, tq, tk, Hq, Hkv, d = _varlen_args(q, k, v, cu_seqlens_q, cu_seqlens_k)
+    for n, t in (("o", o), ("do", do)):
+        _check_tensor(n, t)
+    _check_tensor("lse", lse, torch.float32)
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    nbytes = int(lib().hk_attn_bwd_varlen_workspace_bytes(B, Hq, Hkv, int(max_seqlen_q), int(max_seqlen_k), d))
+    ws = torch.empty(nbytes // 4, dtype=torch.float32, device=q.device) if workspace is None else workspace
+    check(lib().hk_attn_bwd_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
+                                   _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), _ptr(cu_seqlens_q),
+                                   _ptr(cu_seqlens_k), B, Hq, Hkv, tq, tk, int(max_seqlen_q), int(max_seqlen_k), d,
+                                   int(bool(causal)), _stream()))
     return dq, dk, dv
 
 
@@ -139,6 +199,23 @@ class Attention(torch.autograd.Function):
         q, k, v, o, lse = ctx.saved_tensors
         dq, dk, dv = attn_bwd(q, k, v, o, lse, do.contiguous(), ctx.causal)
         return dq, dk, dv, None
+
+
+class AttentionVarlen(torch.autograd.Function):
+    """autograd wrapper: AttentionVarlen.apply(q, k, v, cu_q, cu_k, max_q, max_k, causal) -> o."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, cu_q, cu_k, max_q, max_k, causal=False):
+        o, lse = attn_fwd_varlen(q, k, v, cu_q, cu_k, max_q, max_k, causal)
+        ctx.save_for_backward(q, k, v, o, lse, cu_q, cu_k)
+        ctx.args = (max_q, max_k, causal)
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, o, lse, cu_q, cu_k = ctx.saved_tensors
+        dq, dk, dv = attn_bwd_varlen(q, k, v, o, lse, do.contiguous(), cu_q, cu_k, *ctx.args)
+        return dq, dk, dv, None, None, None, None, None
 
 
 def diag_umma(a, b, n, k, a_tmem: bool, b_mn: bool):

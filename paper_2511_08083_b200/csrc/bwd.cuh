@@ -20,22 +20,30 @@
 
 #include "../../include/hk_attn.h"
 #include "ptx.cuh"
+#include "seq.cuh"
 #include "tma_host.h"
 
 namespace hk {
 
 // ---------------------------------------------------------------- B0
-// One group of d/8 lanes per (b, n, h) row (16-B loads), rows in memory order.
+// Grid (x, b): one group of d/8 lanes per (n, h) row of sequence b (16-B loads),
+// rows in memory order. Workspace rows n in [lq, Np) of each (b, h) are padding:
+// LSE2 = +inf and D = 0, so padded query rows of a last tile give P = 0 and
+// dS = 0 in the dK/dV pass. A row that saw no key (LSE = -inf, O = 0) gets
+// LSE2 = +inf as well: P = 0, no gradient (reading #22).
 template <int D>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ O,
                                                       const __nv_bfloat16* __restrict__ dO,
                                                       const float* __restrict__ lse, float* __restrict__ Dout,
-                                                      float* __restrict__ lse2, int B, int N, int H, int Np,
+                                                      float* __restrict__ lse2, SeqGeom g, int H, int Np,
                                                       unsigned* __restrict__ sched) {
-  if (blockIdx.x == 0 && threadIdx.x < 4) sched[threadIdx.x] = 0u;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 4) sched[threadIdx.x] = 0u;
   constexpr int LPR = D / 8;  // lanes per row
   constexpr int RPW = 32 / LPR;
-  const size_t rows = (size_t)B * N * H;
+  const int b = blockIdx.y;
+  const Seq sq = seq_of(g, b);
+  const size_t rows = (size_t)sq.lq * H;
+  const size_t row0 = (size_t)sq.gq0 * H;  // first (n, h) row of this sequence in O / dO
   const int sub = threadIdx.x % LPR;
   const size_t gwarp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const size_t nwarps = (size_t)gridDim.x * blockDim.x / 32;
@@ -44,8 +52,8 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
     const size_t row = base + lrow;
     float acc = 0.f;
     if (row < rows) {
-      const uint4 a = __ldg(reinterpret_cast<const uint4*>(O + row * D) + sub);
-      const uint4 g = __ldg(reinterpret_cast<const uint4*>(dO + row * D) + sub);
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(O + (row0 + row) * D) + sub);
+      const uint4 g = __ldg(reinterpret_cast<const uint4*>(dO + (row0 + row) * D) + sub);
       const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&a);
       const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&g);
 #pragma unroll
@@ -58,32 +66,32 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
 #pragma unroll
     for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (row < rows && sub == 0) {
-      const size_t h = row % H, n = (row / H) % N, b = row / ((size_t)H * N);
-      const size_t idx = (b * H + h) * Np + n;  // workspace rows are padded to Np
+      const int h = (int)(row % H), n = (int)(row / H);
+      const size_t idx = ((size_t)b * H + h) * Np + n;  // workspace rows are padded to Np
+      const float L = lse[lse_index(g, sq, b, H, h, n)];
       Dout[idx] = acc;
-      lse2[idx] = lse[(b * H + h) * N + n] * 1.4426950408889634f;
+      lse2[idx] = L == -INFINITY ? INFINITY : L * 1.4426950408889634f;
     }
   }
-  // ragged N: padding rows of each (b, h) get LSE2 = +inf and D = 0, so the padded
-  // query rows of the last tile give P = 0 and dS = 0 in the dK/dV pass
-  if (Np > N) {
-    const size_t pad = (size_t)Np - N, npad = (size_t)B * H * pad;
+  if (Np > sq.lq) {
+    const size_t pad = (size_t)Np - sq.lq, npad = (size_t)H * pad;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad; i += (size_t)gridDim.x * blockDim.x) {
-      const size_t bh = i / pad, n = N + i % pad;
-      Dout[bh * Np + n] = 0.f;
-      lse2[bh * Np + n] = INFINITY;
+      const size_t idx = ((size_t)b * H + i / pad) * Np + sq.lq + i % pad;
+      Dout[idx] = 0.f;
+      lse2[idx] = INFINITY;
     }
   }
 }
 
 struct BwdParams {
-  const float* Dv;    // [B][Hq][Np], Np = N rounded up to 128
+  const float* Dv;    // [B][Hq][Np], Np = Nq (varlen: max_seqlen_q) rounded up to 128
   const float* lse2;  // [B][Hq][Np]
-  __nv_bfloat16* dq;  // [B][N][Hq][D]
-  __nv_bfloat16* dk;  // [B][N][Hkv][D]
-  __nv_bfloat16* dv;  // [B][N][Hkv][D]
+  __nv_bfloat16* dq;  // dense [B][Nq][Hq][D]; varlen [total_q][Hq][D]
+  __nv_bfloat16* dk;  // dense [B][Nk][Hkv][D]; varlen [total_k][Hkv][D]
+  __nv_bfloat16* dv;
   unsigned* sched;    // [4] work counters in the workspace: dK/dV draw, done; dQ draw, done
-  int B, Hq, Hkv, N, Np;
+  SeqGeom g;          // dense / varlen geometry (seq.cuh)
+  int B, Hq, Hkv, Np, Npk;  // Npk = Nk (varlen: max_seqlen_k) rounded up to 128
 };
 
 // Dynamic work distribution for the persistent backward kernels: the TMA lane
@@ -224,20 +232,26 @@ __device__ __forceinline__ void tmem_st_packed64(uint32_t taddr, const float (&v
 // work overlaps dV(i+1)/S^T(i+2). The next item's first dV/dK (which overwrite
 // the accumulators) need its first P^T/dS^T, which the elementwise warps
 // publish only after reading this item's dV/dK out.
+// n_it == 0: no query sees this key tile (or it holds no key); the producer and
+// the MMA warp skip the item, the elementwise warps write dK = dV = 0 for its keys.
 struct KvItem {
-  int jt, kvh, b, i0, n_it;
+  Seq sq;
+  int jt, kvh, b, i0, nqt, n_it;
 };
 template <bool CAUSAL>
 __device__ __forceinline__ KvItem kv_decode(const BwdParams& p, int item) {
-  const int T = p.Np / 128;
+  const int T = p.Npk / 128;
   const int tr = item % T;
   const int rest = item / T;
   KvItem it;
   it.kvh = rest % p.Hkv;
   it.b = rest / p.Hkv;
-  it.jt = CAUSAL ? T - 1 - tr : tr;  // heaviest first
-  it.i0 = CAUSAL ? it.jt : 0;        // first query block that sees key tile jt
-  it.n_it = (p.Hq / p.Hkv) * (T - it.i0);
+  it.sq = seq_of(p.g, it.b);
+  it.jt = CAUSAL ? T - 1 - tr : tr;              // heaviest first
+  it.i0 = first_q_tile_for<CAUSAL>(it.sq, it.jt);  // first query block that sees key tile jt
+  it.nqt = (it.sq.lq + 127) / 128;
+  const bool live = it.jt * 128 < it.sq.lk && it.i0 < it.nqt;
+  it.n_it = live ? (p.Hq / p.Hkv) * (it.nqt - it.i0) : 0;
   return it;
 }
 
@@ -272,9 +286,8 @@ __global__ void __launch_bounds__(320, 1)
   static_assert((2 * NSA + 2 * NSB + 8) * 8 + sizeof(Sched) <= C::BAR_BYTES, "barrier area");
 
   const int warp = warp_id(), lane = lane_id();
-  const int T = p.Np / 128;
   const int G = p.Hq / p.Hkv;
-  const int num_items = p.B * p.Hkv * T;
+  const int num_items = p.B * p.Hkv * (p.Npk / 128);
 
   if (threadIdx.x == 0) {
     sched_init(sched);
@@ -316,18 +329,22 @@ __global__ void __launch_bounds__(320, 1)
       const uint64_t pol_stream = policy_evict_normal();
       int u = 0;  // ring uses so far (rings A and B advance together, one use per block)
       uint32_t kvf_ph = 0;
+      bool first = true;
       for (int r = 0;; ++r) {
         const int item = sched_publish(sched, p.sched, r);
         if (item >= num_items) break;
         const KvItem w = kv_decode<CAUSAL>(p, item);
-        if (r > 0) {  // K, V tiles free once the previous item's last S^T / dP^T completed
+        if (w.n_it == 0) continue;
+        if (!first) {  // K, V tiles free once the previous item's last S^T / dP^T completed
           mbar_wait(&bar_kvfree, kvf_ph);
           kvf_ph ^= 1;
         }
+        first = false;
+        const int krow = w.sq.k0 + w.jt * 128;
         mbar_arrive_expect_tx(&bar_kv, 2 * C::T128);
         for (int pn = 0; pn < C::PANELS; ++pn) {
-          tma_load_4d(&mapK, &bar_kv, sK + pn * 128 * 128, pn * 64, w.kvh, w.jt * 128, w.b, pol_stream);
-          tma_load_4d(&mapV, &bar_kv, sV + pn * 128 * 128, pn * 64, w.kvh, w.jt * 128, w.b, pol_stream);
+          tma_load_4d(&mapK, &bar_kv, sK + pn * 128 * 128, pn * 64, w.kvh, krow, w.sq.tb, pol_stream);
+          tma_load_4d(&mapV, &bar_kv, sV + pn * 128 * 128, pn * 64, w.kvh, krow, w.sq.tb, pol_stream);
         }
         // blocking waits (the hardware suspends the warp: no issue slots taken
         // from the elementwise warps sharing its SM sub-partition)
@@ -338,16 +355,17 @@ __global__ void __launch_bounds__(320, 1)
           hk_trace(20, u, 0);  // producer: ring A slot free, loads for it issued
           mbar_arrive_expect_tx(&fullA[sa], C::T128);
           for (int pn = 0; pn < C::PANELS; ++pn)
-            tma_load_4d(&mapQ, &fullA[sa], sA + sa * C::T128 + pn * 128 * 128, pn * 64, h, qi * 128, w.b, pol_keep);
+            tma_load_4d(&mapQ, &fullA[sa], sA + sa * C::T128 + pn * 128 * 128, pn * 64, h, w.sq.q0 + qi * 128,
+                        w.sq.tb, pol_keep);
           mbar_wait(&emptyB[sb], ((u / NSB) & 1) ^ 1);
           uint8_t* st = sB + sb * C::SLOT_B1;
           mbar_arrive_expect_tx(&fullB[sb], C::T128 + 1024);
           for (int pn = 0; pn < C::PANELS; ++pn)
-            tma_load_4d(&mapdO, &fullB[sb], st + pn * 128 * 128, pn * 64, h, qi * 128, w.b, pol_keep);
+            tma_load_4d(&mapdO, &fullB[sb], st + pn * 128 * 128, pn * 64, h, w.sq.q0 + qi * 128, w.sq.tb, pol_keep);
           const size_t off = ((size_t)w.b * p.Hq + h) * p.Np + (size_t)qi * 128;
           bulk_load(st + C::T128, p.lse2 + off, 512, &fullB[sb]);
           bulk_load(st + C::T128 + 512, p.Dv + off, 512, &fullB[sb]);
-          if (++qi == T) {
+          if (++qi == w.nqt) {
             qi = w.i0;
             ++h;
           }
@@ -376,12 +394,14 @@ __global__ void __launch_bounds__(320, 1)
     };
     int u0 = 0;  // ring uses before this item == blocks before this item
     uint32_t kv_ph = 0;
-    int r = 0;
-    for (;; ++r) {
+    int busy = 0;  // items with work so far (one bar_kv / bar_kvfree phase each)
+    for (int r = 0;; ++r) {
       const int item = sched_take(sched, r);
       if (item >= num_items) break;
       const KvItem w = kv_decode<CAUSAL>(p, item);
       const int n = w.n_it;
+      if (n == 0) continue;
+      ++busy;
       mbar_wait(&bar_kv, kv_ph);
       kv_ph ^= 1;
       mbar_wait(&fullA[u0 % NSA], (u0 / NSA) & 1);
@@ -426,7 +446,7 @@ __global__ void __launch_bounds__(320, 1)
     // the releases of the final uses are never waited for by the producer: let them land
     drain_ring(emptyA, NSA, u0);
     drain_ring(emptyB, NSB, u0);
-    if (r > 0) mbar_wait(&bar_kvfree, (r - 1) & 1);
+    if (busy > 0) mbar_wait(&bar_kvfree, (busy - 1) & 1);
   } else {
     // ================= elementwise warpgroups (warps 0-7) =================
     const int wg = warp >> 2;              // query columns [64 wg, 64 wg + 64) of each block
@@ -441,6 +461,16 @@ __global__ void __launch_bounds__(320, 1)
       if (item >= num_items) break;
       const KvItem w = kv_decode<CAUSAL>(p, item);
       const int key = w.jt * 128 + r;
+      const bool key_ok = key < w.sq.lk;  // key rows of a ragged last tile beyond the sequence are not stored
+      __nv_bfloat16* out = (wg == 0 ? p.dv : p.dk) + ((size_t)(w.sq.gk0 + (key_ok ? key : 0)) * p.Hkv + w.kvh) * D;
+      if (w.n_it == 0) {  // no query sees these keys: dK = dV = 0
+        if (key_ok) {
+#pragma unroll
+          for (int k = 0; k < D / 8; ++k) reinterpret_cast<uint4*>(out)[k] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        continue;
+      }
+      const int off = w.sq.lk - w.sq.lq;  // bottom-right causal alignment
       int qi = w.i0;
       for (int it = 0; it < w.n_it; ++it, ++u) {
         const uint8_t* vec = sB + s * C::SLOT_B1 + C::T128;  // lse2 [128], then D [128]
@@ -468,10 +498,10 @@ __global__ void __launch_bounds__(320, 1)
           v[c4 + 2] = eb.x;
           v[c4 + 3] = eb.y;
         }
-        if (CAUSAL && qi == w.jt) {
+        if (CAUSAL && qi * 128 + off < w.jt * 128 + 127) {
 #pragma unroll
           for (int cc = 0; cc < 64; ++cc)
-            if (q0 + cc < key) v[cc] = 0.f;  // query < key is masked
+            if (q0 + cc + off < key) v[cc] = 0.f;  // key > query + (lk - lq) is masked
         }
         tmem_st_packed64(tmem_addr(cS, lb, 0), v);
         tmem_wait_st();
@@ -501,7 +531,7 @@ __global__ void __launch_bounds__(320, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_ds);
         if (threadIdx.x == 0) hk_trace(5, u, 0);
-        if (++qi == T) qi = w.i0;
+        if (++qi == w.nqt) qi = w.i0;
         if (++s == NSB) s = 0;
       }
       // ---- epilogue: WG0 writes dV, WG1 writes dK * (1/sqrt d)
@@ -510,9 +540,6 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_after();
       const float scale = wg == 0 ? 1.f : rsqrtf((float)D);
       const uint32_t tacc = wg == 0 ? tdV : tdK;
-      const bool key_ok = key < p.N;  // key rows of a ragged last tile beyond N are not stored
-      __nv_bfloat16* out =
-          (wg == 0 ? p.dv : p.dk) + (((size_t)w.b * p.N + (key_ok ? key : 0)) * p.Hkv + w.kvh) * D;
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t o[32];
@@ -554,7 +581,10 @@ __global__ void __launch_bounds__(320, 1)
 // bf16 dS overwrites dP. S is single-buffered but released as soon as the
 // elementwise warps have loaded it (bar_sfree), so S(j+1) still overlaps the
 // exponentials of block j. MMA order: S(j+1), dQ(j) [needs dS(j)], dP(j+1).
+// n_it == 0: the tile holds no query row, or none of its rows sees a key; the
+// producer and the MMA warp skip the item, the elementwise warps write dQ = 0.
 struct DqItem {
+  Seq sq;
   int iq, h, kvh, b, n_it;
 };
 template <bool CAUSAL>
@@ -570,7 +600,8 @@ __device__ __forceinline__ DqItem dq_decode(const BwdParams& p, int item) {
   it.b = rest / p.Hkv;
   it.h = it.kvh * G + hg;
   it.iq = CAUSAL ? T - 1 - tr : tr;  // heaviest first
-  it.n_it = CAUSAL ? it.iq + 1 : T;  // 128-key blocks
+  it.sq = seq_of(p.g, it.b);
+  it.n_it = kv_tiles_for<CAUSAL>(it.sq, it.iq);  // 128-key blocks
   return it;
 }
 
@@ -640,7 +671,8 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&emptyA[sa], ((ua / NSA) & 1) ^ 1);
         mbar_arrive_expect_tx(&fullA[sa], C::T128);
         for (int pn = 0; pn < C::PANELS; ++pn)
-          tma_load_4d(&mapK, &fullA[sa], sA + sa * C::T128 + pn * 128 * 128, pn * 64, w.kvh, j * 128, w.b, pol_keep);
+          tma_load_4d(&mapK, &fullA[sa], sA + sa * C::T128 + pn * 128 * 128, pn * 64, w.kvh, w.sq.k0 + j * 128,
+                      w.sq.tb, pol_keep);
         ++ua;
       };
       auto load_b = [&](const CUtensorMap* map, int head, int row0, int b, uint64_t pol) {
@@ -655,13 +687,14 @@ __global__ void __launch_bounds__(320, 1)
         const int item = sched_publish(sched, ctr, r);
         if (item >= num_items) break;
         const DqItem w = dq_decode<CAUSAL>(p, item);
-        load_b(&mapQ, w.h, w.iq * 128, w.b, pol_stream);
-        load_b(&mapdO, w.h, w.iq * 128, w.b, pol_stream);
+        if (w.n_it == 0) continue;
+        load_b(&mapQ, w.h, w.sq.q0 + w.iq * 128, w.sq.tb, pol_stream);
+        load_b(&mapdO, w.h, w.sq.q0 + w.iq * 128, w.sq.tb, pol_stream);
         // K (ring A, freed after dQ) for block it+1 goes out right after V (ring B,
         // freed after dP) for block it, keeping K one block ahead.
         load_k(w, 0);
         for (int it = 0; it < w.n_it; ++it) {
-          load_b(&mapV, w.kvh, it * 128, w.b, pol_keep);
+          load_b(&mapV, w.kvh, w.sq.k0 + it * 128, w.sq.tb, pol_keep);
           if (it + 1 < w.n_it) load_k(w, it + 1);
         }
       }
@@ -692,6 +725,7 @@ __global__ void __launch_bounds__(320, 1)
       if (item >= num_items) break;
       const DqItem w = dq_decode<CAUSAL>(p, item);
       const int n = w.n_it;
+      if (n == 0) continue;
       const int a0 = ua, v0 = ub + 2;  // ring B: Q_i at ub, dO_i at ub + 1, V_j at v0 + j
       mbar_wait(&bar_qa, qa_ph);        // Q_A, dO_A of this item in TMEM
       qa_ph ^= 1;
@@ -764,11 +798,24 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_qa);
     };
+    auto busy = [&](int it) { return it < num_items && dq_decode<CAUSAL>(p, it).n_it > 0; };
     int item = sched_take(sched, 0);
-    if (item < num_items) copy_in();
+    if (busy(item)) copy_in();
     for (int rr = 1; item < num_items; ++rr) {
       const DqItem w = dq_decode<CAUSAL>(p, item);
       const int q = w.iq * 128 + r;
+      const bool q_ok = q < w.sq.lq;  // query rows of a ragged last tile beyond the sequence are not stored
+      __nv_bfloat16* out = p.dq + ((size_t)(w.sq.gq0 + (q_ok ? q : 0)) * p.Hq + w.h) * D + wg * (D / 2);
+      if (w.n_it == 0) {  // no key visible to these rows: dQ = 0
+        if (q_ok) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) reinterpret_cast<uint4*>(out)[k] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        item = sched_take(sched, rr);
+        if (busy(item)) copy_in();
+        continue;
+      }
+      const int off = w.sq.lk - w.sq.lq;  // bottom-right causal alignment
       const size_t vrow = ((size_t)w.b * p.Hq + w.h) * p.Np + q;
       const float l2 = p.lse2[vrow], Dq = p.Dv[vrow];
       for (int it = 0; it < w.n_it; ++it, ++g) {
@@ -789,11 +836,14 @@ __global__ void __launch_bounds__(320, 1)
           v[2 * k] = e.x;
           v[2 * k + 1] = e.y;
         }
-        if (CAUSAL && it == w.iq) {
+        // keys beyond the sequence (ragged / varlen tail: K may hold the next
+        // sequence's rows) and, when causal, keys > query + (lk - lq) are masked
+        if ((it + 1) * 128 > w.sq.lk || (CAUSAL && it * 128 + 127 > w.iq * 128 + off)) {
           const int k0 = it * 128 + 64 * wg;
+          const int klim = CAUSAL ? min(q + off, w.sq.lk - 1) : w.sq.lk - 1;
 #pragma unroll
           for (int cc = 0; cc < 64; ++cc)
-            if (k0 + cc > q) v[cc] = 0.f;
+            if (k0 + cc > klim) v[cc] = 0.f;
         }
         if (threadIdx.x == 0) hk_trace(3, g, 1);
         mbar_wait(&bar_dp, g & 1);
@@ -824,10 +874,8 @@ __global__ void __launch_bounds__(320, 1)
       // the next item's Q/dO go into TMEM before dQ is stored: its S/dP start now.
       // (Its dQ MMAs, which overwrite this accumulator, follow this WG's reads.)
       item = sched_take(sched, rr);  // look ahead: is there a next item?
-      if (item < num_items) copy_in();
+      if (busy(item)) copy_in();
       const float scale = rsqrtf((float)D);
-      const bool q_ok = q < p.N;  // query rows of a ragged last tile beyond N are not stored
-      __nv_bfloat16* out = p.dq + (((size_t)w.b * p.N + (q_ok ? q : 0)) * p.Hq + w.h) * D + wg * (D / 2);
 #pragma unroll
       for (int c0 = 0; c0 < D / 2; c0 += 8) {
         uint4 o4;
@@ -852,18 +900,31 @@ inline bool set_smem(F* fn, uint32_t bytes) {
                               (int)bytes) == cudaSuccess;
 }
 
+// Geometry of one backward call: dense (cu_q == nullptr: Q [B][Nq][Hq][d],
+// K [B][Nk][Hkv][d]) or varlen (Q [total_q][Hq][d], K [total_k][Hkv][d]).
+struct BwdShape {
+  const int* cu_q;
+  const int* cu_k;
+  int B, Hq, Hkv, Nq, Nk;  // varlen: Nq, Nk = max_seqlen_q, max_seqlen_k
+  int total_q, total_k;    // varlen only
+};
+
 template <int D, bool CAUSAL>
 hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,
-                       void* dQ, void* dK, void* dV, float* ws, int B, int Hq, int Hkv, int N, cudaStream_t stream,
-                       char* err, size_t errlen, int phase, int num_sms) {
+                       void* dQ, void* dK, void* dV, float* ws, const BwdShape& sh, cudaStream_t stream, char* err,
+                       size_t errlen, int phase, int num_sms) {
   using C = BwdCfg<D>;
-  const int Np = (N + 127) / 128 * 128;  // workspace rows padded to whole tiles
+  const int B = sh.B, Hq = sh.Hq, Hkv = sh.Hkv;
+  const int Np = (sh.Nq + 127) / 128 * 128;   // workspace rows padded to whole tiles
+  const int Npk = (sh.Nk + 127) / 128 * 128;  // key tiles
   float* Dv = ws;
   float* lse2 = ws + (size_t)B * Hq * Np;
   // every operand tile is a 128-row box (two 64-column panels at D=128)
+  const bool varlen = sh.cu_q != nullptr;
+  const int mb = varlen ? 1 : B, mnq = varlen ? sh.total_q : sh.Nq, mnk = varlen ? sh.total_k : sh.Nk;
   CUtensorMap mQ, mdO, mK, mV;
-  bool ok = encode_bnhd(&mQ, Q, B, N, Hq, D, 128) && encode_bnhd(&mdO, dO, B, N, Hq, D, 128) &&
-            encode_bnhd(&mK, K, B, N, Hkv, D, 128) && encode_bnhd(&mV, V, B, N, Hkv, D, 128);
+  bool ok = encode_bnhd(&mQ, Q, mb, mnq, Hq, D, 128) && encode_bnhd(&mdO, dO, mb, mnq, Hq, D, 128) &&
+            encode_bnhd(&mK, K, mb, mnk, Hkv, D, 128) && encode_bnhd(&mV, V, mb, mnk, Hkv, D, 128);
   if (!ok) {
     snprintf(err, errlen, "cuTensorMapEncodeTiled failed (CUresult %d)", last_encode_result());
     return HK_ERR_DEVICE;
@@ -879,29 +940,34 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     if (dev < 64) attr_done[dev] = true;
   }
   unsigned* sched = reinterpret_cast<unsigned*>(ws + (size_t)2 * B * Hq * Np);  // 4 counters after D, LSE2
+  SeqGeom g{sh.cu_q, sh.cu_k, sh.Nq, sh.Nk, sh.total_q};
   BwdParams p{Dv,
               lse2,
               reinterpret_cast<__nv_bfloat16*>(dQ),
               reinterpret_cast<__nv_bfloat16*>(dK),
               reinterpret_cast<__nv_bfloat16*>(dV),
               sched,
+              g,
               B,
               Hq,
               Hkv,
-              N,
-              Np};
-  // B0
-  const size_t rows = (size_t)B * N * Hq;
+              Np,
+              Npk};
+  // B0: grid (x, b), x sized for the longest sequence and capped at ~16 blocks per SM overall
+  const size_t rows = (size_t)sh.Nq * Hq;
   const size_t warps_needed = (rows + (32 / (D / 8)) - 1) / (32 / (D / 8));
-  size_t blocks = (warps_needed + 7) / 8;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  size_t bx = (warps_needed + 7) / 8;
+  size_t cap = (size_t)num_sms * 16 / (size_t)B;
+  if (cap < 1) cap = 1;
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
   if (phase < 0 || phase == 0)
-    bwd_pre_kernel<D><<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(O),
-                                                              reinterpret_cast<const __nv_bfloat16*>(dO), LSE, Dv,
-                                                              lse2, B, N, Hq, Np, sched);
+    bwd_pre_kernel<D><<<dim3((unsigned)bx, (unsigned)B), 256, 0, stream>>>(
+        reinterpret_cast<const __nv_bfloat16*>(O), reinterpret_cast<const __nv_bfloat16*>(dO), LSE, Dv, lse2, g, Hq,
+        Np, sched);
   // B1, B2
   if (phase < 0 || phase == 1) {
-    const int items = B * Hkv * (Np / 128);  // persistent: one CTA per SM
+    const int items = B * Hkv * (Npk / 128);  // persistent: one CTA per SM
     bwd_dkdv_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS, C::SMEM1, stream>>>(mQ, mdO, mK,
                                                                                                     mV, p);
   }
@@ -918,14 +984,13 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
 }
 
 inline hk_status launch_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
-                            const void* dO, void* dQ, void* dK, void* dV, float* ws, int B, int Hq, int Hkv, int N,
-                            int d, bool causal, cudaStream_t stream, char* err, size_t errlen, int phase,
-                            int num_sms) {
+                            const void* dO, void* dQ, void* dK, void* dV, float* ws, const BwdShape& sh, int d,
+                            bool causal, cudaStream_t stream, char* err, size_t errlen, int phase, int num_sms) {
   if (d == 64)
-    return causal ? launch_bwd_t<64, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase, num_sms)
-                  : launch_bwd_t<64, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase, num_sms);
-  return causal ? launch_bwd_t<128, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase, num_sms)
-                : launch_bwd_t<128, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, B, Hq, Hkv, N, stream, err, errlen, phase, num_sms);
+    return causal ? launch_bwd_t<64, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, sh, stream, err, errlen, phase, num_sms)
+                  : launch_bwd_t<64, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, sh, stream, err, errlen, phase, num_sms);
+  return causal ? launch_bwd_t<128, true>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, sh, stream, err, errlen, phase, num_sms)
+                : launch_bwd_t<128, false>(Q, K, V, O, LSE, dO, dQ, dK, dV, ws, sh, stream, err, errlen, phase, num_sms);
 }
 
 }  // namespace hk

@@ -27,15 +27,17 @@
 // pipe instead of the MUFU (16 ex2/clk/SM, the co-bottleneck at d=128).
 #pragma once
 #include "ptx.cuh"
+#include "seq.cuh"
 #include "softmax.cuh"
 
 namespace hk {
 
 struct FwdParams {
-  float* lse;        // [B][Hq][N]
-  __nv_bfloat16* o;  // [B][N][Hq][D]
-  int B, Hq, Hkv, N;
-  int num_pairs;  // ceil(N / 256): Q-tile pairs per head
+  float* lse;        // dense [B][Hq][Nq]; varlen [Hq][total_q]
+  __nv_bfloat16* o;  // dense [B][Nq][Hq][D]; varlen [total_q][Hq][D]
+  SeqGeom g;         // dense / varlen geometry (seq.cuh)
+  int B, Hq, Hkv;
+  int num_pairs;  // ceil(Nq / 256): Q-tile pairs per head (varlen: of the longest sequence)
   int num_items;  // B * Hq * num_pairs work items
 };
 
@@ -62,7 +64,12 @@ struct FwdCfg {
 // r*G + c for even r, r*G + G-1-c for odd r), which pairs heavy with light
 // items across rounds and keeps the concurrently processed items on a few
 // K/V heads (L2 reuse).
+// nkv_t = key tiles Q tile t visits (0: the tile holds no query row, or none of
+// its rows sees a key); nkv = max. An item with nkv == 0 is skipped by the
+// producer and the MMA warp; the softmax warps still write O = 0, LSE = -inf
+// for any rows it holds (reading #22).
 struct FwdItem {
+  Seq sq;
   int b, h, kvh, qt0, qt1, nkv0, nkv1, nkv;
 };
 
@@ -83,14 +90,23 @@ __device__ __forceinline__ FwdItem fwd_decode(const FwdParams& p, int item) {
   it.b = rest / p.Hkv;
   it.h = it.kvh * G + hg;
   const int pair = CAUSAL ? (p.num_pairs - 1 - pr) : pr;
-  const int T = (p.N + 127) / 128;  // 128-row tiles along the sequence (last one may be ragged)
+  it.sq = seq_of(p.g, it.b);
   it.qt0 = 2 * pair;
   it.qt1 = 2 * pair + 1;
-  const bool has1 = it.qt1 < T;
-  it.nkv0 = CAUSAL ? it.qt0 + 1 : T;
-  it.nkv1 = has1 ? (CAUSAL ? it.qt1 + 1 : T) : 0;
+  it.nkv0 = kv_tiles_for<CAUSAL>(it.sq, it.qt0);
+  it.nkv1 = kv_tiles_for<CAUSAL>(it.sq, it.qt1);
   it.nkv = it.nkv1 > it.nkv0 ? it.nkv1 : it.nkv0;
   return it;
+}
+
+// First round >= r whose item has work for the producer / MMA warp, or -1.
+template <bool CAUSAL>
+__device__ __forceinline__ int fwd_next_busy(const FwdParams& p, int r, int cta, int ctas) {
+  for (;; ++r) {
+    const int item = fwd_item_index<CAUSAL>(r, cta, ctas);
+    if (item >= p.num_items) return -1;
+    if (fwd_decode<CAUSAL>(p, item).nkv > 0) return r;
+  }
 }
 
 template <int D, bool CAUSAL>
@@ -158,32 +174,36 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t ph = 0, qf_ph = 0;
       auto load_kv = [&](const FwdItem& it, int j) {
         mbar_wait(&bar_kempty[s], ph ^ 1);
+        const int row = it.sq.k0 + j * 128;
         mbar_arrive_expect_tx(&bar_kfull[s], TB);
         for (int pnl = 0; pnl < C::PANELS; ++pnl)
-          tma_load_4d(&mapK, &bar_kfull[s], sK + s * TB + pnl * 128 * 128, pnl * 64, it.kvh, j * 128, it.b, pol_kv);
+          tma_load_4d(&mapK, &bar_kfull[s], sK + s * TB + pnl * 128 * 128, pnl * 64, it.kvh, row, it.sq.tb, pol_kv);
         mbar_wait(&bar_vempty[s], ph ^ 1);
         mbar_arrive_expect_tx(&bar_vfull[s], TB);
         for (int pnl = 0; pnl < C::PANELS; ++pnl)
-          tma_load_4d(&mapV, &bar_vfull[s], sV + s * TB + pnl * 128 * 128, pnl * 64, it.kvh, j * 128, it.b, pol_kv);
+          tma_load_4d(&mapV, &bar_vfull[s], sV + s * TB + pnl * 128 * 128, pnl * 64, it.kvh, row, it.sq.tb, pol_kv);
         if (++s == NS) {
           s = 0;
           ph ^= 1;
         }
       };
-      for (int r = 0;; ++r) {
-        const int item = fwd_item_index<CAUSAL>(r, cta, ctas);
-        if (item >= p.num_items) break;
-        const FwdItem it = fwd_decode<CAUSAL>(p, item);
+      bool first = true;
+      for (int r = fwd_next_busy<CAUSAL>(p, 0, cta, ctas); r >= 0; r = fwd_next_busy<CAUSAL>(p, r + 1, cta, ctas)) {
+        const FwdItem it = fwd_decode<CAUSAL>(p, fwd_item_index<CAUSAL>(r, cta, ctas));
         load_kv(it, 0);  // K/V of the next item stream in while the previous one finishes
-        if (r > 0) {     // Q buffer is free once the previous item's last S = Q K^T completed
+        if (!first) {    // Q buffer is free once the previous item's last S = Q K^T completed
           mbar_wait(&bar_qfree, qf_ph);
           qf_ph ^= 1;
         }
-        const bool has1 = it.nkv1 > 0;
-        mbar_arrive_expect_tx(&bar_q, (has1 ? 2 : 1) * TB);
+        first = false;
+        const bool has0 = it.nkv0 > 0, has1 = it.nkv1 > 0;
+        mbar_arrive_expect_tx(&bar_q, ((has0 ? 1 : 0) + (has1 ? 1 : 0)) * TB);
         for (int pnl = 0; pnl < C::PANELS; ++pnl) {
-          tma_load_4d(&mapQ, &bar_q, sQ + pnl * 128 * 128, pnl * 64, it.h, it.qt0 * 128, it.b, pol_q);
-          if (has1) tma_load_4d(&mapQ, &bar_q, sQ + TB + pnl * 128 * 128, pnl * 64, it.h, it.qt1 * 128, it.b, pol_q);
+          if (has0)
+            tma_load_4d(&mapQ, &bar_q, sQ + pnl * 128 * 128, pnl * 64, it.h, it.sq.q0 + it.qt0 * 128, it.sq.tb, pol_q);
+          if (has1)
+            tma_load_4d(&mapQ, &bar_q, sQ + TB + pnl * 128 * 128, pnl * 64, it.h, it.sq.q0 + it.qt1 * 128, it.sq.tb,
+                        pol_q);
         }
         for (int j = 1; j < it.nkv; ++j) load_kv(it, j);
       }
@@ -208,16 +228,16 @@ __global__ void __launch_bounds__(384, 1)
 #ifdef HK_TRACE
       uint32_t tstep[2] = {0, 0};
 #endif
-      for (int r = 0;; ++r) {
-        const int item = fwd_item_index<CAUSAL>(r, cta, ctas);
-        if (item >= p.num_items) break;
-        const FwdItem it = fwd_decode<CAUSAL>(p, item);
-        const bool last_item = fwd_item_index<CAUSAL>(r + 1, cta, ctas) >= p.num_items;
+      int rn = fwd_next_busy<CAUSAL>(p, 0, cta, ctas);
+      while (rn >= 0) {
+        const FwdItem it = fwd_decode<CAUSAL>(p, fwd_item_index<CAUSAL>(rn, cta, ctas));
+        rn = fwd_next_busy<CAUSAL>(p, rn + 1, cta, ctas);
+        const bool last_item = rn < 0;
         mbar_wait(&bar_q, q_ph);
         q_ph ^= 1;
         mbar_wait(&bar_kfull[s], ph);
         tc_fence_after();
-        issue_s(0, s);
+        if (it.nkv0 > 0) issue_s(0, s);
         if (it.nkv1 > 0) issue_s(1, s);
         tc_commit_w(&bar_kempty[s]);
         if (it.nkv == 1 && !last_item) tc_commit_w(&bar_qfree);
@@ -277,7 +297,6 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_base = (warp & 3) * 32;
     const int r = (warp & 3) * 32 + lane;  // row within the Q tile == TMEM lane
     const float c = 1.4426950408889634f / sqrtf((float)D);  // (1/sqrt d) log2 e
-    const int T = (p.N + 127) / 128;
     uint32_t s_ph = 0, o_ph = 0;
     int step = 0;  // running KV-step count (trace index only)
     for (int rr = 0;; ++rr) {
@@ -285,8 +304,19 @@ __global__ void __launch_bounds__(384, 1)
       if (item >= p.num_items) break;
       const FwdItem it = fwd_decode<CAUSAL>(p, item);
       const int nk = t == 0 ? it.nkv0 : it.nkv1;
-      if (nk == 0) continue;
       const int qt = t == 0 ? it.qt0 : it.qt1;
+      const int row = qt * 128 + r;
+      const bool row_ok = row < it.sq.lq;  // rows of a ragged last tile beyond the sequence are not stored
+      if (nk == 0) {  // no row of this tile sees a key: O = 0, LSE = -inf (reading #22)
+        if (row_ok) {
+          uint4* dst = reinterpret_cast<uint4*>(p.o + ((size_t)(it.sq.gq0 + row) * p.Hq + it.h) * D);
+#pragma unroll
+          for (int q = 0; q < D / 8; ++q) dst[q] = make_uint4(0u, 0u, 0u, 0u);
+          p.lse[lse_index(p.g, it.sq, it.b, p.Hq, it.h, row)] = -INFINITY;
+        }
+        continue;
+      }
+      const int off = it.sq.lk - it.sq.lq;  // bottom-right causal alignment
       float m = -INFINITY;  // running max, log2-scaled units
       float l = 0.f;        // running row sum
       for (int j = 0; j < nk; ++j, ++step) {
@@ -295,11 +325,11 @@ __global__ void __launch_bounds__(384, 1)
         s_ph ^= 1;
         tc_fence_after();
         if (threadIdx.x % 128 == 0) hk_trace(2 + 4 * t, step, 0);  // S_t(j) ready
-        const bool diag = CAUSAL && j == qt;
-        // keys >= N (zero-filled by TMA) only need a mask when not causal: under the
-        // causal mask they already lie beyond every valid query row
-        const int kvalid = (!CAUSAL && j == T - 1) ? p.N - j * 128 : 128;
-        softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, diag, j > 0, kvalid, 40 + 4 * t, step,
+        // row r sees key column cc iff cc <= r + shift (causal) and cc < kvalid
+        const int shift = CAUSAL ? qt * 128 + off - j * 128 : (1 << 20);
+        const int kleft = it.sq.lk - j * 128;
+        const int kvalid = kleft < 128 ? kleft : 128;
+        softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, shift, j > 0, kvalid, 40 + 4 * t, step,
                                      &bar_pl[t]);
         tmem_wait_st();
         if (threadIdx.x % 128 == 0) hk_trace(43 + 4 * t, step, 0);  // P stores complete
@@ -312,10 +342,8 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&bar_o[t], o_ph);
       o_ph ^= 1;
       tc_fence_after();
-      const float inv_l = 1.f / l;
-      const int row = qt * 128 + r;
-      const bool row_ok = row < p.N;  // rows of a ragged last tile beyond N are not stored
-      __nv_bfloat16* orow = p.o + (((size_t)it.b * p.N + (row_ok ? row : 0)) * p.Hq + it.h) * D;
+      const float inv_l = l > 0.f ? 1.f / l : 0.f;  // l = 0: the row saw no key (O = 0)
+      __nv_bfloat16* orow = p.o + ((size_t)(it.sq.gq0 + (row_ok ? row : 0)) * p.Hq + it.h) * D;
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t o[32];
@@ -337,7 +365,9 @@ __global__ void __launch_bounds__(384, 1)
           for (int q = 0; q < 4; ++q) dst[q] = v[q];
         }
       }
-      if (row_ok) p.lse[((size_t)it.b * p.Hq + it.h) * p.N + row] = (m + __log2f(l)) * 0.69314718055994531f;
+      if (row_ok)
+        p.lse[lse_index(p.g, it.sq, it.b, p.Hq, it.h, row)] =
+            l > 0.f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
       if (threadIdx.x % 128 == 0) hk_trace(31 + t, rr, 0);  // epilogue of tile t done
     }
   }

@@ -90,15 +90,42 @@ hk_status launched(const char* what) {
   return HK_OK;
 }
 
-hk_status validate_common(int B, int Hq, int Hkv, int N, int d) {
-  if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0)
-    return fail(HK_ERR_INVALID_ARGUMENT, "B, Hq, Hkv, N must be positive (got %d, %d, %d, %d)", B, Hq, Hkv, N);
+// Shape of one call (dense when cu_q == nullptr; varlen: Nq, Nk are the max lengths).
+struct Shape {
+  const int* cu_q;
+  const int* cu_k;
+  int B, Hq, Hkv, Nq, Nk, total_q, total_k;
+  size_t q_rows() const { return cu_q ? (size_t)total_q : (size_t)B * Nq; }
+  size_t k_rows() const { return cu_q ? (size_t)total_k : (size_t)B * Nk; }
+};
+
+hk_status validate_common(const Shape& sh, int d) {
+  const int B = sh.B, Hq = sh.Hq, Hkv = sh.Hkv;
+  if (B <= 0 || Hq <= 0 || Hkv <= 0 || sh.Nq <= 0 || sh.Nk <= 0)
+    return fail(HK_ERR_INVALID_ARGUMENT, "B, Hq, Hkv, Nq, Nk must be positive (got %d, %d, %d, %d, %d)", B, Hq, Hkv,
+                sh.Nq, sh.Nk);
   if (Hq % Hkv != 0) return fail(HK_ERR_INVALID_ARGUMENT, "Hq (%d) must be a multiple of Hkv (%d)", Hq, Hkv);
   if (d != 64 && d != 128) return fail(HK_ERR_UNSUPPORTED, "head dim d=%d unsupported (need 64 or 128)", d);
   if (Hq > 65535 || B > 65535) return fail(HK_ERR_UNSUPPORTED, "Hq and B must be <= 65535");
-  if ((long long)B * Hq * ((N + 127) / 128) > 0x7fffffffLL)
-    return fail(HK_ERR_UNSUPPORTED, "B * Hq * ceil(N/128) must fit in int32");
+  const long long tq = (sh.Nq + 127) / 128, tk = (sh.Nk + 127) / 128;
+  if ((long long)B * Hq * tq > 0x7fffffffLL || (long long)B * Hkv * tk > 0x7fffffffLL)
+    return fail(HK_ERR_UNSUPPORTED, "B * H * ceil(N/128) must fit in int32");
+  if (sh.cu_q) {
+    if (!sh.cu_k) return fail(HK_ERR_INVALID_ARGUMENT, "cu_seqlens_k is null");
+    if (sh.total_q <= 0 || sh.total_k <= 0)
+      return fail(HK_ERR_INVALID_ARGUMENT, "total_q, total_k must be positive (got %d, %d)", sh.total_q, sh.total_k);
+    if ((reinterpret_cast<uintptr_t>(sh.cu_q) | reinterpret_cast<uintptr_t>(sh.cu_k)) & 3u)
+      return fail(HK_ERR_INVALID_ARGUMENT, "cu_seqlens must be 4-byte aligned");
+  }
+  if (sh.q_rows() * Hq > 0x7fffffffULL || sh.k_rows() * Hkv > 0x7fffffffULL)
+    return fail(HK_ERR_UNSUPPORTED, "rows * H must fit in int32");
   return HK_OK;
+}
+
+size_t ws_bytes(int B, int Hq, int Nq) {
+  if (B <= 0 || Hq <= 0 || Nq <= 0) return 0;
+  const size_t Np = ((size_t)Nq + 127) / 128 * 128;  // rows padded to whole 128-row tiles
+  return (size_t)2 * B * Hq * Np * sizeof(float) + 256;  // + the persistent kernels' work counters
 }
 
 template <int D, bool CAUSAL>
@@ -117,21 +144,21 @@ hk_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
 }  // namespace
 
 static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V, const void* O, const float* LSE,
-                          const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes, int B,
-                          int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream) {
+                          const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
+                          const Shape& sh, int d, int causal, cudaStream_t stream) {
   g_err[0] = 0;
-  hk_status s = validate_common(B, Hq, Hkv, N, d);
+  hk_status s = validate_common(sh, d);
   if (s != HK_OK) return s;
   if (!Q || !K || !V || !O || !LSE || !dO || !dQ || !dK || !dV || !workspace)
     return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
   const void* ptrs[] = {Q, K, V, O, LSE, dO, dQ, dK, dV, workspace};
   for (const void* ptr : ptrs)
     if (!aligned16(ptr)) return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
-  if (workspace_bytes < hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d))
-    return fail(HK_ERR_INVALID_ARGUMENT, "workspace too small: %zu < %zu bytes", workspace_bytes,
-                hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d));
-  const size_t q_bytes = (size_t)B * N * Hq * d * 2, kv_bytes = (size_t)B * N * Hkv * d * 2;
-  const size_t lse_bytes = (size_t)B * Hq * N * 4;
+  const size_t need = ws_bytes(sh.B, sh.Hq, sh.Nq);
+  if (workspace_bytes < need)
+    return fail(HK_ERR_INVALID_ARGUMENT, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+  const size_t q_bytes = sh.q_rows() * sh.Hq * d * 2, kv_bytes = sh.k_rows() * sh.Hkv * d * 2;
+  const size_t lse_bytes = sh.q_rows() * sh.Hq * 4;
   const void* ins[] = {Q, K, V, O, LSE, dO};
   const size_t in_sz[] = {q_bytes, kv_bytes, kv_bytes, q_bytes, lse_bytes, q_bytes};
   void* outs[] = {dQ, dK, dV, workspace};
@@ -147,8 +174,55 @@ static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V
   int num_sms = 0;
   s = check_device(&num_sms);
   if (s != HK_OK) return s;
-  return hk::launch_bwd(Q, K, V, O, LSE, dO, dQ, dK, dV, reinterpret_cast<float*>(workspace), B, Hq, Hkv, N, d,
-                        causal != 0, stream, g_err, sizeof(g_err), phase, num_sms);
+  const hk::BwdShape bs{sh.cu_q, sh.cu_k, sh.B, sh.Hq, sh.Hkv, sh.Nq, sh.Nk, sh.total_q, sh.total_k};
+  return hk::launch_bwd(Q, K, V, O, LSE, dO, dQ, dK, dV, reinterpret_cast<float*>(workspace), bs, d, causal != 0,
+                        stream, g_err, sizeof(g_err), phase, num_sms);
+}
+
+static hk_status fwd_impl(const void* Q, const void* K, const void* V, void* O, float* LSE, const Shape& sh, int d,
+                          int causal, cudaStream_t stream) {
+  g_err[0] = 0;
+  hk_status s = validate_common(sh, d);
+  if (s != HK_OK) return s;
+  if (!Q || !K || !V || !O || !LSE) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(LSE))
+    return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  const size_t q_bytes = sh.q_rows() * sh.Hq * d * 2, kv_bytes = sh.k_rows() * sh.Hkv * d * 2;
+  const size_t lse_bytes = sh.q_rows() * sh.Hq * 4;
+  if (overlaps(O, q_bytes, Q, q_bytes) || overlaps(O, q_bytes, K, kv_bytes) || overlaps(O, q_bytes, V, kv_bytes) ||
+      overlaps(LSE, lse_bytes, O, q_bytes) || overlaps(LSE, lse_bytes, Q, q_bytes) ||
+      overlaps(LSE, lse_bytes, K, kv_bytes) || overlaps(LSE, lse_bytes, V, kv_bytes))
+    return fail(HK_ERR_INVALID_ARGUMENT, "outputs O/LSE must not alias inputs or each other");
+  int num_sms = 0;
+  s = check_device(&num_sms);
+  if (s != HK_OK) return s;
+
+  const bool varlen = sh.cu_q != nullptr;
+  const int mb = varlen ? 1 : sh.B, mnq = varlen ? sh.total_q : sh.Nq, mnk = varlen ? sh.total_k : sh.Nk;
+  CUtensorMap mq, mk, mv;
+  if (!hk::encode_bnhd(&mq, Q, mb, mnq, sh.Hq, d, 128) || !hk::encode_bnhd(&mk, K, mb, mnk, sh.Hkv, d, 128) ||
+      !hk::encode_bnhd(&mv, V, mb, mnk, sh.Hkv, d, 128))
+    return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (CUresult %d)", hk::last_encode_result());
+  hk::FwdParams p;
+  p.lse = LSE;
+  p.o = reinterpret_cast<__nv_bfloat16*>(O);
+  p.g = hk::SeqGeom{sh.cu_q, sh.cu_k, sh.Nq, sh.Nk, sh.total_q};
+  p.B = sh.B;
+  p.Hq = sh.Hq;
+  p.Hkv = sh.Hkv;
+  p.num_pairs = ((sh.Nq + 127) / 128 + 1) / 2;
+  p.num_items = sh.B * sh.Hq * p.num_pairs;
+  if (d == 64)
+    return causal ? launch_fwd<64, true>(mq, mk, mv, p, num_sms, stream)
+                  : launch_fwd<64, false>(mq, mk, mv, p, num_sms, stream);
+  return causal ? launch_fwd<128, true>(mq, mk, mv, p, num_sms, stream)
+                : launch_fwd<128, false>(mq, mk, mv, p, num_sms, stream);
+}
+
+static Shape dense(int B, int Hq, int Hkv, int Nq, int Nk) { return Shape{nullptr, nullptr, B, Hq, Hkv, Nq, Nk, 0, 0}; }
+static Shape packed(const int* cu_q, const int* cu_k, int B, int Hq, int Hkv, int total_q, int total_k, int max_q,
+                    int max_k) {
+  return Shape{cu_q, cu_k, B, Hq, Hkv, max_q, max_k, total_q, total_k};
 }
 
 extern "C" {
@@ -166,67 +240,81 @@ const char* hk_status_string(hk_status s) {
   return "HK_ERR_UNKNOWN";
 }
 
-int hk_attn_abi_version(void) { return 1; }
+int hk_attn_abi_version(void) { return 2; }  // 2: + Nq != Nk and varlen entry points
 
 hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, float* LSE, int B, int Hq, int Hkv,
                       int N, int d, int causal, cudaStream_t stream) {
-  g_err[0] = 0;
-  hk_status s = validate_common(B, Hq, Hkv, N, d);
-  if (s != HK_OK) return s;
-  if (!Q || !K || !V || !O || !LSE) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
-  if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(LSE))
-    return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
-  const size_t q_bytes = (size_t)B * N * Hq * d * 2, kv_bytes = (size_t)B * N * Hkv * d * 2;
-  const size_t lse_bytes = (size_t)B * Hq * N * 4;
-  if (overlaps(O, q_bytes, Q, q_bytes) || overlaps(O, q_bytes, K, kv_bytes) || overlaps(O, q_bytes, V, kv_bytes) ||
-      overlaps(LSE, lse_bytes, O, q_bytes) || overlaps(LSE, lse_bytes, Q, q_bytes) ||
-      overlaps(LSE, lse_bytes, K, kv_bytes) || overlaps(LSE, lse_bytes, V, kv_bytes))
-    return fail(HK_ERR_INVALID_ARGUMENT, "outputs O/LSE must not alias inputs or each other");
-  int num_sms = 0;
-  s = check_device(&num_sms);
-  if (s != HK_OK) return s;
-
-  CUtensorMap mq, mk, mv;
-  if (!hk::encode_bnhd(&mq, Q, B, N, Hq, d, 128) || !hk::encode_bnhd(&mk, K, B, N, Hkv, d, 128) ||
-      !hk::encode_bnhd(&mv, V, B, N, Hkv, d, 128))
-    return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (CUresult %d)", hk::last_encode_result());
-  hk::FwdParams p;
-  p.lse = LSE;
-  p.o = reinterpret_cast<__nv_bfloat16*>(O);
-  p.B = B;
-  p.Hq = Hq;
-  p.Hkv = Hkv;
-  p.N = N;
-  p.num_pairs = ((N + 127) / 128 + 1) / 2;
-  p.num_items = B * Hq * p.num_pairs;
-  if (d == 64)
-    return causal ? launch_fwd<64, true>(mq, mk, mv, p, num_sms, stream)
-                  : launch_fwd<64, false>(mq, mk, mv, p, num_sms, stream);
-  return causal ? launch_fwd<128, true>(mq, mk, mv, p, num_sms, stream)
-                : launch_fwd<128, false>(mq, mk, mv, p, num_sms, stream);
+  if (N <= 0) {
+    g_err[0] = 0;
+    return fail(HK_ERR_INVALID_ARGUMENT, "N must be positive (got %d)", N);
+  }
+  return fwd_impl(Q, K, V, O, LSE, dense(B, Hq, Hkv, N, N), d, causal, stream);
 }
-
 size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d) {
   (void)Hkv;
   (void)d;
-  if (B <= 0 || Hq <= 0 || N <= 0) return 0;
-  const size_t Np = ((size_t)N + 127) / 128 * 128;  // rows padded to whole 128-row tiles
-  return (size_t)2 * B * Hq * Np * sizeof(float) + 256;  // + the persistent kernels' work counters
+  return ws_bytes(B, Hq, N);
 }
-
 hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,
                       void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes, int B, int Hq, int Hkv,
                       int N, int d, int causal, cudaStream_t stream) {
-  return bwd_impl(-1, Q, K, V, O, LSE, dO, dQ, dK, dV, workspace, workspace_bytes, B, Hq, Hkv, N, d, causal, stream);
+  return bwd_impl(-1, Q, K, V, O, LSE, dO, dQ, dK, dV, workspace, workspace_bytes, dense(B, Hq, Hkv, N, N), d, causal,
+                  stream);
 }
-
+hk_status hk_attn_fwd_qk(const void* Q, const void* K, const void* V, void* O, float* LSE, int B, int Hq, int Hkv,
+                         int Nq, int Nk, int d, int causal, cudaStream_t stream) {
+  return fwd_impl(Q, K, V, O, LSE, dense(B, Hq, Hkv, Nq, Nk), d, causal, stream);
+}
+size_t hk_attn_bwd_qk_workspace_bytes(int B, int Hq, int Hkv, int Nq, int Nk, int d) {
+  (void)Hkv;
+  (void)Nk;
+  (void)d;
+  return ws_bytes(B, Hq, Nq);
+}
+hk_status hk_attn_bwd_qk(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                         const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes, int B,
+                         int Hq, int Hkv, int Nq, int Nk, int d, int causal, cudaStream_t stream) {
+  return bwd_impl(-1, Q, K, V, O, LSE, dO, dQ, dK, dV, workspace, workspace_bytes, dense(B, Hq, Hkv, Nq, Nk), d,
+                  causal, stream);
+}
+hk_status hk_attn_fwd_varlen(const void* Q, const void* K, const void* V, void* O, float* LSE,
+                             const int* cu_seqlens_q, const int* cu_seqlens_k, int B, int Hq, int Hkv, int total_q,
+                             int total_k, int max_seqlen_q, int max_seqlen_k, int d, int causal,
+                             cudaStream_t stream) {
+  if (!cu_seqlens_q || !cu_seqlens_k) {
+    g_err[0] = 0;
+    return fail(HK_ERR_INVALID_ARGUMENT, "null cu_seqlens");
+  }
+  return fwd_impl(Q, K, V, O, LSE,
+                  packed(cu_seqlens_q, cu_seqlens_k, B, Hq, Hkv, total_q, total_k, max_seqlen_q, max_seqlen_k), d,
+                  causal, stream);
+}
+size_t hk_attn_bwd_varlen_workspace_bytes(int B, int Hq, int Hkv, int max_seqlen_q, int max_seqlen_k, int d) {
+  (void)Hkv;
+  (void)max_seqlen_k;
+  (void)d;
+  return ws_bytes(B, Hq, max_seqlen_q);
+}
+hk_status hk_attn_bwd_varlen(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                             const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
+                             const int* cu_seqlens_q, const int* cu_seqlens_k, int B, int Hq, int Hkv, int total_q,
+                             int total_k, int max_seqlen_q, int max_seqlen_k, int d, int causal,
+                             cudaStream_t stream) {
+  if (!cu_seqlens_q || !cu_seqlens_k) {
+    g_err[0] = 0;
+    return fail(HK_ERR_INVALID_ARGUMENT, "null cu_seqlens");
+  }
+  return bwd_impl(-1, Q, K, V, O, LSE, dO, dQ, dK, dV, workspace, workspace_bytes,
+                  packed(cu_seqlens_q, cu_seqlens_k, B, Hq, Hkv, total_q, total_k, max_seqlen_q, max_seqlen_k), d,
+                  causal, stream);
+}
 hk_status hk_diag_bwd_phase(int phase, const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                             const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
                             int B, int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream) {
   g_err[0] = 0;
   if (phase < 0 || phase > 2) return fail(HK_ERR_INVALID_ARGUMENT, "phase must be 0, 1 or 2");
-  return bwd_impl(phase, Q, K, V, O, LSE, dO, dQ, dK, dV, workspace, workspace_bytes, B, Hq, Hkv, N, d, causal,
-                  stream);
+  return bwd_impl(phase, Q, K, V, O, LSE, dO, dQ, dK, dV, workspace, workspace_bytes, dense(B, Hq, Hkv, N, N), d,
+                  causal, stream);
 }
 
 hk_status hk_diag_umma(const void* A, const void* Bm, float* D, int N, int K, int a_tmem, int b_mn,

@@ -167,7 +167,7 @@ __global__ void softmax_rate_kernel(int iters, float* out_cycles, float* sink) {
   const long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
     float m = -INFINITY;
-    softmax_step<128, EMU_OF_8>(tS, tO, lane_base, r, c, m, l, false, false);
+    softmax_step<128, EMU_OF_8>(tS, tO, lane_base, r, c, m, l, 1 << 20, false);
     msum += m;
   }
   tmem_wait_st();

@@ -46,13 +46,16 @@ __device__ __forceinline__ void softmax_chunk32(const float* s, float c, float m
 
 // tS: this tile's score columns (fp32 S in, bf16 P out over its first 64
 // columns); tO: its O accumulator (rescaled in place when the max moves).
-// m, l: running max (log2 units, always integral) and row sum. `diag`: causal
-// diagonal tile (mask key > query); `kvalid` < 128: only the first kvalid keys
-// of this block exist (ragged N). Masked blocks run all exps on the MUFU so a
-// masked P is exactly 0. `o_live`: O already holds earlier P V products.
+// m, l: running max (log2 units, always integral) and row sum. `shift`: causal
+// limit — key column cc is visible to row r iff cc <= r + shift (a large value
+// = no causal limit; 0 on the square diagonal tile); `kvalid` < 128: only the
+// first kvalid keys of this block exist (ragged / varlen tail). Masked blocks
+// run all exps on the MUFU so a masked P is exactly 0; a row that has seen no
+// key so far keeps m = -inf and l = 0 (reading #22). `o_live`: O already
+// holds earlier P V products.
 template <int D, int EMU_OF_8>
 __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t lane_base, int r, float c,
-                                             float& m, float& l, bool diag, bool o_live, int kvalid = 128,
+                                             float& m, float& l, int shift, bool o_live, int kvalid = 128,
                                              int trace_ev = -1, uint32_t trace_idx = 0, uint64_t* bar_lo = nullptr) {
 #ifdef HK_TRACE
   const bool tr = trace_ev >= 0 && (threadIdx.x % 128) == 0;
@@ -67,9 +70,9 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
     tmem_ld32(tmem_addr(tS, lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(&s[c0]));
   tmem_wait_ld();
   HK_SM_TRACE(0)  // S in registers
-  const bool masked = diag || kvalid < 128;
+  const bool masked = shift < 127 || kvalid < 128;
   if (masked) {
-    const int lim = diag ? (r + 1 < kvalid ? r + 1 : kvalid) : kvalid;  // keys [0, lim) visible
+    const int lim = r + 1 + shift < kvalid ? r + 1 + shift : kvalid;  // keys [0, lim) visible (lim may be <= 0)
 #pragma unroll
     for (int cc = 0; cc < 128; ++cc)
       if (cc >= lim) s[cc] = -INFINITY;
@@ -114,8 +117,8 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
 #pragma unroll
   for (int c0 = 0; c0 < 128; c0 += 32) {
     uint32_t pk[16];
-    if (masked)
-      softmax_chunk32<false, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);
+    if (masked)  // a row with no visible key yet (m_use = -inf) gets P = 2^-inf = 0, not NaN
+      softmax_chunk32<false, EMU_OF_8>(s + c0, c, m_use == -INFINITY ? 0.f : m_use, smin, pk, acc);
     else
       softmax_chunk32<true, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);
     tmem_st16(tmem_addr(tS, lane_base, c0 / 2), pk);

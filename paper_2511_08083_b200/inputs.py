@@ -102,3 +102,33 @@ def make_ln_inputs(rows: int, D: int, seed: int = 0, device="cpu"):
 def make_rope_inputs(B: int, N: int, H: int, d: int, seed: int = 0, device="cpu"):
     """x [B, N, H, d] bf16 N(0,1) (the Q or K tensor a rotary step transforms)."""
     return {"x": _block((B, N, H, d), splitmix64(seed, 31), device, 1.0)}
+
+
+def make_qk_inputs(B: int, Nq: int, Nk: int, Hq: int, Hkv: int, d: int, seed: int = 0, device="cpu",
+                   std: float = 1.0):
+    """Nq != Nk (NEXT #4): Q, dO [B, Nq, Hq, d] and K, V [B, Nk, Hkv, d] bf16, N(0, std^2);
+    each tensor has its own splitmix64 stream."""
+    return {"Q": _block((B, Nq, Hq, d), splitmix64(seed, 41), device, std),
+            "K": _block((B, Nk, Hkv, d), splitmix64(seed, 42), device, std),
+            "V": _block((B, Nk, Hkv, d), splitmix64(seed, 43), device, std),
+            "dO": _block((B, Nq, Hq, d), splitmix64(seed, 44), device, 1.0)}
+
+
+def varlen_lengths(B: int, mean: int, seed: int = 0, lo: int = 1):
+    """A length mix for packed batches: B lengths uniform in [lo, 2*mean - lo]
+    (the document-length spread of a packed pre-training batch)."""
+    g = torch.Generator().manual_seed(splitmix64(seed, 51))
+    return [int(x) for x in torch.randint(lo, max(lo + 1, 2 * mean - lo + 1), (B,), generator=g)]
+
+
+def make_varlen_inputs(lens_q, lens_k, Hq: int, Hkv: int, d: int, seed: int = 0, device="cpu", std: float = 1.0):
+    """Packed variable-length batch: Q, dO [sum(lens_q), Hq, d], K, V [sum(lens_k), Hkv, d]
+    bf16 N(0, std^2), and int32 offsets cu_q, cu_k [B+1] (cu[0] = 0, running sums)."""
+    tq, tk = int(sum(lens_q)), int(sum(lens_k))
+    cu_q = torch.tensor([0] + list(torch.tensor(list(lens_q)).cumsum(0).tolist()), dtype=torch.int32, device=device)
+    cu_k = torch.tensor([0] + list(torch.tensor(list(lens_k)).cumsum(0).tolist()), dtype=torch.int32, device=device)
+    return {"Q": _block((tq, Hq, d), splitmix64(seed, 61), device, std),
+            "K": _block((tk, Hkv, d), splitmix64(seed, 62), device, std),
+            "V": _block((tk, Hkv, d), splitmix64(seed, 63), device, std),
+            "dO": _block((tq, Hq, d), splitmix64(seed, 64), device, 1.0),
+            "cu_q": cu_q, "cu_k": cu_k}

@@ -16,10 +16,22 @@ def test_rejects_cpu_and_bad_dtype_and_layout():
     with pytest.raises(ValueError):
         api._check_tensor("q", t(2, 2, dtype=torch.float32))
     with pytest.raises(ValueError):
-        api._shapes(t(1, 128, 2, 64), t(1, 64, 2, 64), t(1, 64, 2, 64))
+        api._shapes(t(1, 128, 2, 64), t(1, 64, 2, 64), t(1, 32, 2, 64))  # k, v differ
     with pytest.raises(ValueError):
         api._shapes(t(1, 128, 2, 64), t(1, 128, 2, 32), t(1, 128, 2, 32))
-    assert api._shapes(t(2, 256, 8, 128), t(2, 256, 2, 128), t(2, 256, 2, 128)) == (2, 256, 8, 2, 128)
+    with pytest.raises(ValueError):
+        api._shapes(t(1, 128, 2, 64), t(2, 128, 2, 64), t(2, 128, 2, 64))
+    assert api._shapes(t(2, 256, 8, 128), t(2, 256, 2, 128), t(2, 256, 2, 128)) == (2, 256, 256, 8, 2, 128)
+    assert api._shapes(t(2, 100, 8, 64), t(2, 300, 2, 64), t(2, 300, 2, 64)) == (2, 100, 300, 8, 2, 64)
+
+
+def test_varlen_binding_validation():
+    q, k = t(10, 4, 64), t(12, 2, 64)
+    cu = torch.tensor([0, 4, 10], dtype=torch.int32)
+    with pytest.raises(ValueError, match="CUDA"):
+        api.attn_fwd_varlen(q, k, k, cu, cu, 6, 8)
+    with pytest.raises(ValueError):
+        api._check_tensor("cu", cu.to(torch.int64), torch.int32)
 
 
 def test_library_missing_is_loud(monkeypatch, tmp_path):
