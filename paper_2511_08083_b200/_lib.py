@@ -31,6 +31,8 @@ SIGNATURES = {
     "hk_attn_bwd_varlen_workspace_bytes": (_Z, [_I, _I, _I, _I, _I, _I]),
     "hk_attn_bwd_varlen": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P, _P, _I, _I, _I, _I, _I, _I, _I,
                                 _I, _I, _P]),
+    "hk_attn_merge": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P]),
+    "hk_accum_bf16": (_I, [_P, _P, _P, _Z, _I, _P]),
     "hk_attn_last_error": (ctypes.c_char_p, []),
     "hk_status_string": (ctypes.c_char_p, [_I]),
     "hk_attn_abi_version": (_I, []),

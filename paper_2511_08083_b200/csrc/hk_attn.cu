@@ -21,11 +21,13 @@
 #include "../../include/hk_attn_diag.h"
 #include "../../include/hk_gemm.h"
 #include "../../include/hk_membound.h"
+#include "../../include/hk_ring.h"
 #pragma GCC visibility pop
 #include "bwd.cuh"
 #include "fwd.cuh"
 #include "gemm.cuh"
 #include "membound.cuh"
+#include "ring.cuh"
 #include "tma_host.h"
 #include "rates_diag.cuh"
 #include "umma_diag.cuh"
@@ -552,6 +554,51 @@ hk_status hk_rope(const void* x, const float* cos, const float* sin, void* out, 
   return launched("hk_rope");
 }
 
+hk_status hk_attn_merge(float* O_acc, float* LSE_acc, const void* O_part, const float* LSE_part, void* O_out, int B,
+                        int N, int H, int d, int init, cudaStream_t stream) {
+  g_err[0] = 0;
+  if (B <= 0 || N <= 0 || H <= 0) return fail(HK_ERR_INVALID_ARGUMENT, "B, N, H must be positive");
+  if (!O_acc || !LSE_acc || !O_part || !LSE_part) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (!aligned16(O_acc) || !aligned16(O_part) || (O_out && !aligned16(O_out)) ||
+      (reinterpret_cast<uintptr_t>(LSE_acc) & 3u) || (reinterpret_cast<uintptr_t>(LSE_part) & 3u))
+    return fail(HK_ERR_INVALID_ARGUMENT, "O pointers must be 16-byte aligned, LSE pointers 4-byte aligned");
+  if (d < 8 || d > 256 || (d & (d - 1))) return fail(HK_ERR_UNSUPPORTED, "d must be a power of two in [8, 256]");
+  const size_t rows = (size_t)B * N * H;
+  const size_t ob = rows * d * 2, ab = rows * d * 4, lb = rows * 4;
+  if (overlaps(O_acc, ab, O_part, ob) || overlaps(O_acc, ab, LSE_part, lb) || overlaps(LSE_acc, lb, O_part, ob) ||
+      overlaps(LSE_acc, lb, LSE_part, lb) || overlaps(O_acc, ab, LSE_acc, lb) ||
+      (O_out && (overlaps(O_out, ob, O_acc, ab) || overlaps(O_out, ob, LSE_acc, lb) || overlaps(O_out, ob, O_part, ob))))
+    return fail(HK_ERR_INVALID_ARGUMENT, "buffers must not overlap");
+  int num_sms = 0;
+  hk_status s = check_device(&num_sms);
+  if (s != HK_OK) return s;
+  hk::MergeParams q{O_acc, LSE_acc, reinterpret_cast<const __nv_bfloat16*>(O_part), LSE_part,
+                    reinterpret_cast<__nv_bfloat16*>(O_out), B, N, H, d, init != 0};
+  const size_t warps = (rows + (32 / (d / 8)) - 1) / (32 / (d / 8));
+  size_t blocks = (warps + 7) / 8;
+  if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
+  hk::attn_merge_kernel<<<(unsigned)blocks, 256, 0, stream>>>(q);
+  return launched("hk_attn_merge");
+}
+hk_status hk_accum_bf16(float* acc, const void* x, void* out, size_t n, int init, cudaStream_t stream) {
+  g_err[0] = 0;
+  if (n == 0 || n % 8) return fail(HK_ERR_INVALID_ARGUMENT, "n must be a positive multiple of 8");
+  if (!x || (!acc && !(out && init))) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if ((acc && !aligned16(acc)) || !aligned16(x) || (out && !aligned16(out)))
+    return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  if ((acc && overlaps(acc, n * 4, x, n * 2)) || (out && (overlaps(out, n * 2, x, n * 2) ||
+                                                          (acc && overlaps(out, n * 2, acc, n * 4)))))
+    return fail(HK_ERR_INVALID_ARGUMENT, "buffers must not overlap");
+  int num_sms = 0;
+  hk_status s = check_device(&num_sms);
+  if (s != HK_OK) return s;
+  const size_t n8 = n / 8;
+  size_t blocks = (n8 + 255) / 256;
+  if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
+  hk::accum_bf16_kernel<<<(unsigned)blocks, 256, 0, stream>>>(acc, reinterpret_cast<const __nv_bfloat16*>(x),
+                                                               reinterpret_cast<__nv_bfloat16*>(out), n8, init != 0);
+  return launched("hk_accum_bf16");
+}
 hk_status hk_diag_trace_read(void* dst, size_t bytes, int reset) {
   g_err[0] = 0;
 #ifdef HK_TRACE
