@@ -1,5 +1,6 @@
 """fp64 CPU oracles for fused attention forward/backward, the BF16 GEMM and the
-memory-bound dropout-residual-LayerNorm and rotary kernels (HipKittens, arXiv 2511.08083).
+memory-bound dropout-residual-LayerNorm and rotary kernels and the ring-attention LSE
+merge (HipKittens, arXiv 2511.08083).
 
 TEST INFRASTRUCTURE ONLY. Only `tests/`, `__graft_entry__.smoke()` and the
 `cpu_baseline` / `--impl reference` legs of `bench.py` may import this package.
@@ -23,3 +24,4 @@ from .attention import (  # noqa: F401
 )
 from .gemm import gemm_abt, gemm_abt_rows, gemm_loops  # noqa: F401,E402
 from .membound import dropout_keep, layernorm_dropout_residual, rope, rope_tables  # noqa: F401,E402
+from .ring import attn_merge  # noqa: F401,E402
