@@ -33,7 +33,8 @@ hk_status hk_attn_merge(float* O_acc, float* LSE_acc, const void* O_part, const 
 
 /* Gradient accumulation over ring steps, n bf16 elements x (n % 8 == 0):
  *   out == NULL:  acc = (init ? 0 : acc) + x          (fp32)
- *   out != NULL:  out = bf16((init ? 0 : acc) + x)     (the last step; acc not written) */
+ *   out != NULL:  out = bf16((init ? 0 : acc) + x)     (the last step; acc not written)
+ * x may be NULL (treated as 0) when out != NULL and init == 0: out = bf16(acc). */
 hk_status hk_accum_bf16(float* acc, const void* x, void* out, size_t n, int init, cudaStream_t stream);
 
 #ifdef __cplusplus

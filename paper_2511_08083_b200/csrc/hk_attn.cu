@@ -583,11 +583,12 @@ hk_status hk_attn_merge(float* O_acc, float* LSE_acc, const void* O_part, const 
 hk_status hk_accum_bf16(float* acc, const void* x, void* out, size_t n, int init, cudaStream_t stream) {
   g_err[0] = 0;
   if (n == 0 || n % 8) return fail(HK_ERR_INVALID_ARGUMENT, "n must be a positive multiple of 8");
-  if (!x || (!acc && !(out && init))) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
-  if ((acc && !aligned16(acc)) || !aligned16(x) || (out && !aligned16(out)))
+  if (!x && !(out && acc && !init)) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (!acc && !(out && init)) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if ((acc && !aligned16(acc)) || (x && !aligned16(x)) || (out && !aligned16(out)))
     return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
-  if ((acc && overlaps(acc, n * 4, x, n * 2)) || (out && (overlaps(out, n * 2, x, n * 2) ||
-                                                          (acc && overlaps(out, n * 2, acc, n * 4)))))
+  if ((acc && x && overlaps(acc, n * 4, x, n * 2)) ||
+      (out && ((x && overlaps(out, n * 2, x, n * 2)) || (acc && overlaps(out, n * 2, acc, n * 4)))))
     return fail(HK_ERR_INVALID_ARGUMENT, "buffers must not overlap");
   int num_sms = 0;
   hk_status s = check_device(&num_sms);

@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(256) attn_merge_kernel(const MergeParams p) {
 __global__ void __launch_bounds__(256) accum_bf16_kernel(float* __restrict__ acc, const __nv_bfloat16* __restrict__ x,
                                                          __nv_bfloat16* __restrict__ out, size_t n8, int init) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x) {
-    float v[8];
-    unpack8(reinterpret_cast<const uint4*>(x)[i], v);
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (x) unpack8(reinterpret_cast<const uint4*>(x)[i], v);  // x == nullptr: cast acc to bf16
     if (!init) {
       const float4 a0 = reinterpret_cast<const float4*>(acc)[2 * i], a1 = reinterpret_cast<const float4*>(acc)[2 * i + 1];
       v[0] += a0.x; v[1] += a0.y; v[2] += a0.z; v[3] += a0.w;

@@ -1,0 +1,99 @@
+"""GPU parity of context-parallel ring attention (NEXT #4) through the C ABI:
+the LSE merge kernel (hk_attn_merge) and the gradient accumulator (hk_accum_bf16)
+against the fp64 oracle, and the whole ring forward + backward — P virtual ranks
+driven by one process on one GPU (LoopbackRing: the same schedule and kernels as
+DistRing, the exchange is a list rotation) — against the oracle's attention over
+the whole sequence, at the BASELINE tolerances."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from util import TOL_MAXABS, TOL_RELL2, np64, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def test_merge_kernel_matches_oracle():
+    from paper_2511_08083_b200 import _lib, api
+    from paper_2511_08083_b200.inputs import make_qk_inputs
+    B, Nq, Nk, Hq, Hkv, d = 2, 300, 700, 4, 2, 128
+    x = make_qk_inputs(B, Nq, Nk, Hq, Hkv, d, seed=1, device="cuda")
+    split = 333
+    o1, l1 = api.attn_fwd(x["Q"], x["K"][:, :split].contiguous(), x["V"][:, :split].contiguous(), False)
+    o2, l2 = api.attn_fwd(x["Q"], x["K"][:, split:].contiguous(), x["V"][:, split:].contiguous(), False)
+    # a third partial that saw no key at all (LSE = -inf) must leave the result unchanged
+    o3 = torch.zeros_like(o1)
+    l3 = torch.full_like(l1, float("-inf"))
+    acc = torch.empty(o1.shape, dtype=torch.float32, device="cuda")
+    lacc = torch.empty_like(l1)
+    out = torch.empty_like(o1)
+    L = _lib.lib()
+    for i, (o, lse) in enumerate(((o1, l1), (o3, l3), (o2, l2))):
+        _lib.check(L.hk_attn_merge(api._ptr(acc), api._ptr(lacc), api._ptr(o), api._ptr(lse),
+                                   api._ptr(out) if i == 2 else None, B, Nq, Hq, d, int(i == 0), api._stream()))
+    torch.cuda.synchronize()
+    ref_o, ref_l = oracle.attn_merge(*oracle.attn_merge(np64(o1), np64(l1), np64(o3), np64(l3)), np64(o2), np64(l2))
+    assert np.abs(np64(acc) - ref_o).max() < 1e-5
+    assert np.abs(np64(lacc) - ref_l).max() < 1e-5
+    assert torch.equal(out, acc.to(torch.bfloat16))
+    # and the merged result is the attention over all keys
+    full = oracle.attn_fwd(np64(x["Q"]), np64(x["K"]), np64(x["V"]), False)
+    assert np.abs(np64(out) - full[0]).max() <= TOL_MAXABS
+    assert np.abs(np64(lacc) - full[1]).max() <= TOL_MAXABS
+
+
+def test_accum_kernel():
+    from paper_2511_08083_b200 import _lib, api
+    L = _lib.lib()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    xs = [torch.randn(4096, generator=g, device="cuda").to(torch.bfloat16) for _ in range(3)]
+    acc = torch.empty(4096, dtype=torch.float32, device="cuda")
+    out = torch.empty(4096, dtype=torch.bfloat16, device="cuda")
+    for i, x in enumerate(xs[:2]):
+        _lib.check(L.hk_accum_bf16(api._ptr(acc), api._ptr(x), None, ctypes.c_size_t(4096), int(i == 0),
+                                   api._stream()))
+    _lib.check(L.hk_accum_bf16(api._ptr(acc), api._ptr(xs[2]), api._ptr(out), ctypes.c_size_t(4096), 0,
+                               api._stream()))
+    torch.cuda.synchronize()
+    want = xs[0].double() + xs[1].double()
+    assert torch.equal(acc, (xs[0].float() + xs[1].float()))
+    assert torch.allclose(out.double(), want + xs[2].double(), rtol=2 ** -8, atol=1e-6)
+    _lib.check(L.hk_accum_bf16(api._ptr(acc), None, api._ptr(out), ctypes.c_size_t(4096), 0, api._stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(out, acc.to(torch.bfloat16))
+
+
+CASES = [
+    # P, B, N, Hq, Hkv, d
+    (2, 1, 1024, 4, 2, 128),
+    (4, 2, 2048, 4, 1, 64),
+    (3, 1, 1536, 8, 2, 128),   # c = 256
+    (2, 2, 640, 2, 2, 64),     # c = 160: ragged 128-row tiles inside every chunk
+]
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("case", CASES)
+def test_ring_loopback_matches_whole_sequence(case, causal):
+    from paper_2511_08083_b200 import ring
+    from paper_2511_08083_b200.inputs import make_inputs
+    P, B, N, Hq, Hkv, d = case
+    x = make_inputs(B, N, Hq, Hkv, d, seed=7, device="cuda")
+    sh = {n: [ring.zigzag_shard(x[n], P, r) for r in range(P)] for n in ("Q", "K", "V", "dO")}
+    comm = ring.LoopbackRing(P)
+    fw = ring.ring_attn_fwd(sh["Q"], sh["K"], sh["V"], causal, comm)
+    o = [f[0] for f in fw]
+    lse = [f[1] for f in fw]
+    bw = ring.ring_attn_bwd(sh["Q"], sh["K"], sh["V"], o, lse, sh["dO"], causal, comm)
+    torch.cuda.synchronize()
+    O = ring.zigzag_unshard(o)
+    LSE = ring.zigzag_unshard([(a.transpose(1, 2), b.transpose(1, 2)) for a, b in lse]).transpose(1, 2)
+    dQ, dK, dV = (ring.zigzag_unshard([b[i] for b in bw]) for i in range(3))
+    ref = oracle.attn_fwd_bwd(np64(x["Q"]), np64(x["K"]), np64(x["V"]), np64(x["dO"]), causal)
+    assert np.abs(np64(O) - ref["O"]).max() <= TOL_MAXABS
+    assert np.abs(np64(LSE) - ref["LSE"]).max() <= TOL_MAXABS
+    for n, t in (("dQ", dQ), ("dK", dK), ("dV", dV)):
+        assert rel_l2(np64(t), ref[n]) <= TOL_RELL2, n
