@@ -97,3 +97,53 @@ def test_ring_loopback_matches_whole_sequence(case, causal):
     assert np.abs(np64(LSE) - ref["LSE"]).max() <= TOL_MAXABS
     for n, t in (("dQ", dQ), ("dK", dK), ("dV", dV)):
         assert rel_l2(np64(t), ref[n]) <= TOL_RELL2, n
+
+
+def _dist_worker(rank, world, port, causal, out):
+    import os
+    import torch.distributed as dist
+    from paper_2511_08083_b200 import ring
+    from paper_2511_08083_b200.inputs import make_inputs
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    B, N, Hq, Hkv, d = 1, 1024, 4, 2, 128
+    x = make_inputs(B, N, Hq, Hkv, d, seed=11, device="cuda")
+    sh = {n: ring.zigzag_shard(x[n], world, rank) for n in ("Q", "K", "V", "dO")}
+    comm = ring.DistRing()
+    (o, lse), = ring.ring_attn_fwd([sh["Q"]], [sh["K"]], [sh["V"]], causal, comm)
+    (dq, dk, dv), = ring.ring_attn_bwd([sh["Q"]], [sh["K"]], [sh["V"]], [o], [lse], [sh["dO"]], causal, comm)
+    torch.cuda.synchronize()
+    loop = ring.LoopbackRing(world)
+    shl = {n: [ring.zigzag_shard(x[n], world, r) for r in range(world)] for n in ("Q", "K", "V", "dO")}
+    fw = ring.ring_attn_fwd(shl["Q"], shl["K"], shl["V"], causal, loop)
+    bw = ring.ring_attn_bwd(shl["Q"], shl["K"], shl["V"], [f[0] for f in fw], [f[1] for f in fw], shl["dO"],
+                            causal, loop)
+    torch.cuda.synchronize()
+    same = all(torch.equal(a, b) for a, b in zip(o + dq + dk + dv, fw[rank][0] + bw[rank][0] + bw[rank][1] +
+                                                 bw[rank][2]))
+    out.put((rank, bool(same)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_ring_two_processes_equal_loopback(causal):
+    """Two processes (ranks) sharing the GPU, exchanging over gloo through DistRing,
+    produce bitwise the loopback results (same kernels, same order of merges)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, causal, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert res[0] and res[1], res
