@@ -44,6 +44,12 @@ struct FwdParams {
 template <int D>
 struct FwdCfg {
   static constexpr int PANELS = D / 64;
+  // d=64: TMEM has room for P next to S (S0 S1 O0 O1 P0 P1 = 128+128+64+64+64+64), so S can be
+  // released as soon as it is read and the next Q K^T overlaps the softmax (split P).
+#ifndef HK_FWD_SPLIT64
+#define HK_FWD_SPLIT64 0  // measured slower (DESIGN.md §8 "did not pay"): off
+#endif
+  static constexpr bool SPLIT_P = (D == 64) && HK_FWD_SPLIT64;
   static constexpr uint32_t TILE_BYTES = 128 * D * 2;  // one 128-row tile
   static constexpr int NS = (D == 128) ? 2 : 4;        // K/V ring depth
   static constexpr uint32_t SMEM = 2 * TILE_BYTES + 2 * NS * TILE_BYTES + 1024;
@@ -124,7 +130,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sV = sK + NS * TB;   // NS tiles
 
   __shared__ uint64_t bar_q, bar_qfree, bar_kfull[NS], bar_kempty[NS], bar_vfull[NS], bar_vempty[NS];
-  __shared__ uint64_t bar_s[2], bar_p[2], bar_pl[2], bar_o[2], bar_oempty[2];
+  __shared__ uint64_t bar_s[2], bar_p[2], bar_pl[2], bar_o[2], bar_oempty[2], bar_sfree[2], bar_pv[2];
   __shared__ uint32_t tmem_base_s;
 
   const int warp = warp_id();
@@ -147,6 +153,8 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&bar_pl[t], 4);  // first half of P_t (keys [0, 64)) published
       mbar_init(&bar_o[t], 1);
       mbar_init(&bar_oempty[t], 4);
+      mbar_init(&bar_sfree[t], 4);  // split P: S_t read into registers
+      mbar_init(&bar_pv[t], 1);     // split P: P_t V done (P_t and O_t reusable)
     }
     fence_barrier_init();
   }
@@ -225,6 +233,7 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t ph = 0, q_ph = 0;
       uint32_t p_ph[2] = {0, 0}, oe_ph[2] = {0, 0};  // bar_pl and bar_p complete in lockstep
       bool o_used[2] = {false, false};  // O_t holds an earlier item's accumulator (wait for its epilogue)
+      uint32_t sf_ph[2] = {0, 0};        // split P: bar_sfree phases
 #ifdef HK_TRACE
       uint32_t tstep[2] = {0, 0};
 #endif
@@ -244,8 +253,24 @@ __global__ void __launch_bounds__(384, 1)
         for (int j = 0; j < it.nkv; ++j) {
           const int s1 = s + 1 == NS ? 0 : s + 1;
           const uint32_t ph1 = s + 1 == NS ? ph ^ 1 : ph;
-          mbar_wait(&bar_vfull[s], ph);
           bool k_next_waited = false;
+          if constexpr (C::SPLIT_P) {  // S_t(j+1) as soon as the softmax has read S_t(j)
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const int nk = t == 0 ? it.nkv0 : it.nkv1;
+              if (j + 1 < nk) {
+                mbar_wait(&bar_sfree[t], sf_ph[t]);
+                sf_ph[t] ^= 1;
+                if (!k_next_waited) {
+                  mbar_wait(&bar_kfull[s1], ph1);
+                  k_next_waited = true;
+                }
+                tc_fence_after();
+                issue_s(t, s1);
+              }
+            }
+          }
+          mbar_wait(&bar_vfull[s], ph);
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             const int nk = t == 0 ? it.nkv0 : it.nkv1;
@@ -260,12 +285,20 @@ __global__ void __launch_bounds__(384, 1)
               hk_trace(10 + t, tstep[t]++, 0);  // MMA: P_t seen, PV issue (running step of tile t)
 #endif
               const uint64_t vd = dv0 + ((s * TB) >> 4);
-              gemm_ts_mn_lo(tbase + 256 + D * t, tbase + 128 * t, vd, idesc_o, j > 0 ? 1u : 0u);
+              const uint32_t tPa = C::SPLIT_P ? tbase + 256 + 2 * D + 64 * t : tbase + 128 * t;
+              gemm_ts_mn_lo(tbase + 256 + D * t, tPa, vd, idesc_o, j > 0 ? 1u : 0u);
               mbar_wait(&bar_p[t], p_ph[t]);
               p_ph[t] ^= 1;
               tc_fence_after();
-              gemm_ts_mn_hi(tbase + 256 + D * t, tbase + 128 * t, vd, idesc_o);
-              if (j + 1 < nk) {
+              gemm_ts_mn_hi(tbase + 256 + D * t, tPa, vd, idesc_o);
+              if (C::SPLIT_P) {
+                if (j + 1 < nk) {
+                  tc_commit_w(&bar_pv[t]);
+                } else {
+                  tc_commit_w(&bar_o[t]);
+                  o_used[t] = true;
+                }
+              } else if (j + 1 < nk) {
                 if (!k_next_waited) {
                   mbar_wait(&bar_kfull[s1], ph1);
                   tc_fence_after();
@@ -294,6 +327,8 @@ __global__ void __launch_bounds__(384, 1)
     const int t = warp >> 2;  // Q tile of this warpgroup
     const uint32_t tS = tbase + 128 * t;
     const uint32_t tO = tbase + 256 + D * t;
+    const uint32_t tP = C::SPLIT_P ? tbase + 256 + 2 * D + 64 * t : tS;  // bf16 P (split P: own columns)
+    uint32_t pv_ph = 0;
     const uint32_t lane_base = (warp & 3) * 32;
     const int r = (warp & 3) * 32 + lane;  // row within the Q tile == TMEM lane
     const float c = 1.4426950408889634f / sqrtf((float)D);  // (1/sqrt d) log2 e
@@ -330,7 +365,8 @@ __global__ void __launch_bounds__(384, 1)
         const int kleft = it.sq.lk - j * 128;
         const int kvalid = kleft < 128 ? kleft : 128;
         softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, shift, j > 0, kvalid, 40 + 4 * t, step,
-                                     &bar_pl[t]);
+                                     &bar_pl[t], tP, C::SPLIT_P && j + 1 < nk ? &bar_sfree[t] : nullptr,
+                                     C::SPLIT_P && j > 0 ? &bar_pv[t] : nullptr, &pv_ph);
         tmem_wait_st();
         if (threadIdx.x % 128 == 0) hk_trace(43 + 4 * t, step, 0);  // P stores complete
         tc_fence_before();

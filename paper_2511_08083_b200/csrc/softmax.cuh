@@ -53,10 +53,17 @@ __device__ __forceinline__ void softmax_chunk32(const float* s, float c, float m
 // run all exps on the MUFU so a masked P is exactly 0; a row that has seen no
 // key so far keeps m = -inf and l = 0 (reading #22). `o_live`: O already
 // holds earlier P V products.
+// Split-P mode (tP != tS, the d=64 forward): P goes to its own TMEM columns, the
+// S columns are released (bar_sfree) as soon as S is in registers so the next
+// S = Q K^T can overwrite them while this step runs, and the step waits for the
+// previous P V (bar_pv) before it rescales O or overwrites P.
 template <int D, int EMU_OF_8>
 __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t lane_base, int r, float c,
                                              float& m, float& l, int shift, bool o_live, int kvalid = 128,
-                                             int trace_ev = -1, uint32_t trace_idx = 0, uint64_t* bar_lo = nullptr) {
+                                             int trace_ev = -1, uint32_t trace_idx = 0, uint64_t* bar_lo = nullptr,
+                                             uint32_t tP = 0, uint64_t* bar_sfree = nullptr,
+                                             uint64_t* bar_pv = nullptr, uint32_t* pv_phase = nullptr) {
+  if (tP == 0) tP = tS;
 #ifdef HK_TRACE
   const bool tr = trace_ev >= 0 && (threadIdx.x % 128) == 0;
 #define HK_SM_TRACE(k) \
@@ -69,6 +76,11 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
   for (int c0 = 0; c0 < 128; c0 += 32)
     tmem_ld32(tmem_addr(tS, lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(&s[c0]));
   tmem_wait_ld();
+  if (bar_sfree != nullptr) {  // S columns free for the next S = Q K^T
+    tc_fence_before();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(bar_sfree);
+  }
   HK_SM_TRACE(0)  // S in registers
   const bool masked = shift < 127 || kvalid < 128;
   if (masked) {
@@ -94,8 +106,14 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
   }
   const float smin = (m_use - 125.f) / c;
   HK_SM_TRACE(1)  // row max done
-  // O holds P(j-1) V_{j-1}, complete: the S barrier tracked every earlier MMA. The
-  // rescale comes before any part of P(j) is published (P V(j) accumulates onto it).
+  if (bar_pv != nullptr) {  // split P: the previous P V must be complete (O and P reused)
+    mbar_wait(bar_pv, *pv_phase);
+    *pv_phase ^= 1;
+    tc_fence_after();
+  }
+  // O holds P(j-1) V_{j-1}, complete: the S barrier (split P: bar_pv) tracked every
+  // earlier MMA. The rescale comes before any part of P(j) is published (P V(j)
+  // accumulates onto it).
   if (o_live && __any_sync(0xffffffffu, alpha != 1.f)) {
     // 16 columns at a time: the 128 scores are still live here
 #pragma unroll 1
@@ -121,7 +139,7 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
       softmax_chunk32<false, EMU_OF_8>(s + c0, c, m_use == -INFINITY ? 0.f : m_use, smin, pk, acc);
     else
       softmax_chunk32<true, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);
-    tmem_st16(tmem_addr(tS, lane_base, c0 / 2), pk);
+    tmem_st16(tmem_addr(tP, lane_base, c0 / 2), pk);
     if (bar_lo != nullptr && c0 == 32) {  // P of keys [0, 64) (and the O rescale) in TMEM:
       tmem_wait_st();                     // the first half of P V may start
       tc_fence_before();
