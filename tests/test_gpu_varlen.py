@@ -145,3 +145,52 @@ def test_qk_full_size_sampled():
             assert np.abs(np64(o)[b, rows, h] - r["O"]).max() <= TOL_MAXABS
             assert np.abs(np64(lse)[b, h, rows] - r["LSE"]).max() <= TOL_MAXABS
             assert rel_l2(np64(dq)[b, rows, h], r["dQ"]) <= TOL_RELL2
+
+
+def test_varlen_full_size_sampled():
+    """The packed-document workload scripts/bench_varlen.py times (C3 heads, 131072
+    tokens, document lengths uniform in [1, 16383]) checked per document on
+    sampled query rows (O, LSE, dQ) and key rows (dK, dV) against the oracle run
+    on that document alone, plus the any-size invariants per document and KV head:
+    sum_j dK_j = 0 and sum_j dV_j = sum over the group's heads and rows of dO."""
+    from paper_2511_08083_b200 import attn_bwd_varlen, attn_fwd_varlen
+    from paper_2511_08083_b200.inputs import make_varlen_inputs, sample_rows, varlen_lengths
+    Hq, Hkv, d, causal, total = 32, 8, 128, True, 16 * 8192
+    lens, s = [], 0
+    for L in varlen_lengths(64, 8192, seed=7):
+        L = min(L, total - s)
+        lens.append(L)
+        s += L
+        if s == total:
+            break
+    x = make_varlen_inputs(lens, lens, Hq, Hkv, d, seed=1, device="cuda")
+    mx = max(lens)
+    o, lse = attn_fwd_varlen(x["Q"], x["K"], x["V"], x["cu_q"], x["cu_k"], mx, mx, causal)
+    dq, dk, dv = attn_bwd_varlen(x["Q"], x["K"], x["V"], o, lse, x["dO"], x["cu_q"], x["cu_k"], mx, mx, causal)
+    torch.cuda.synchronize()
+    cu = x["cu_q"].tolist()
+    G = Hq // Hkv
+    for b in (0, len(lens) // 2, len(lens) - 1):
+        a, e = cu[b], cu[b + 1]
+        n = e - a
+        Q, K, V, dO = (np64(x[k][a:e])[None] for k in ("Q", "K", "V", "dO"))
+        rows = sample_rows(n, 48, seed=b)  # first/last 8, tile edges, random (as the dense full-size tests)
+        kvh = 3
+        for h in (kvh * G, kvh * G + G - 1):
+            r = oracle.attn_rows(Q, K, V, dO, causal, 0, h, rows)
+            assert np.abs(np64(o)[a:e][rows, h] - r["O"]).max() <= TOL_MAXABS
+            assert np.abs(np64(lse)[h, a:e][rows] - r["LSE"]).max() <= TOL_MAXABS
+            assert rel_l2(np64(dq)[a:e][rows, h], r["dQ"]) <= TOL_RELL2
+        LSEf = np.zeros((1, Hq, n))
+        Df = np.zeros((1, Hq, n))
+        for h in range(kvh * G, kvh * G + G):
+            rr = oracle.attn_rows(Q, K, V, dO, causal, 0, h, np.arange(n))
+            LSEf[0, h], Df[0, h] = rr["LSE"], rr["D"]
+        kr = oracle.attn_key_rows(Q, K, V, dO, causal, 0, kvh, rows, LSEf, Df)
+        assert rel_l2(np64(dk)[a:e][rows, kvh], kr["dK"]) <= TOL_RELL2
+        assert rel_l2(np64(dv)[a:e][rows, kvh], kr["dV"]) <= TOL_RELL2
+        sdk = dk[a:e].float().sum(dim=0)
+        sdv = dv[a:e].float().sum(dim=0)
+        want = x["dO"][a:e].float().reshape(n, Hkv, G, d).sum(dim=(0, 2))
+        assert float(sdk.abs().max()) <= 0.05 * float(dk[a:e].float().abs().max()) * np.sqrt(n) / 8 + 1e-3
+        assert torch.allclose(sdv, want, rtol=2e-2, atol=0.05 * np.sqrt(n))
