@@ -66,15 +66,25 @@ __global__ void __launch_bounds__(256) ln_dropout_residual_kernel(const LnParams
   for (size_t row = gwarp; row < (size_t)p.rows; row += nwarps) {
     const uint4* xr = reinterpret_cast<const uint4*>(p.x + row * p.D);
     const uint4* rr = reinterpret_cast<const uint4*>(p.residual + row * p.D);
-    uint4 rv[VPL];
+    // every load of the row is issued before any store (the stores could alias the
+    // inputs as far as the compiler knows, which would serialise one round trip per vector)
+    uint4 xv[VPL], rv[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int v = lane + 32 * k;
+      if (v < nv) {
+        xv[k] = __ldcs(xr + v);  // streamed once: evict-first
+        rv[k] = __ldcs(rr + v);
+      }
+    }
     float sum = 0.f;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       const int v = lane + 32 * k;
       if (v < nv) {
         float xf[8], rf[8];
-        unpack8(__ldcs(xr + v), xf);  // streamed once: evict-first
-        unpack8(__ldcs(rr + v), rf);
+        unpack8(xv[k], xf);
+        unpack8(rv[k], rf);
         const uint32_t base = (uint32_t)(row * p.D + (size_t)v * 8);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
