@@ -48,29 +48,47 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
   const size_t gwarp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const size_t nwarps = (size_t)gridDim.x * blockDim.x / 32;
   const int lrow = (threadIdx.x % 32) / LPR;
-  for (size_t base = gwarp * RPW; base < rows; base += nwarps * RPW) {
-    const size_t row = base + lrow;
-    float acc = 0.f;
-    if (row < rows) {
-      const uint4 a = __ldg(reinterpret_cast<const uint4*>(O + (row0 + row) * D) + sub);
-      const uint4 g = __ldg(reinterpret_cast<const uint4*>(dO + (row0 + row) * D) + sub);
-      const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&a);
-      const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&g);
+  // U row groups per warp iteration, every load issued before the first reduction
+  // (bytes in flight per SM are what an HBM-bound pass needs)
+#ifndef HK_PRE_U128
+#define HK_PRE_U128 2
+#endif
+  constexpr int U = D == 128 ? HK_PRE_U128 : 4;  // measured (scripts/ab.py): d=128 best at 2, d=64 at 4
+  for (size_t base = gwarp * RPW * U; base < rows; base += nwarps * RPW * U) {
+    uint4 a[U], gv[U];
+    float L[U];  // LSE of the row (lane sub == 0), loaded with O / dO: not a dependent round trip later
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t row = base + u * RPW + lrow;
+      L[u] = 0.f;
+      if (row < rows) {
+        a[u] = __ldcs(reinterpret_cast<const uint4*>(O + (row0 + row) * D) + sub);
+        gv[u] = __ldcs(reinterpret_cast<const uint4*>(dO + (row0 + row) * D) + sub);
+        if (sub == 0) L[u] = __ldg(lse + lse_index(g, sq, b, H, (int)(row % H), (int)(row / H)));
+      } else {
+        a[u] = gv[u] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t row = base + u * RPW + lrow;
+      float acc = 0.f;
+      const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&a[u]);
+      const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&gv[u]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 x = __bfloat1622float2(ap[k]), y = __bfloat1622float2(gp[k]);
         acc = fmaf(x.x, y.x, acc);
         acc = fmaf(x.y, y.y, acc);
       }
-    }
 #pragma unroll
-    for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (row < rows && sub == 0) {
-      const int h = (int)(row % H), n = (int)(row / H);
-      const size_t idx = ((size_t)b * H + h) * Np + n;  // workspace rows are padded to Np
-      const float L = lse[lse_index(g, sq, b, H, h, n)];
-      Dout[idx] = acc;
-      lse2[idx] = L == -INFINITY ? INFINITY : L * 1.4426950408889634f;
+      for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (row < rows && sub == 0) {
+        const int h = (int)(row % H), n = (int)(row / H);
+        const size_t idx = ((size_t)b * H + h) * Np + n;  // workspace rows are padded to Np
+        Dout[idx] = acc;
+        lse2[idx] = L[u] == -INFINITY ? INFINITY : L[u] * 1.4426950408889634f;
+      }
     }
   }
   if (Np > sq.lq) {
