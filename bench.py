@@ -274,9 +274,29 @@ def main():
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     ws = torch.empty(bwd_workspace_bytes(B, Hq, Hkv, N, d) // 4, dtype=torch.float32, device="cuda")
 
-    def step():
+    L = _lib.lib()
+    import ctypes
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    st = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(st.cuda_stream)
+
+    def phase(ph):
+        # one of hk_attn_bwd's three stream-ordered kernels (pre, dK/dV, dQ) per call: the same
+        # validation and launches as the public entry point, so events can sit between kernels
+        _lib.check(L.hk_diag_bwd_phase(ph, P(q), P(k), P(v), P(o), P(lse), P(do), P(dq), P(dk), P(dv), P(ws),
+                                       ws.numel() * 4, B, Hq, Hkv, N, d, int(causal), sp))
+
+    def step(e=None):
+        """One step = hk_attn_fwd + hk_attn_bwd's kernels; e: 5 events around the 4 kernels."""
+        if e is not None:
+            e[0].record(st)
         attn_fwd(q, k, v, causal, out=o, lse=lse)
-        attn_bwd(q, k, v, o, lse, do, causal, workspace=ws, dq=dq, dk=dk, dv=dv)
+        if e is not None:
+            e[1].record(st)
+        for ph in range(3):
+            phase(ph)
+            if e is not None:
+                e[2 + ph].record(st)
 
     in_bytes = sum(t.numel() * t.element_size() for t in (q, k, v, do))
     l2_note = "inputs larger than L2 (126 MB)" if in_bytes > 126e6 else "L2 flushed between steps"
@@ -284,10 +304,11 @@ def main():
 
     for _ in range(args.warmup):
         step()
+    # the public backward entry point, once, on the same buffers (what e2e and the tests call)
+    attn_bwd(q, k, v, o, lse, do, causal, workspace=ws, dq=dq, dk=dk, dv=dv)
     torch.cuda.synchronize()
     barrier(world)
-    st = torch.cuda.current_stream()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         barrier(world)
@@ -295,40 +316,19 @@ def main():
         for i in range(args.steps):
             if flush is not None:
                 flush.zero_()
-            ev[i][0].record(st)
-            step()
-            ev[i][1].record(st)
+            step(ev[i])
         torch.cuda.synchronize()
         barrier(world)
         wall = time.perf_counter() - t0
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    step_ms = [e[0].elapsed_time(e[4]) for e in ev]
     ms = max_over_ranks(sum(step_ms) / len(step_ms), world)
     flops_rank = 3.5 * fwd_flops(B, N, Hq, d, causal)
     value = flops_rank * world / (ms * 1e-3) / 1e12
     launches = 4 * args.steps
 
-    # ---- per-kernel breakdown (same kernels, one launch per call, events between them)
-    L = _lib.lib()
-    import ctypes
-    P = lambda t: ctypes.c_void_p(t.data_ptr())
-    sp = ctypes.c_void_p(st.cuda_stream)
-
-    def phase(ph):
-        _lib.check(L.hk_diag_bwd_phase(ph, P(q), P(k), P(v), P(o), P(lse), P(do), P(dq), P(dk), P(dv), P(ws),
-                                       ws.numel() * 4, B, Hq, Hkv, N, d, int(causal), sp))
-
+    # ---- per-kernel durations from the events between kernels inside the timed region
     kern = {"fwd": [], "bwd_pre": [], "bwd_dkdv": [], "bwd_dq": []}
-    for it in range(args.steps + 1):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        e[0].record(st)
-        attn_fwd(q, k, v, causal, out=o, lse=lse)
-        e[1].record(st)
-        for ph in range(3):
-            phase(ph)
-            e[2 + ph].record(st)
-        torch.cuda.synchronize()
-        if it == 0:
-            continue  # warm
+    for e in ev:
         for i, name in enumerate(kern):
             kern[name].append(e[i].elapsed_time(e[i + 1]))
     kern_ms = {n: sum(t) / len(t) for n, t in kern.items()}
@@ -378,7 +378,10 @@ def main():
            "fwd_tflops_per_gpu": round(fwd_flops(B, N, Hq, d, causal) / (kern_ms["fwd"] * 1e-3) / 1e12, 1),
            "bwd_tflops_per_gpu": round(2.5 * fwd_flops(B, N, Hq, d, causal) /
                                        ((kern_ms["bwd_pre"] + kern_ms["bwd_dkdv"] + kern_ms["bwd_dq"]) * 1e-3) / 1e12, 1),
-           "kernels": kernels, "roofline": roofline, "gpu_launches": launches, "clocks": clk.summary(),
+           "kernels": kernels, "timing": "CUDA events on the launching stream around each of the step's 4 kernels "
+                                           "(hk_attn_fwd; hk_attn_bwd's pre, dK/dV, dQ one per call) inside the timed "
+                                           "region; value uses the first and last event of each step",
+           "roofline": roofline, "gpu_launches": launches, "clocks": clk.summary(),
            "wall_s_timed_region": round(wall, 3), "e2e": e2e}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args, x, o, lse, dq, dk, dv)
