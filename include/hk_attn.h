@@ -99,10 +99,14 @@ hk_status hk_attn_bwd_qk(const void* Q, const void* K, const void* V, const void
  * break the contract give undefined results, and rows beyond a sequence's
  * max_seqlen are not computed. A query sequence with no keys gets O = 0,
  * LSE = -inf, dQ = 0; keys no query sees get dK = dV = 0. */
+/* workspace: NULL (the forward's CTAs take work items in a static order) or >= 256 bytes of
+ * device memory, 16-B aligned, for the dynamic scheduler's counters (CTAs draw items from a
+ * counter: balanced when sequence lengths differ). Calls sharing a workspace must be
+ * stream-ordered; the call initialises it (no zeroing needed). */
 hk_status hk_attn_fwd_varlen(const void* Q, const void* K, const void* V, void* O, float* LSE,
                              const int* cu_seqlens_q, const int* cu_seqlens_k, int B, int Hq, int Hkv,
                              int total_q, int total_k, int max_seqlen_q, int max_seqlen_k, int d, int causal,
-                             cudaStream_t stream);
+                             void* workspace, size_t workspace_bytes, cudaStream_t stream);
 /* = 2*B*Hq*Mp*4 + 256, Mp = max_seqlen_q rounded up to a multiple of 128. */
 size_t hk_attn_bwd_varlen_workspace_bytes(int B, int Hq, int Hkv, int max_seqlen_q, int max_seqlen_k, int d);
 hk_status hk_attn_bwd_varlen(const void* Q, const void* K, const void* V, const void* O, const float* LSE,

@@ -27,7 +27,7 @@ SIGNATURES = {
     "hk_attn_fwd_qk": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P]),
     "hk_attn_bwd_qk_workspace_bytes": (_Z, [_I, _I, _I, _I, _I, _I]),
     "hk_attn_bwd_qk": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _I, _I, _I, _I, _I, _I, _I, _P]),
-    "hk_attn_fwd_varlen": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P]),
+    "hk_attn_fwd_varlen": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _Z, _P]),
     "hk_attn_bwd_varlen_workspace_bytes": (_Z, [_I, _I, _I, _I, _I, _I]),
     "hk_attn_bwd_varlen": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P, _P, _I, _I, _I, _I, _I, _I, _I,
                                 _I, _I, _P]),

@@ -103,18 +103,24 @@ def _varlen_args(q, k, v, cu_seqlens_q, cu_seqlens_k):
 
 
 def attn_fwd_varlen(q, k, v, cu_seqlens_q, cu_seqlens_k, max_seqlen_q: int, max_seqlen_k: int,
-                    causal: bool = False, out=None, lse=None):
+                    causal: bool = False, out=None, lse=None, workspace=None, dynamic: bool = True):
     """Packed variable-length attention (hk_attn_fwd_varlen). q [total_q,Hq,d],
     k/v [total_k,Hkv,d] bf16; cu_seqlens_* int32 [B+1] on the device (not
-    validated: see hk_attn.h). Returns (o [total_q,Hq,d], lse [Hq,total_q] fp32)."""
+    validated: see hk_attn.h). Returns (o [total_q,Hq,d], lse [Hq,total_q] fp32).
+    dynamic: CTAs draw work items from a counter in `workspace` (>= 256 bytes;
+    allocated here if None) — balanced when sequence lengths differ; False = static order."""
     B, tq, tk, Hq, Hkv, d = _varlen_args(q, k, v, cu_seqlens_q, cu_seqlens_k)
     o = torch.empty_like(q) if out is None else out
     L = torch.empty((Hq, tq), dtype=torch.float32, device=q.device) if lse is None else lse
     _check_tensor("out", o)
     _check_tensor("lse", L, torch.float32)
+    ws = None
+    if dynamic:
+        ws = torch.empty(64, dtype=torch.int32, device=q.device) if workspace is None else workspace
     check(lib().hk_attn_fwd_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), _ptr(cu_seqlens_q),
                                    _ptr(cu_seqlens_k), B, Hq, Hkv, tq, tk, int(max_seqlen_q), int(max_seqlen_k), d,
-                                   int(bool(causal)), _stream()))
+                                   int(bool(causal)), _ptr(ws) if ws is not None else None,
+                                   ws.numel() * ws.element_size() if ws is not None else 0, _stream()))
     return o, L
 
 

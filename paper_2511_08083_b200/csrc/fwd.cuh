@@ -27,6 +27,7 @@
 // pipe instead of the MUFU (16 ex2/clk/SM, the co-bottleneck at d=128).
 #pragma once
 #include "ptx.cuh"
+#include "sched.cuh"
 #include "seq.cuh"
 #include "softmax.cuh"
 
@@ -39,6 +40,7 @@ struct FwdParams {
   int B, Hq, Hkv;
   int num_pairs;  // ceil(Nq / 256): Q-tile pairs per head (varlen: of the longest sequence)
   int num_items;  // B * Hq * num_pairs work items
+  unsigned* sched;  // [2] work counters: dynamic scheduling (varlen with a workspace); nullptr = static snake
 };
 
 template <int D>
@@ -132,13 +134,16 @@ __global__ void __launch_bounds__(384, 1)
   __shared__ uint64_t bar_q, bar_qfree, bar_kfull[NS], bar_kempty[NS], bar_vfull[NS], bar_vempty[NS];
   __shared__ uint64_t bar_s[2], bar_p[2], bar_pl[2], bar_o[2], bar_oempty[2], bar_sfree[2], bar_pv[2];
   __shared__ uint32_t tmem_base_s;
+  __shared__ Sched sched;
 
   const int warp = warp_id();
   const int lane = lane_id();
   const int cta = blockIdx.x, ctas = gridDim.x;
+  const bool dyn = p.sched != nullptr;  // dynamic scheduling: every role takes the producer's draws
   if (threadIdx.x == 0) hk_trace(30, 0, 0);  // CTA start
 
   if (threadIdx.x == 0) {
+    sched_init(sched);
     mbar_init(&bar_q, 1);
     mbar_init(&bar_qfree, 1);
     for (int s = 0; s < NS; ++s) {
@@ -196,8 +201,22 @@ __global__ void __launch_bounds__(384, 1)
         }
       };
       bool first = true;
-      for (int r = fwd_next_busy<CAUSAL>(p, 0, cta, ctas); r >= 0; r = fwd_next_busy<CAUSAL>(p, r + 1, cta, ctas)) {
-        const FwdItem it = fwd_decode<CAUSAL>(p, fwd_item_index<CAUSAL>(r, cta, ctas));
+      int r = dyn ? 0 : fwd_next_busy<CAUSAL>(p, 0, cta, ctas);
+      for (;;) {
+        int item;
+        if (dyn) {  // items without any query row are drawn past; the rest go to every role
+          item = sched_publish(sched, p.sched, r++, p.num_items, [&](int i) {
+            const FwdItem w = fwd_decode<CAUSAL>(p, i);
+            return w.qt0 * 128 >= w.sq.lq;
+          });
+          if (item >= p.num_items) break;
+        } else {
+          if (r < 0) break;
+          item = fwd_item_index<CAUSAL>(r, cta, ctas);
+          r = fwd_next_busy<CAUSAL>(p, r + 1, cta, ctas);
+        }
+        const FwdItem it = fwd_decode<CAUSAL>(p, item);
+        if (it.nkv == 0) continue;
         load_kv(it, 0);  // K/V of the next item stream in while the previous one finishes
         if (!first) {    // Q buffer is free once the previous item's last S = Q K^T completed
           mbar_wait(&bar_qfree, qf_ph);
@@ -237,11 +256,25 @@ __global__ void __launch_bounds__(384, 1)
 #ifdef HK_TRACE
       uint32_t tstep[2] = {0, 0};
 #endif
-      int rn = fwd_next_busy<CAUSAL>(p, 0, cta, ctas);
-      while (rn >= 0) {
-        const FwdItem it = fwd_decode<CAUSAL>(p, fwd_item_index<CAUSAL>(rn, cta, ctas));
-        rn = fwd_next_busy<CAUSAL>(p, rn + 1, cta, ctas);
-        const bool last_item = rn < 0;
+      // static: the last busy item skips its final Q / V releases (nothing waits for them);
+      // dynamic: the next draw is unknown, so every release is committed and drained at exit
+      int rn = dyn ? 0 : fwd_next_busy<CAUSAL>(p, 0, cta, ctas);
+      int uses = 0, busy = 0;  // K/V ring uses and busy items so far (dynamic-mode drain)
+      for (;;) {
+        int item;
+        if (dyn) {
+          item = sched_take(sched, rn++);
+          if (item >= p.num_items) break;
+        } else {
+          if (rn < 0) break;
+          item = fwd_item_index<CAUSAL>(rn, cta, ctas);
+          rn = fwd_next_busy<CAUSAL>(p, rn + 1, cta, ctas);
+        }
+        const FwdItem it = fwd_decode<CAUSAL>(p, item);
+        if (it.nkv == 0) continue;
+        const bool last_item = !dyn && rn < 0;
+        uses += it.nkv;
+        ++busy;
         mbar_wait(&bar_q, q_ph);
         q_ph ^= 1;
         mbar_wait(&bar_kfull[s], ph);
@@ -320,6 +353,14 @@ __global__ void __launch_bounds__(384, 1)
           ph = ph1;
         }
       }
+      if (dyn) {  // let the releases nothing waits for land before the CTA exits
+        for (int k = 0; k < NS && k < uses; ++k) {
+          const int last = uses - 1 - ((uses - 1 - k) % NS);
+          mbar_wait(&bar_kempty[k], (last / NS) & 1);
+          mbar_wait(&bar_vempty[k], (last / NS) & 1);
+        }
+        if (busy > 0) mbar_wait(&bar_qfree, (busy - 1) & 1);
+      }
     }
   } else {
     // ================= softmax warpgroups =================
@@ -335,7 +376,7 @@ __global__ void __launch_bounds__(384, 1)
     uint32_t s_ph = 0, o_ph = 0;
     int step = 0;  // running KV-step count (trace index only)
     for (int rr = 0;; ++rr) {
-      const int item = fwd_item_index<CAUSAL>(rr, cta, ctas);
+      const int item = dyn ? sched_take(sched, rr) : fwd_item_index<CAUSAL>(rr, cta, ctas);
       if (item >= p.num_items) break;
       const FwdItem it = fwd_decode<CAUSAL>(p, item);
       const int nk = t == 0 ? it.nkv0 : it.nkv1;
@@ -411,6 +452,7 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc<512>(tbase);
+  if (dyn && threadIdx.x == 0) sched_exit(p.sched);
 }
 
 }  // namespace hk

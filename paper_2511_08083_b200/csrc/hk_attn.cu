@@ -182,7 +182,7 @@ static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V
 }
 
 static hk_status fwd_impl(const void* Q, const void* K, const void* V, void* O, float* LSE, const Shape& sh, int d,
-                          int causal, cudaStream_t stream) {
+                          int causal, cudaStream_t stream, void* workspace = nullptr, size_t workspace_bytes = 0) {
   g_err[0] = 0;
   hk_status s = validate_common(sh, d);
   if (s != HK_OK) return s;
@@ -195,6 +195,12 @@ static hk_status fwd_impl(const void* Q, const void* K, const void* V, void* O, 
       overlaps(LSE, lse_bytes, O, q_bytes) || overlaps(LSE, lse_bytes, Q, q_bytes) ||
       overlaps(LSE, lse_bytes, K, kv_bytes) || overlaps(LSE, lse_bytes, V, kv_bytes))
     return fail(HK_ERR_INVALID_ARGUMENT, "outputs O/LSE must not alias inputs or each other");
+  if (workspace && (workspace_bytes < 256 || !aligned16(workspace)))
+    return fail(HK_ERR_INVALID_ARGUMENT, "forward workspace must be >= 256 bytes and 16-byte aligned");
+  if (workspace && (overlaps(workspace, 256, O, q_bytes) || overlaps(workspace, 256, LSE, lse_bytes) ||
+                    overlaps(workspace, 256, Q, q_bytes) || overlaps(workspace, 256, K, kv_bytes) ||
+                    overlaps(workspace, 256, V, kv_bytes)))
+    return fail(HK_ERR_INVALID_ARGUMENT, "workspace must not alias the inputs or outputs");
   int num_sms = 0;
   s = check_device(&num_sms);
   if (s != HK_OK) return s;
@@ -214,6 +220,9 @@ static hk_status fwd_impl(const void* Q, const void* K, const void* V, void* O, 
   p.Hkv = sh.Hkv;
   p.num_pairs = ((sh.Nq + 127) / 128 + 1) / 2;
   p.num_items = sh.B * sh.Hq * p.num_pairs;
+  p.sched = reinterpret_cast<unsigned*>(workspace);  // dynamic scheduling when given a workspace
+  if (workspace && cudaMemsetAsync(workspace, 0, 8, stream) != cudaSuccess)
+    return fail(HK_ERR_LAUNCH, "cudaMemsetAsync(workspace counters) failed");
   if (d == 64)
     return causal ? launch_fwd<64, true>(mq, mk, mv, p, num_sms, stream)
                   : launch_fwd<64, false>(mq, mk, mv, p, num_sms, stream);
@@ -242,7 +251,7 @@ const char* hk_status_string(hk_status s) {
   return "HK_ERR_UNKNOWN";
 }
 
-int hk_attn_abi_version(void) { return 2; }  // 2: + Nq != Nk and varlen entry points
+int hk_attn_abi_version(void) { return 3; }  // 2: + Nq != Nk and varlen entry points
 
 hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, float* LSE, int B, int Hq, int Hkv,
                       int N, int d, int causal, cudaStream_t stream) {
@@ -281,15 +290,15 @@ hk_status hk_attn_bwd_qk(const void* Q, const void* K, const void* V, const void
 }
 hk_status hk_attn_fwd_varlen(const void* Q, const void* K, const void* V, void* O, float* LSE,
                              const int* cu_seqlens_q, const int* cu_seqlens_k, int B, int Hq, int Hkv, int total_q,
-                             int total_k, int max_seqlen_q, int max_seqlen_k, int d, int causal,
-                             cudaStream_t stream) {
+                             int total_k, int max_seqlen_q, int max_seqlen_k, int d, int causal, void* workspace,
+                             size_t workspace_bytes, cudaStream_t stream) {
   if (!cu_seqlens_q || !cu_seqlens_k) {
     g_err[0] = 0;
     return fail(HK_ERR_INVALID_ARGUMENT, "null cu_seqlens");
   }
   return fwd_impl(Q, K, V, O, LSE,
                   packed(cu_seqlens_q, cu_seqlens_k, B, Hq, Hkv, total_q, total_k, max_seqlen_q, max_seqlen_k), d,
-                  causal, stream);
+                  causal, stream, workspace, workspace_bytes);
 }
 size_t hk_attn_bwd_varlen_workspace_bytes(int B, int Hq, int Hkv, int max_seqlen_q, int max_seqlen_k, int d) {
   (void)Hkv;

@@ -74,14 +74,19 @@ def main():
     mx = max(lens)
     o, lse = attn_fwd_varlen(x["Q"], x["K"], x["V"], x["cu_q"], x["cu_k"], mx, mx, causal)
     ws = torch.empty(int(2 * len(lens) * Hq * ((mx + 127) // 128 * 128) + 64), dtype=torch.float32, device="cuda")
-    t_f = timed(lambda: attn_fwd_varlen(x["Q"], x["K"], x["V"], x["cu_q"], x["cu_k"], mx, mx, causal, out=o, lse=lse),
-                a.iters)
+    fws = torch.empty(64, dtype=torch.int32, device="cuda")
+    t_fs = timed(lambda: attn_fwd_varlen(x["Q"], x["K"], x["V"], x["cu_q"], x["cu_k"], mx, mx, causal, out=o, lse=lse,
+                                         dynamic=False), a.iters)
+    t_f = timed(lambda: attn_fwd_varlen(x["Q"], x["K"], x["V"], x["cu_q"], x["cu_k"], mx, mx, causal, out=o, lse=lse,
+                                        workspace=fws), a.iters)
     g = [torch.empty_like(x[n]) for n in ("Q", "K", "V")]
     t_b = timed(lambda: attn_bwd_varlen(x["Q"], x["K"], x["V"], o, lse, x["dO"], x["cu_q"], x["cu_k"], mx, mx, causal,
                                         workspace=ws, dq=g[0], dk=g[1], dv=g[2]), a.iters)
     npairs = sum(pairs(L, L, causal) for L in lens)
     report("varlen_C3_docs", {"docs": len(lens), "tokens": total, "max_len": mx, "Hq": Hq, "Hkv": Hkv, "d": d,
-                              "causal": causal}, npairs, Hq, d, t_f, t_b, peak)
+                              "causal": causal, "fwd_schedule": "dynamic",
+                              "fwd_tflops_static_schedule": round(4.0 * d * Hq * npairs / t_fs / 1e9, 1)},
+           npairs, Hq, d, t_f, t_b, peak)
     del x, o, lse, ws, g
     y = make_inputs(16, 8192, Hq, Hkv, d, seed=1, device="cuda")
     o, lse = attn_fwd(y["Q"], y["K"], y["V"], causal)

@@ -46,7 +46,7 @@ def test_host_only_validation(lib):
     size, and argument validation that fails before any CUDA call."""
     from paper_2511_08083_b200 import _lib
     L = _lib.lib()
-    assert L.hk_attn_abi_version() == 2
+    assert L.hk_attn_abi_version() == 3
     assert L.hk_status_string(2) == b"HK_ERR_UNSUPPORTED"
     assert L.hk_attn_bwd_workspace_bytes(2, 4, 2, 256, 64) == 2 * 2 * 4 * 256 * 4 + 256
     p = ctypes.c_void_p(16)

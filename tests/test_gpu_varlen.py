@@ -194,3 +194,20 @@ def test_varlen_full_size_sampled():
         want = x["dO"][a:e].float().reshape(n, Hkv, G, d).sum(dim=(0, 2))
         assert float(sdk.abs().max()) <= 0.05 * float(dk[a:e].float().abs().max()) * np.sqrt(n) / 8 + 1e-3
         assert torch.allclose(sdv, want, rtol=2e-2, atol=0.05 * np.sqrt(n))
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_varlen_dynamic_schedule_equals_static_bitwise(causal):
+    """The forward's dynamic scheduler (workspace counter) changes only which CTA takes
+    which item: O and LSE must be bitwise those of the static order, across repeats."""
+    from paper_2511_08083_b200 import attn_fwd_varlen
+    from paper_2511_08083_b200.inputs import make_varlen_inputs
+    lens = [900, 3, 0, 2049, 640, 1, 1500]
+    x = make_varlen_inputs(lens, lens, 8, 2, 128, seed=21, device="cuda")
+    args = (x["Q"], x["K"], x["V"], x["cu_q"], x["cu_k"], max(lens), max(lens), causal)
+    o0, l0 = attn_fwd_varlen(*args, dynamic=False)
+    ws = torch.empty(64, dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        o1, l1 = attn_fwd_varlen(*args, workspace=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(o0, o1) and torch.equal(l0, l1)
