@@ -154,12 +154,49 @@ def _accum(acc, x, out=None, init=False):
                               api._stream()))
 
 
+class _Fanout:
+    """Runs a step's independent attention calls on a pool of side streams (so the small
+    chunk-pair kernels of one step fill the SMs together); the dependent merges and
+    accumulations stay on the calling stream, in plan order, each after its call's event.
+    n <= 1: everything on the calling stream, in order."""
+
+    def __init__(self, n: int):
+        self.main = torch.cuda.current_stream()
+        self.side = [torch.cuda.Stream() for _ in range(n)] if n > 1 else []
+        self.i = 0
+
+    def begin(self):  # side streams see everything enqueued so far on the calling stream
+        if self.side:
+            e = torch.cuda.Event()
+            e.record(self.main)
+            for st in self.side:
+                st.wait_event(e)
+
+    def run(self, fn):
+        if not self.side:
+            fn()
+            return None
+        st = self.side[self.i % len(self.side)]
+        self.i += 1
+        with torch.cuda.stream(st):
+            fn()
+        e = torch.cuda.Event()
+        e.record(st)
+        return e
+
+    def join(self, e):
+        if e is not None:
+            self.main.wait_event(e)
+
+
 # ---------------------------------------------------------------- forward / backward
-def ring_attn_fwd(q, k, v, causal: bool, comm: RingComm):
+def ring_attn_fwd(q, k, v, causal: bool, comm: RingComm, streams: int = 1):
     """q, k, v: per local rank, (A, B) chunk pairs of [B, c, H, d] bf16 CUDA tensors
     (zigzag_shard). Returns per local rank ((oA, oB), (lseA, lseB)): O bf16
-    [B, c, Hq, d], LSE fp32 [B, Hq, c] of the attention over the whole sequence."""
+    [B, c, Hq, d], LSE fp32 [B, Hq, c] of the attention over the whole sequence.
+    streams > 1: a step's attention calls run concurrently on that many side streams."""
     P = comm.world
+    fan = _Fanout(streams)
     plans = [plan(P, r, causal) for r in comm.ranks]
     out = []
     for li, _ in enumerate(comm.ranks):
@@ -173,24 +210,35 @@ def ring_attn_fwd(q, k, v, causal: bool, comm: RingComm):
     kv = [[k[li][0], k[li][1], v[li][0], v[li][1]] for li in range(len(comm.ranks))]
     for s in range(P):
         handle = comm.start(kv) if s + 1 < P else None
+        fan.begin()
+        parts = []
         for li in range(len(comm.ranks)):
-            st = out[li]
             for i, (ps, qh, kh, mode) in enumerate(plans[li]):
                 if ps != s:
                     continue
-                o_p, l_p = api.attn_fwd(q[li][qh], kv[li][kh], kv[li][2 + kh], mode == "causal")
-                _merge(st["acc"][qh], st["lse"][qh], o_p, l_p, st["o"][qh] if i == st["last"][qh] else None,
-                       st["seen"][qh] == 0)
-                st["seen"][qh] += 1
+                qq, kk, vv = q[li][qh], kv[li][kh], kv[li][2 + kh]
+                o_p = torch.empty_like(qq)
+                l_p = torch.empty((qq.shape[0], qq.shape[2], qq.shape[1]), dtype=torch.float32, device=qq.device)
+                e = fan.run(lambda qq=qq, kk=kk, vv=vv, o_p=o_p, l_p=l_p, m=mode:
+                            api.attn_fwd(qq, kk, vv, m == "causal", out=o_p, lse=l_p))
+                parts.append((li, i, qh, o_p, l_p, e))
+        for li, i, qh, o_p, l_p, e in parts:
+            st = out[li]
+            fan.join(e)
+            _merge(st["acc"][qh], st["lse"][qh], o_p, l_p, st["o"][qh] if i == st["last"][qh] else None,
+                   st["seen"][qh] == 0)
+            st["seen"][qh] += 1
         if handle is not None:
             kv = comm.finish(handle)
     return [((st["o"][0], st["o"][1]), (st["lse"][0], st["lse"][1])) for st in out]
 
 
-def ring_attn_bwd(q, k, v, o, lse, do, causal: bool, comm: RingComm):
+def ring_attn_bwd(q, k, v, o, lse, do, causal: bool, comm: RingComm, streams: int = 1):
     """Backward of ring_attn_fwd. All arguments per local rank as (A, B) chunk pairs
-    (o, lse from ring_attn_fwd). Returns per local rank ((dqA, dqB), (dkA, dkB), (dvA, dvB))."""
+    (o, lse from ring_attn_fwd). Returns per local rank ((dqA, dqB), (dkA, dkB), (dvA, dvB)).
+    streams > 1: a step's backward calls run concurrently on that many side streams."""
     P = comm.world
+    fan = _Fanout(streams)
     plans = [plan(P, r, causal) for r in comm.ranks]
     n_local = len(comm.ranks)
     dq_acc = [[torch.empty(q[li][h].shape, dtype=torch.float32, device=q[li][h].device) for h in (0, 1)]
@@ -209,18 +257,29 @@ def ring_attn_bwd(q, k, v, o, lse, do, causal: bool, comm: RingComm):
         # accumulators follow once this step's contributions are in (after the last
         # step that rotation brings every chunk's dK, dV back to its owner)
         h_kv = comm.start([t[:4] for t in trav]) if s + 1 < P else None
+        fan.begin()
+        parts = []
         for li in range(n_local):
             t = trav[li]
             for i, (ps, qh, kh, mode) in enumerate(plans[li]):
                 if ps != s:
                     continue
-                dq_p, dk_p, dv_p = api.attn_bwd(q[li][qh], t[kh], t[2 + kh], o[li][qh], lse[li][qh], do[li][qh],
-                                                mode == "causal")
-                last = i == dq_last[li][qh]
-                _accum(dq_acc[li][qh], dq_p, dq[li][qh] if last else None, dq_seen[li][qh] == 0)
-                dq_seen[li][qh] += 1
-                _accum(t[4 + kh], dk_p)
-                _accum(t[6 + kh], dv_p)
+                args = (q[li][qh], t[kh], t[2 + kh], o[li][qh], lse[li][qh], do[li][qh])
+                g = [torch.empty_like(args[0]), torch.empty_like(args[1]), torch.empty_like(args[2])]
+                ws = torch.empty(api.bwd_workspace_bytes(args[0].shape[0], args[0].shape[2], args[1].shape[2],
+                                                         args[0].shape[1], args[0].shape[3]) // 4,
+                                 dtype=torch.float32, device=args[0].device)
+                e = fan.run(lambda args=args, g=g, ws=ws, m=mode:
+                            api.attn_bwd(*args, m == "causal", workspace=ws, dq=g[0], dk=g[1], dv=g[2]))
+                parts.append((li, i, qh, kh, g, e))
+        for li, i, qh, kh, (dq_p, dk_p, dv_p), e in parts:
+            t = trav[li]
+            fan.join(e)
+            last = i == dq_last[li][qh]
+            _accum(dq_acc[li][qh], dq_p, dq[li][qh] if last else None, dq_seen[li][qh] == 0)
+            dq_seen[li][qh] += 1
+            _accum(t[4 + kh], dk_p)
+            _accum(t[6 + kh], dv_p)
         acc = comm.finish(comm.start([t[4:] for t in trav]))
         kv = comm.finish(h_kv) if h_kv is not None else [[None] * 4 for _ in range(n_local)]
         trav = [kv[li] + acc[li] for li in range(n_local)]

@@ -47,11 +47,12 @@ def main():
             sh = {n: [ring.zigzag_shard(x[n], P, r) for r in range(P)] for n in ("Q", "K", "V", "dO")}
             comm = ring.LoopbackRing(P)
 
-            def step():
-                fw = ring.ring_attn_fwd(sh["Q"], sh["K"], sh["V"], causal, comm)
+            def step(streams=1):
+                fw = ring.ring_attn_fwd(sh["Q"], sh["K"], sh["V"], causal, comm, streams=streams)
                 ring.ring_attn_bwd(sh["Q"], sh["K"], sh["V"], [f[0] for f in fw], [f[1] for f in fw], sh["dO"],
-                                   causal, comm)
+                                   causal, comm, streams=streams)
             t = timed(step)
+            t_s = timed(lambda: step(4))
             # the same schedule captured once into a CUDA graph: no host launch overhead per kernel
             step()
             torch.cuda.synchronize()
@@ -63,7 +64,9 @@ def main():
                               "Hkv": Hkv, "d": d, "causal": causal, "ms_all_ranks": round(t, 3),
                               "tflops": round(flops / t / 1e9, 1), "vs_dense": round(t_d / t, 3),
                               "graph_ms_all_ranks": round(t_g, 3), "graph_tflops": round(flops / t_g / 1e9, 1),
-                              "graph_vs_dense": round(t_d / t_g, 3)}), flush=True)
+                              "graph_vs_dense": round(t_d / t_g, 3), "streams4_ms_all_ranks": round(t_s, 3),
+                              "streams4_tflops": round(flops / t_s / 1e9, 1),
+                              "streams4_vs_dense": round(t_d / t_s, 3)}), flush=True)
             del g
             del sh
         del x

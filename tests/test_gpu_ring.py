@@ -88,7 +88,13 @@ def test_ring_loopback_matches_whole_sequence(case, causal):
     o = [f[0] for f in fw]
     lse = [f[1] for f in fw]
     bw = ring.ring_attn_bwd(sh["Q"], sh["K"], sh["V"], o, lse, sh["dO"], causal, comm)
+    # the same schedule with each step's calls on 3 side streams: bitwise the same results
+    fw3 = ring.ring_attn_fwd(sh["Q"], sh["K"], sh["V"], causal, comm, streams=3)
+    bw3 = ring.ring_attn_bwd(sh["Q"], sh["K"], sh["V"], o, lse, sh["dO"], causal, comm, streams=3)
     torch.cuda.synchronize()
+    for r in range(P):
+        assert all(torch.equal(a, b) for a, b in zip(fw[r][0] + fw[r][1], fw3[r][0] + fw3[r][1]))
+        assert all(torch.equal(a, b) for x, y in zip(bw[r], bw3[r]) for a, b in zip(x, y))
     O = ring.zigzag_unshard(o)
     LSE = ring.zigzag_unshard([(a.transpose(1, 2), b.transpose(1, 2)) for a, b in lse]).transpose(1, 2)
     dQ, dK, dV = (ring.zigzag_unshard([b[i] for b in bw]) for i in range(3))
