@@ -19,10 +19,10 @@ struct Sched {
   uint64_t full[SCHED_NQ], empty[SCHED_NQ];
   int item[SCHED_NQ];
 };
-__device__ __forceinline__ void sched_init(Sched& q) {
+__device__ __forceinline__ void sched_init(Sched& q, int consumers = 9) {  // default: MMA warp + 8 warps
   for (int i = 0; i < SCHED_NQ; ++i) {
     mbar_init(&q.full[i], 1);
-    mbar_init(&q.empty[i], 9);  // the MMA warp + 8 elementwise warps
+    mbar_init(&q.empty[i], consumers);
   }
 }
 // producer lane: draw number k. `skip(item)` (optional) marks items no role has any
