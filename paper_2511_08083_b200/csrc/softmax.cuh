@@ -104,7 +104,9 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
     m_use = ceilf(mxs);        // integral max: exact f in the polynomial exp
     alpha = ex2(m - m_use);
   }
-  const float smin = (m_use - 125.f) / c;
+  // scores below smin would take the emulated 2^x under 2^-125; multiply by 1/c (a division
+  // here compiled to the IEEE slow path: FCHK + call, every step)
+  const float smin = (m_use - 125.f) * __frcp_rn(c);
   HK_SM_TRACE(1)  // row max done
   if (bar_pv != nullptr) {  // split P: the previous P V must be complete (O and P reused)
     mbar_wait(bar_pv, *pv_phase);
