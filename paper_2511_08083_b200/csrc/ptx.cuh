@@ -77,7 +77,23 @@ __device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, in
 }
 #define mbar_wait(bar, parity) mbar_wait_dbg((bar), (parity), __LINE__)
 #else
+// HK_WAIT_HINT (ns): suspend-time hint of try_wait. Without it the hardware returns after
+// a short, system-dependent time and the retry loop (try_wait, branch, yield) issued ~18% of
+// all forward instructions (ncu r1g), taking issue slots from the softmax warps of the same
+// sub-partition; the warp is woken when the phase completes either way.
+#ifndef HK_WAIT_HINT
+#define HK_WAIT_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if HK_WAIT_HINT
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"((uint32_t)HK_WAIT_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
@@ -85,6 +101,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 #endif
 
