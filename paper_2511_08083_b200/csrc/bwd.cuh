@@ -478,13 +478,17 @@ __global__ void __launch_bounds__(320, 1)
         tmem_ld64(tmem_addr(cP, lb, 0), dp);
         tmem_wait_ld();
 #pragma unroll
-        for (int c4 = 0; c4 < 64; c4 += 4) {
+        for (int c4 = 0; c4 < 64; c4 += 4) {  // packed f32x2: half the issue slots of scalar FADD + FMUL
           float d0, d1, d2, d3;
           lds_v4(vec + 512 + 4 * (64 * wg + c4), d0, d1, d2, d3);
-          dp[c4 + 0] = v[c4 + 0] * (dp[c4 + 0] - d0);
-          dp[c4 + 1] = v[c4 + 1] * (dp[c4 + 1] - d1);
-          dp[c4 + 2] = v[c4 + 2] * (dp[c4 + 2] - d2);
-          dp[c4 + 3] = v[c4 + 3] * (dp[c4 + 3] - d3);
+          const float2 a = mul2(make_float2(v[c4], v[c4 + 1]),
+                                sub2(make_float2(dp[c4], dp[c4 + 1]), make_float2(d0, d1)));
+          const float2 b = mul2(make_float2(v[c4 + 2], v[c4 + 3]),
+                                sub2(make_float2(dp[c4 + 2], dp[c4 + 3]), make_float2(d2, d3)));
+          dp[c4] = a.x;
+          dp[c4 + 1] = a.y;
+          dp[c4 + 2] = b.x;
+          dp[c4 + 3] = b.y;
         }
         tmem_st_packed64(tmem_addr(cP, lb, 0), dp);
         tmem_wait_st();
@@ -814,7 +818,12 @@ __global__ void __launch_bounds__(320, 1)
         tmem_ld64(tmem_addr(cP, lb, 0), dp);
         tmem_wait_ld();
 #pragma unroll
-        for (int cc = 0; cc < 64; ++cc) dp[cc] = v[cc] * (dp[cc] - Dq);
+        for (int cc = 0; cc < 64; cc += 2) {  // packed f32x2: half the issue slots of scalar FADD + FMUL
+          const float2 r2 = mul2(make_float2(v[cc], v[cc + 1]),
+                                 sub2(make_float2(dp[cc], dp[cc + 1]), make_float2(Dq, Dq)));
+          dp[cc] = r2.x;
+          dp[cc + 1] = r2.y;
+        }
         tmem_st_packed64(tmem_addr(cP, lb, 0), dp);
         tmem_wait_st();
         tc_fence_before();
