@@ -65,3 +65,31 @@ def test_host_only_validation(lib):
     a = [ctypes.c_void_p(16 * (i + 1) << 30) for i in range(10)]
     assert L.hk_attn_bwd(*a, 0, 1, 2, 2, 128, 64, 0, None) == 1
     assert b"workspace" in L.hk_attn_last_error()
+
+
+def test_host_only_validation_next4(lib):
+    """Validation of the NEXT #4 entry points (Nq != Nk, varlen, ring merge / accumulate)
+    fails before any CUDA call; workspace sizes follow the header formulas."""
+    from paper_2511_08083_b200 import _lib
+    L = _lib.lib()
+    p = ctypes.c_void_p(16)
+    Z = ctypes.c_size_t
+    assert L.hk_attn_bwd_qk_workspace_bytes(2, 4, 2, 200, 1000, 64) == 2 * 2 * 4 * 256 * 4 + 256
+    assert L.hk_attn_bwd_varlen_workspace_bytes(3, 4, 2, 129, 7, 128) == 2 * 3 * 4 * 256 * 4 + 256
+    assert L.hk_attn_fwd_qk(p, p, p, p, p, 1, 2, 2, 128, 0, 64, 0, None) == 1     # Nk = 0
+    assert L.hk_attn_fwd_qk(p, p, p, p, p, 1, 2, 2, 128, 256, 80, 0, None) == 2   # d = 80
+    a = [ctypes.c_void_p(16 * (i + 1) << 30) for i in range(7)]
+    # varlen: null offsets, zero totals, misaligned offsets, a too-small forward workspace
+    assert L.hk_attn_fwd_varlen(*a[:5], None, a[6], 2, 2, 2, 100, 100, 64, 64, 64, 0, None, Z(0), None) == 1
+    assert L.hk_attn_fwd_varlen(*a[:7], 2, 2, 2, 0, 100, 64, 64, 64, 0, None, Z(0), None) == 1
+    assert L.hk_attn_fwd_varlen(*a[:5], ctypes.c_void_p(18), a[6], 2, 2, 2, 100, 100, 64, 64, 64, 0, None, Z(0),
+                                None) == 1
+    assert L.hk_attn_fwd_varlen(*a[:7], 2, 2, 2, 100, 100, 64, 64, 64, 0, ctypes.c_void_p(16 << 35), Z(64),
+                                None) == 1
+    assert b"workspace" in L.hk_attn_last_error()
+    # ring building blocks
+    assert L.hk_attn_merge(p, p, p, p, None, 1, 128, 2, 96, 0, None) == 2       # d not a power of two
+    assert L.hk_attn_merge(p, p, p, p, None, 0, 128, 2, 64, 0, None) == 1       # B = 0
+    assert L.hk_attn_merge(p, p, p, p, None, 1, 128, 2, 64, 0, None) == 1       # buffers overlap
+    assert L.hk_accum_bf16(p, p, None, Z(12), 0, None) == 1                     # n % 8
+    assert L.hk_accum_bf16(None, None, p, Z(16), 0, None) == 1                  # nothing to read
