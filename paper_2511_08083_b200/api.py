@@ -102,6 +102,22 @@ def _varlen_args(q, k, v, cu_seqlens_q, cu_seqlens_k):
     return cu_seqlens_q.numel() - 1, q.shape[0], k.shape[0], q.shape[1], k.shape[1], q.shape[2]
 
 
+def check_cu_seqlens(cu_seqlens_q, cu_seqlens_k, total_q: int, total_k: int, max_seqlen_q: int,
+                     max_seqlen_k: int):
+    """Host-side check of the varlen offset contract of include/hk_attn.h (the library does not
+    read device offsets on the host): cu[0] = 0, non-decreasing, cu[B] = total, every length
+    <= max_seqlen. Copies the offsets to the host (a synchronisation): a debugging aid, not
+    called on the fast path. Raises ValueError."""
+    for name, cu, total, mx in (("q", cu_seqlens_q, total_q, max_seqlen_q), ("k", cu_seqlens_k, total_k,
+                                                                              max_seqlen_k)):
+        c = [int(x) for x in cu.detach().cpu().tolist()]
+        lens = [b - a for a, b in zip(c, c[1:])]
+        if c[0] != 0 or c[-1] != total or any(n < 0 for n in lens):
+            raise ValueError(f"cu_seqlens_{name} must rise from 0 to total_{name}={total}: {c[:8]}...")
+        if lens and max(lens) > mx:
+            raise ValueError(f"a {name} sequence has length {max(lens)} > max_seqlen_{name}={mx}")
+
+
 def attn_fwd_varlen(q, k, v, cu_seqlens_q, cu_seqlens_k, max_seqlen_q: int, max_seqlen_k: int,
                     causal: bool = False, out=None, lse=None, workspace=None, dynamic: bool = True):
     """Packed variable-length attention (hk_attn_fwd_varlen). q [total_q,Hq,d],

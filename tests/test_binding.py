@@ -40,3 +40,14 @@ def test_library_missing_is_loud(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "_LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(RuntimeError, match="not built"):
         _lib.lib()
+
+
+def test_check_cu_seqlens():
+    cu = lambda *v: torch.tensor(v, dtype=torch.int32)
+    api.check_cu_seqlens(cu(0, 3, 3, 10), cu(0, 5, 9, 9), 10, 9, 7, 5)
+    with pytest.raises(ValueError, match="rise"):
+        api.check_cu_seqlens(cu(0, 3, 2, 10), cu(0, 5, 9, 9), 10, 9, 8, 5)
+    with pytest.raises(ValueError, match="rise"):
+        api.check_cu_seqlens(cu(0, 3, 3, 10), cu(0, 5, 9, 9), 11, 9, 8, 5)
+    with pytest.raises(ValueError, match="max_seqlen_q"):
+        api.check_cu_seqlens(cu(0, 3, 3, 10), cu(0, 5, 9, 9), 10, 9, 6, 5)
