@@ -16,10 +16,15 @@ from paper_2511_08083_b200 import _lib, attn_fwd  # noqa: E402
 from paper_2511_08083_b200.inputs import make_inputs  # noqa: E402
 
 shapes = {"C5-1024-c": (16, 1024, 64, 8, 128, True), "C5-1024-nc": (16, 1024, 64, 8, 128, False),
+          "qk-c": (16, 1024, 32, 8, 128, True, 16384), "qk-nc": (16, 1024, 32, 8, 128, False, 16384),
           "C3": (16, 8192, 32, 8, 128, True), "C4-2048": (16, 2048, 32, 32, 64, True)}
 for cfg in sys.argv[1:]:
-    B, N, Hq, Hkv, d, causal = shapes[cfg]
-    x = make_inputs(B, N, Hq, Hkv, d, seed=0, device="cuda")
+    B, N, Hq, Hkv, d, causal = shapes[cfg][:6]
+    if len(shapes[cfg]) > 6:  # Nq != Nk
+        from paper_2511_08083_b200.inputs import make_qk_inputs
+        x = make_qk_inputs(B, N, shapes[cfg][6], Hq, Hkv, d, seed=0, device="cuda")
+    else:
+        x = make_inputs(B, N, Hq, Hkv, d, seed=0, device="cuda")
     L = _lib.lib()
     attn_fwd(x["Q"], x["K"], x["V"], causal)
     torch.cuda.synchronize()
