@@ -34,10 +34,10 @@ def main():
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     a = ap.parse_args()
-    peaks = {}
-    pp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
-    if os.path.exists(pp):
-        peaks = json.load(open(pp))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from bench import load_peaks  # MEASURED_PEAKS.json, else the profiling guide's fallback
+    pk = load_peaks()
     for sh in a.shapes.split(";"):
         M, N, K = (int(v) for v in sh.split(","))
         x = make_gemm_inputs(M, N, K, seed=0, device="cuda")
@@ -53,7 +53,9 @@ def main():
         rec = {"metric": "bf16 GEMM C = A B^T TFLOPS", "shape": [M, N, K], "ours_ms": round(mo, 4),
                "ours_tflops": round(flops / mo / 1e9, 1), "cublas_ms": round(mc, 4),
                "cublas_tflops": round(flops / mc / 1e9, 1), "ours_vs_cublas": round(mc / mo, 3),
-               "peaks_json": {k: v for k, v in peaks.items() if "bf16" in k.lower() or "tflop" in k.lower()}}
+               "roofline": {"bound": "tensor", "peak_burst": pk["burst"], "frac_of_burst":
+                            round(flops / mo / 1e9 / pk["burst"], 3), "cublas_frac_of_burst":
+                            round(flops / mc / 1e9 / pk["burst"], 3), "peaks_source": pk["source"]}}
         print(json.dumps(rec), flush=True)
         del x, A, B, C
 
