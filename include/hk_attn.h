@@ -60,8 +60,12 @@ hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, floa
 size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d);
 
 /* Backward: given Q, K, V, the forward's O and LSE, and dO, writes dQ, dK, dV
- * (bf16, fully overwritten). Runs three stream-ordered kernels:
- * D-preprocess, dK/dV pass (GQA group reduced inside the kernel), dQ pass. */
+ * (bf16, fully overwritten). Runs three kernels: D-preprocess, then the dK/dV pass
+ * (GQA group reduced inside the kernel) on `stream` and the dQ pass, which is
+ * independent of it, on a library-owned non-blocking side stream forked from `stream`
+ * after the preprocess and joined back into `stream` with events (one side stream per
+ * device, created on first use). Work enqueued on `stream` afterwards sees all three;
+ * the fork/join is CUDA-graph capturable. */
 hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                       const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
                       int B, int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream);

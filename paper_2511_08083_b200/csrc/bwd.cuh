@@ -17,6 +17,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdio>
+#include <mutex>
 
 #include "../../include/hk_attn.h"
 #include "ptx.cuh"
@@ -864,6 +865,22 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ---------------------------------------------------------------- host launch
+#ifndef HK_BWD_FORK
+#define HK_BWD_FORK 1
+#endif
+// One non-blocking side stream per device for the forked dQ pass (created on first use, never
+// destroyed; the library otherwise keeps no state between calls).
+inline cudaStream_t side_stream() {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
+    streams[dev] = nullptr;
+  return streams[dev];
+}
+
 template <typename F>
 inline bool set_smem(F* fn, uint32_t bytes) {
   return cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -935,7 +952,20 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     bwd_pre_kernel<D><<<dim3((unsigned)bx, (unsigned)B), 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(O), reinterpret_cast<const __nv_bfloat16*>(dO), LSE, Dv, lse2, g, Hq,
         Np, sched);
-  // B1, B2
+  // B1, B2. They are independent (both only read the preprocess output): with HK_BWD_FORK the dQ
+  // pass goes on a side stream forked from `stream` after B0 and joined back after it, so its
+  // CTAs take the SMs the dK/dV pass's last CTAs free instead of waiting for the whole pass.
+  cudaStream_t s2 = stream;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (HK_BWD_FORK && phase < 0) {
+    s2 = side_stream();
+    if (s2 && cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventRecord(ev_fork, stream) == cudaSuccess && cudaStreamWaitEvent(s2, ev_fork, 0) == cudaSuccess) {
+    } else {
+      s2 = stream;  // no side stream: serial launches on `stream`
+    }
+  }
   if (phase < 0 || phase == 1) {
     const int items = B * Hkv * (Npk / 128);  // persistent: one CTA per SM
     bwd_dkdv_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS, C::SMEM1, stream>>>(mQ, mdO, mK,
@@ -943,8 +973,14 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   }
   if (phase < 0 || phase == 2) {
     const int items = B * Hq * (Np / 128);  // persistent: one CTA per SM
-    bwd_dq_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS, C::SMEM2, stream>>>(mQ, mdO, mK, mV, p);
+    bwd_dq_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS, C::SMEM2, s2>>>(mQ, mdO, mK, mV, p);
   }
+  if (s2 != stream) {
+    cudaEventRecord(ev_join, s2);
+    cudaStreamWaitEvent(stream, ev_join, 0);
+  }
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(err, errlen, "hk_attn_bwd launch failed: %s", cudaGetErrorString(e));

@@ -39,3 +39,37 @@ def test_batch_shard_bitwise(d, causal):
     torch.cuda.synchronize()
     for a, b in zip(*outs):
         assert torch.equal(a[2:4], b)
+
+
+def test_cuda_graph_capture_fwd_bwd():
+    """fwd + bwd (whose dQ pass forks onto the library's side stream and joins back)
+    captured into a CUDA graph and replayed: bitwise the eager results."""
+    from paper_2511_08083_b200 import attn_bwd, attn_fwd, bwd_workspace_bytes
+    B, N, Hq, Hkv, d, causal = 2, 640, 8, 2, 128, True
+    x = make_inputs(B, N, Hq, Hkv, d, seed=31, device="cuda")
+    o = torch.empty_like(x["Q"])
+    lse = torch.empty((B, Hq, N), dtype=torch.float32, device="cuda")
+    g3 = [torch.empty_like(x[n]) for n in ("Q", "K", "V")]
+    ws = torch.empty(bwd_workspace_bytes(B, Hq, Hkv, N, d) // 4, dtype=torch.float32, device="cuda")
+
+    def step():
+        attn_fwd(x["Q"], x["K"], x["V"], causal, out=o, lse=lse)
+        attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, workspace=ws, dq=g3[0], dk=g3[1], dv=g3[2])
+
+    step()
+    torch.cuda.synchronize()
+    eager = [t.clone() for t in (o, lse, *g3)]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()  # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    for t in (o, lse, *g3):
+        t.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, (o, lse, *g3)):
+        assert torch.equal(a, b)
