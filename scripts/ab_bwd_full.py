@@ -1,5 +1,8 @@
+"""Interleaved A/B of the full public hk_attn_bwd (preprocess + dK/dV + dQ, including the
+dQ fork) between two library builds: python scripts/ab_bwd_full.py libA.so libB.so C3,C5-1024-c"""
 import sys, os, ctypes, torch, json, statistics
-sys.path.insert(0, '/root/repo/scripts'); sys.path.insert(0, '/root/repo')
+_root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(_root, 'scripts')); sys.path.insert(0, _root)
 from probe import CONFIGS
 from paper_2511_08083_b200.inputs import make_inputs
 def load(path):

@@ -2,7 +2,7 @@
 batch through the varlen entry point (uniform lengths) with the static and the dynamic
 scheduler. Prints min-of-3 ms per variant."""
 import sys, torch, json
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from paper_2511_08083_b200 import attn_fwd, attn_fwd_varlen
 from paper_2511_08083_b200.inputs import make_inputs
 def timed(fn, iters=10, warm=3):
