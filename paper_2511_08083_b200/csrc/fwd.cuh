@@ -53,7 +53,10 @@ struct FwdCfg {
 #endif
   static constexpr bool SPLIT_P = (D == 64) && HK_FWD_SPLIT64;
   static constexpr uint32_t TILE_BYTES = 128 * D * 2;  // one 128-row tile
-  static constexpr int NS = (D == 128) ? 2 : 4;        // K/V ring depth
+#ifndef HK_FWD_NS64
+#define HK_FWD_NS64 4
+#endif
+  static constexpr int NS = (D == 128) ? 2 : HK_FWD_NS64;  // K/V ring depth
   static constexpr uint32_t SMEM = 2 * TILE_BYTES + 2 * NS * TILE_BYTES + 1024;
   static constexpr int THREADS = 384;
 #ifndef HK_FWD_EMU128
