@@ -136,6 +136,13 @@ struct BwdCfg {
   // B2: ring A = {K_j}, ring B = {Q_i, dO_i, V_j ...} (NSB + 2 slots)
   static constexpr uint32_t SMEM2 = 2 * T128 + (NSA + NSB) * T128 + 1024;
   static constexpr int THREADS = 320;  // 8 elementwise warps + TMA warp + MMA warp
+  // dK/dV pass: elementwise warpgroups (HK_DKDV_4WG: 4 at d=64, 32 query columns each, to hide
+  // the per-phase latency that bounds the d=64 pass; 2 otherwise)
+#ifndef HK_DKDV_4WG
+#define HK_DKDV_4WG 1
+#endif
+  static constexpr int NWG1 = (D == 64 && HK_DKDV_4WG) ? 4 : 2;
+  static constexpr int THREADS1 = 32 * (4 * NWG1 + 2);
 };
 
 // SMEM descriptor helpers for [rows][D] bf16 tiles stored as D/64 panels of rows x 128 B.
@@ -180,6 +187,27 @@ __device__ __forceinline__ void tmem_st_packed64(uint32_t taddr, const float (&v
   tmem_st32(taddr, pk);
 }
 
+// CW fp32 TMEM columns of this thread's lane -> registers, and CW values packed to bf16 pairs
+// back into CW/2 columns (CW = 64: two warpgroups per block, 32: four).
+template <int CW>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[CW]) {
+  if constexpr (CW == 64)
+    tmem_ld64(taddr, v);
+  else
+    tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+}
+template <int CW>
+__device__ __forceinline__ void tmem_st_packed_cols(uint32_t taddr, const float (&v)[CW]) {
+  if constexpr (CW == 64) {
+    tmem_st_packed64(taddr, v);
+  } else {
+    uint32_t pk[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) pk[c] = pack_bf16(v[2 * c], v[2 * c + 1]);
+    tmem_st16(taddr, pk);
+  }
+}
+
 // ---------------------------------------------------------------- B1: dK, dV
 // Persistent: one CTA per SM draws work items (key tile jt, kvh, b) from the
 // dynamic scheduler (items numbered tiles fastest, heaviest first when causal;
@@ -218,7 +246,7 @@ __device__ __forceinline__ KvItem kv_decode(const BwdParams& p, int item) {
 }
 
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
     bwd_dkdv_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapdO,
                     const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                     const BwdParams p) {
@@ -248,11 +276,14 @@ __global__ void __launch_bounds__(320, 1)
   static_assert((2 * NSA + 2 * NSB + 8) * 8 + sizeof(Sched) <= C::BAR_BYTES, "barrier area");
 
   const int warp = warp_id(), lane = lane_id();
+  constexpr int NWG = C::NWG1;            // elementwise warpgroups
+  constexpr int CW = 128 / NWG;           // query columns per elementwise thread
+  constexpr int WTMA = 4 * NWG, WMMA = 4 * NWG + 1;
   const int G = p.Hq / p.Hkv;
   const int num_items = p.B * p.Hkv * (p.Npk / 128);
 
   if (threadIdx.x == 0) {
-    sched_init(sched);
+    sched_init(sched, 1 + 4 * NWG);
     mbar_init(&bar_kv, 1);
     mbar_init(&bar_kvfree, 1);
     for (int s = 0; s < NSA; ++s) {
@@ -265,18 +296,18 @@ __global__ void __launch_bounds__(320, 1)
     }
     mbar_init(&bar_s, 1);
     mbar_init(&bar_dp, 1);
-    mbar_init(&bar_p, 8);
-    mbar_init(&bar_ds, 8);
+    mbar_init(&bar_p, 4 * NWG);
+    mbar_init(&bar_ds, 4 * NWG);
     mbar_init(&bar_acc, 1);
     fence_barrier_init();
   }
-  if (warp == 8) {
+  if (warp == WTMA) {
     tma_prefetch(&mapQ);
     tma_prefetch(&mapdO);
     tma_prefetch(&mapK);
     tma_prefetch(&mapV);
   }
-  if (warp == 9) tmem_alloc<512>(&tmem_base_s);
+  if (warp == WMMA) tmem_alloc<512>(&tmem_base_s);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -284,7 +315,7 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t tdV = tb, tdK = tb + D, tS = tb + 2 * D, tP = tb + 2 * D + 128;
 
   // All roles walk the same items; ring uses and barrier phases run on across items.
-  if (warp == 8) {
+  if (warp == WTMA) {
     // ================= TMA producer =================
     if (lane == 0) {
       const uint64_t pol_keep = policy_evict_last();
@@ -334,7 +365,7 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == WMMA) {
     // ================= MMA issuer (whole warp, one elected lane issues) =================
     constexpr uint32_t idesc_sp = idesc_bf16(128, 128, 0, 0);  // S^T / dP^T: M=128 keys, N=128 queries
     constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);   // dV / dK: B = dO_i / Q_i MN-major
@@ -381,7 +412,10 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&bar_p, u & 1);
         tc_fence_after();
         hk_trace(10, u, 0);  // MMA: P^T(it) seen, dV issue
-        gemm_tsp_mn(tdV, tS, mnmaj(dO, 0), idesc_acc, acc);
+        if constexpr (NWG == 4)
+          gemm_tsp4_mn(tdV, tS, mnmaj(dO, 0), idesc_acc, acc);
+        else
+          gemm_tsp_mn(tdV, tS, mnmaj(dO, 0), idesc_acc, acc);
         if (more) {
           mbar_wait(&fullA[(u + 1) % NSA], ((u + 1) / NSA) & 1);
           tc_fence_after();
@@ -391,7 +425,10 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&bar_ds, u & 1);
         tc_fence_after();
         hk_trace(11, u, 0);  // MMA: dS^T(it) seen, dK issue
-        gemm_tsp_mn(tdK, tP, mnmaj(q, 0), idesc_acc, acc);
+        if constexpr (NWG == 4)
+          gemm_tsp4_mn(tdK, tP, mnmaj(q, 0), idesc_acc, acc);
+        else
+          gemm_tsp_mn(tdK, tP, mnmaj(q, 0), idesc_acc, acc);
         // Q(it) (last use dK) and dO/lse2/D(it) (last uses dV, the dS phase): free both
         tc_commit_w(&emptyA[u % NSA]);
         tc_commit_w(&emptyB[u % NSB]);
@@ -410,12 +447,16 @@ __global__ void __launch_bounds__(320, 1)
     drain_ring(emptyB, NSB, u0);
     if (busy > 0) mbar_wait(&bar_kvfree, (busy - 1) & 1);
   } else {
-    // ================= elementwise warpgroups (warps 0-7) =================
-    const int wg = warp >> 2;              // query columns [64 wg, 64 wg + 64) of each block
+    // ================= elementwise warpgroups (warps 0 .. 4 NWG - 1) =================
+    const int wg = warp >> 2;              // query columns [CW wg, CW wg + CW) of each block
     const uint32_t lb = (warp & 3) * 32;   // TMEM lane base
     const int r = (warp & 3) * 32 + lane;  // key row within the tile
     const float c = 1.4426950408889634f / sqrtf((float)D);
-    const uint32_t cS = tS + 64 * wg, cP = tP + 64 * wg;
+    const uint32_t cS = tS + CW * wg, cP = tP + CW * wg;
+    // epilogue columns: the first half of the warpgroups write dV, the second dK
+    constexpr int HALF = NWG / 2, ECOLS = D / HALF;
+    const bool is_dk = wg >= HALF;
+    const int ecol0 = (wg % HALF) * ECOLS;
     int u = 0, s = 0;  // blocks so far; ring B slot of block u
     uint32_t acc_ph = 0;
     for (int rr = 0;; ++rr) {
@@ -424,11 +465,12 @@ __global__ void __launch_bounds__(320, 1)
       const KvItem w = kv_decode<CAUSAL>(p, item);
       const int key = w.jt * 128 + r;
       const bool key_ok = key < w.sq.lk;  // key rows of a ragged last tile beyond the sequence are not stored
-      __nv_bfloat16* out = (wg == 0 ? p.dv : p.dk) + ((size_t)(w.sq.gk0 + (key_ok ? key : 0)) * p.Hkv + w.kvh) * D;
+      __nv_bfloat16* out =
+          (is_dk ? p.dk : p.dv) + ((size_t)(w.sq.gk0 + (key_ok ? key : 0)) * p.Hkv + w.kvh) * D + ecol0;
       if (w.n_it == 0) {  // no query sees these keys: dK = dV = 0
         if (key_ok) {
 #pragma unroll
-          for (int k = 0; k < D / 8; ++k) reinterpret_cast<uint4*>(out)[k] = make_uint4(0u, 0u, 0u, 0u);
+          for (int k = 0; k < ECOLS / 8; ++k) reinterpret_cast<uint4*>(out)[k] = make_uint4(0u, 0u, 0u, 0u);
         }
         continue;
       }
@@ -437,20 +479,20 @@ __global__ void __launch_bounds__(320, 1)
       for (int it = 0; it < w.n_it; ++it, ++u) {
         const uint8_t* vec = sB + s * C::SLOT_B1 + C::T128;  // lse2 [128], then D [128]
         const uint32_t par = u & 1;
-        float v[64];
+        float v[CW];
         // ---- phase 1: P^T = exp2(c S^T - LSE2) (masked), bf16 into TMEM for dV += P^T dO
         if (threadIdx.x == 0) hk_trace(1, u, 0);
         mbar_wait(&fullB[s], (u / NSB) & 1);  // lse2/D ride with dO in ring B: landed?
         mbar_wait(&bar_s, par);
         tc_fence_after();
         if (threadIdx.x == 0) hk_trace(2, u, 0);
-        tmem_ld64(tmem_addr(cS, lb, 0), v);
+        tmem_ld_cols<CW>(tmem_addr(cS, lb, 0), v);
         tmem_wait_ld();
-        const int q0 = qi * 128 + 64 * wg;
+        const int q0 = qi * 128 + CW * wg;
 #pragma unroll
-        for (int c4 = 0; c4 < 64; c4 += 4) {
+        for (int c4 = 0; c4 < CW; c4 += 4) {
           float l0, l1, l2, l3;
-          lds_v4(vec + 4 * (64 * wg + c4), l0, l1, l2, l3);
+          lds_v4(vec + 4 * (CW * wg + c4), l0, l1, l2, l3);
           const float2 xa = fma2(make_float2(v[c4], v[c4 + 1]), make_float2(c, c), make_float2(-l0, -l1));
           const float2 xb = fma2(make_float2(v[c4 + 2], v[c4 + 3]), make_float2(c, c), make_float2(-l2, -l3));
           const float2 ea = bwd_exp2_pair<BWD_EMU_OF_8>(xa, c4 / 2);
@@ -462,10 +504,10 @@ __global__ void __launch_bounds__(320, 1)
         }
         if (CAUSAL && qi * 128 + off < w.jt * 128 + 127) {
 #pragma unroll
-          for (int cc = 0; cc < 64; ++cc)
+          for (int cc = 0; cc < CW; ++cc)
             if (q0 + cc + off < key) v[cc] = 0.f;  // key > query + (lk - lq) is masked
         }
-        tmem_st_packed64(tmem_addr(cS, lb, 0), v);
+        tmem_st_packed_cols<CW>(tmem_addr(cS, lb, 0), v);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -475,13 +517,13 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&bar_dp, par);
         tc_fence_after();
         if (threadIdx.x == 0) hk_trace(4, u, 0);
-        float dp[64];
-        tmem_ld64(tmem_addr(cP, lb, 0), dp);
+        float dp[CW];
+        tmem_ld_cols<CW>(tmem_addr(cP, lb, 0), dp);
         tmem_wait_ld();
 #pragma unroll
-        for (int c4 = 0; c4 < 64; c4 += 4) {  // packed f32x2: half the issue slots of scalar FADD + FMUL
+        for (int c4 = 0; c4 < CW; c4 += 4) {  // packed f32x2: half the issue slots of scalar FADD + FMUL
           float d0, d1, d2, d3;
-          lds_v4(vec + 512 + 4 * (64 * wg + c4), d0, d1, d2, d3);
+          lds_v4(vec + 512 + 4 * (CW * wg + c4), d0, d1, d2, d3);
           const float2 a = mul2(make_float2(v[c4], v[c4 + 1]),
                                 sub2(make_float2(dp[c4], dp[c4 + 1]), make_float2(d0, d1)));
           const float2 b = mul2(make_float2(v[c4 + 2], v[c4 + 3]),
@@ -491,7 +533,7 @@ __global__ void __launch_bounds__(320, 1)
           dp[c4 + 2] = b.x;
           dp[c4 + 3] = b.y;
         }
-        tmem_st_packed64(tmem_addr(cP, lb, 0), dp);
+        tmem_st_packed_cols<CW>(tmem_addr(cP, lb, 0), dp);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -504,10 +546,10 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(&bar_acc, acc_ph);
       acc_ph ^= 1;
       tc_fence_after();
-      const float scale = wg == 0 ? 1.f : rsqrtf((float)D);
-      const uint32_t tacc = wg == 0 ? tdV : tdK;
+      const float scale = is_dk ? rsqrtf((float)D) : 1.f;
+      const uint32_t tacc = (is_dk ? tdK : tdV) + ecol0;
 #pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 32) {
+      for (int c0 = 0; c0 < ECOLS; c0 += 32) {
         uint32_t o[32];
         tmem_ld32(tmem_addr(tacc, lb, c0), o);
         tmem_wait_ld();
@@ -526,7 +568,7 @@ __global__ void __launch_bounds__(320, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc<512>(tb);
+  if (warp == WMMA) tmem_dealloc<512>(tb);
   if (threadIdx.x == 0) sched_exit(p.sched);
 }
 
@@ -968,7 +1010,7 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   }
   if (phase < 0 || phase == 1) {
     const int items = B * Hkv * (Npk / 128);  // persistent: one CTA per SM
-    bwd_dkdv_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS, C::SMEM1, stream>>>(mQ, mdO, mK,
+    bwd_dkdv_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS1, C::SMEM1, stream>>>(mQ, mdO, mK,
                                                                                                     mV, p);
   }
   if (phase < 0 || phase == 2) {

@@ -419,6 +419,16 @@ __device__ __forceinline__ void gemm_ts_mn_hi(uint32_t d, uint32_t a_tmem, uint6
                "r"(a_tmem + 32), "l"(b + 512), "r"(idesc), "r"(1u)
                : "memory");
 }
+// A from TMEM packed by four warpgroups (warpgroup w owns score columns [32w, 32w+32) and packs
+// its 32 queries into the first 16 of them: queries 16kk.. at column 32(kk/2) + 8(kk%2)),
+// B MN-major SW128, K = 128 (the d=64 dK/dV pass with 4 elementwise warpgroups)
+__device__ __forceinline__ void gemm_tsp4_mn(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(HK_MMA_HEAD HK_TS_FIRST HK_TS_STEP(8, 128) HK_TS_STEP(32, 256) HK_TS_STEP(40, 384)
+                   HK_TS_STEP(64, 512) HK_TS_STEP(72, 640) HK_TS_STEP(96, 768) HK_TS_STEP(104, 896) "}" ::"r"(d),
+               "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+               : "memory");
+}
 // A from TMEM packed by two warpgroups (columns 16kk.. at kk*8 for kk<4, 64+(kk-4)*8 after),
 // B MN-major SW128, K = 128 (dV += P^T dO, dK += dS^T Q, dQ += dS K)
 __device__ __forceinline__ void gemm_tsp_mn(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
