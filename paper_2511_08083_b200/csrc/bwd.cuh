@@ -143,6 +143,12 @@ struct BwdCfg {
 #endif
   static constexpr int NWG1 = (D == 64 && HK_DKDV_4WG) ? 4 : 2;
   static constexpr int THREADS1 = 32 * (4 * NWG1 + 2);
+  // dQ pass: the same at d=64 (HK_DQ_4WG): 4 elementwise warpgroups of 32 key columns
+#ifndef HK_DQ_4WG
+#define HK_DQ_4WG 1
+#endif
+  static constexpr int NWG2 = (D == 64 && HK_DQ_4WG) ? 4 : 2;
+  static constexpr int THREADS2 = 32 * (4 * NWG2 + 2);
 };
 
 // SMEM descriptor helpers for [rows][D] bf16 tiles stored as D/64 panels of rows x 128 B.
@@ -614,7 +620,7 @@ __device__ __forceinline__ DqItem dq_decode(const BwdParams& p, int item) {
 }
 
 template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(BwdCfg<D>::THREADS2, 1)
     bwd_dq_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapdO,
                   const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                   const BwdParams p) {
@@ -634,11 +640,14 @@ __global__ void __launch_bounds__(320, 1)
   __shared__ uint32_t tmem_base_s;
 
   const int warp = warp_id(), lane = lane_id();
+  constexpr int NWG = C::NWG2;            // elementwise warpgroups
+  constexpr int CW = 128 / NWG;           // key columns per elementwise thread
+  constexpr int WTMA = 4 * NWG, WMMA = 4 * NWG + 1;
   const int num_items = p.B * p.Hq * (p.Np / 128);
   unsigned* const ctr = p.sched + 2;
 
   if (threadIdx.x == 0) {
-    sched_init(sched);
+    sched_init(sched, 1 + 4 * NWG);
     mbar_init(&bar_qa, 8);
     for (int s = 0; s < NSA; ++s) {
       mbar_init(&fullA[s], 1);
@@ -649,19 +658,19 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&emptyB[s], 1);
     }
     mbar_init(&bar_s, 1);
-    mbar_init(&bar_sfree, 8);
+    mbar_init(&bar_sfree, 4 * NWG);
     mbar_init(&bar_dp, 1);
-    mbar_init(&bar_ds, 8);
+    mbar_init(&bar_ds, 4 * NWG);
     mbar_init(&bar_acc, 1);
     fence_barrier_init();
   }
-  if (warp == 8) {
+  if (warp == WTMA) {
     tma_prefetch(&mapQ);
     tma_prefetch(&mapdO);
     tma_prefetch(&mapK);
     tma_prefetch(&mapV);
   }
-  if (warp == 9) tmem_alloc<512>(&tmem_base_s);
+  if (warp == WMMA) tmem_alloc<512>(&tmem_base_s);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -669,7 +678,7 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t tdQ = tb, tS = tb + D, tP = tb + D + 128, tQa = tb + D + 256, tdOa = tQa + D / 2;
 
   // All roles walk the same items; ring uses and barrier phases run on across items.
-  if (warp == 8) {
+  if (warp == WTMA) {
     if (lane == 0) {
       const uint64_t pol_keep = policy_evict_last();
       const uint64_t pol_stream = policy_evict_normal();
@@ -707,7 +716,7 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == WMMA) {
     // ================= MMA issuer (whole warp, one elected lane issues) =================
     constexpr uint32_t idesc_sp = idesc_bf16(128, 128, 0, 0);  // S / dP: A (Q/dO) from TMEM, B K-major
     constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);   // dQ += dS K_j: K_j MN-major
@@ -759,7 +768,10 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&bar_ds, g & 1);
         tc_fence_after();
         hk_trace(11, g, 1);  // MMA: dS(it) seen, dQ issue
-        gemm_tsp_mn(tdQ, tP, mnmaj(aA + ((a0 + it) % NSA) * C::T128, 0), idesc_acc, it > 0 ? 1u : 0u);
+        if constexpr (NWG == 4)
+          gemm_tsp4_mn(tdQ, tP, mnmaj(aA + ((a0 + it) % NSA) * C::T128, 0), idesc_acc, it > 0 ? 1u : 0u);
+        else
+          gemm_tsp_mn(tdQ, tP, mnmaj(aA + ((a0 + it) % NSA) * C::T128, 0), idesc_acc, it > 0 ? 1u : 0u);
         tc_commit_w(&emptyA[(a0 + it) % NSA]);  // K(it): last use dQ(it)
         if (more) {  // dP(it+1) overwrites dS(it): after dQ(it) in issue order
           const int u = v0 + it + 1;
@@ -776,15 +788,17 @@ __global__ void __launch_bounds__(320, 1)
     drain_ring(emptyA, NSA, ua);
     drain_ring(emptyB, NB, ub);
   } else {
-    const int wg = warp >> 2;              // key columns [64 wg, 64 wg + 64) of each block
+    const int wg = warp >> 2;              // key columns [CW wg, CW wg + CW) of each block
     const uint32_t lb = (warp & 3) * 32;
     const int r = (warp & 3) * 32 + lane;  // query row within the tile
     const float c = 1.4426950408889634f / sqrtf((float)D);
-    const uint32_t cP = tP + 64 * wg, cS = tS + 64 * wg;
+    const uint32_t cP = tP + CW * wg, cS = tS + CW * wg;
+    constexpr int QC = D / NWG;  // dQ columns each warpgroup stores
     uint32_t g = 0, acc_ph = 0;
     int ub = 0;  // ring B uses so far (Q_i of the current item sits at ub, dO_i at ub + 1)
     // WG0 copies Q_i, WG1 dO_i from swizzled SMEM rows into TMEM (A operands)
     auto copy_in = [&]() {
+      if (wg >= 2) return;  // WG0 copies Q_i, WG1 dO_i; the others have no copy
       const int u = ub + wg;
       mbar_wait(&fullB[u % NB], (u / NB) & 1);
       const uint8_t* src = sB + (u % NB) * C::T128;
@@ -813,11 +827,11 @@ __global__ void __launch_bounds__(320, 1)
       const DqItem w = dq_decode<CAUSAL>(p, item);
       const int q = w.iq * 128 + r;
       const bool q_ok = q < w.sq.lq;  // query rows of a ragged last tile beyond the sequence are not stored
-      __nv_bfloat16* out = p.dq + ((size_t)(w.sq.gq0 + (q_ok ? q : 0)) * p.Hq + w.h) * D + wg * (D / 2);
+      __nv_bfloat16* out = p.dq + ((size_t)(w.sq.gq0 + (q_ok ? q : 0)) * p.Hq + w.h) * D + wg * QC;
       if (w.n_it == 0) {  // no key visible to these rows: dQ = 0
         if (q_ok) {
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) reinterpret_cast<uint4*>(out)[k] = make_uint4(0u, 0u, 0u, 0u);
+          for (int k = 0; k < QC / 8; ++k) reinterpret_cast<uint4*>(out)[k] = make_uint4(0u, 0u, 0u, 0u);
         }
         item = sched_take(sched, rr);
         if (busy(item)) copy_in();
@@ -827,18 +841,18 @@ __global__ void __launch_bounds__(320, 1)
       const size_t vrow = ((size_t)w.b * p.Hq + w.h) * p.Np + q;
       const float l2 = p.lse2[vrow], Dq = p.Dv[vrow];
       for (int it = 0; it < w.n_it; ++it, ++g) {
-        float v[64];
+        float v[CW];
         if (threadIdx.x == 0) hk_trace(1, g, 1);
         mbar_wait(&bar_s, g & 1);
         tc_fence_after();
         if (threadIdx.x == 0) hk_trace(2, g, 1);
-        tmem_ld64(tmem_addr(cS, lb, 0), v);
+        tmem_ld_cols<CW>(tmem_addr(cS, lb, 0), v);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_sfree);  // S buffer free for S(it+1)
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
+        for (int k = 0; k < CW / 2; ++k) {
           const float2 e = bwd_exp2_pair<BWD_EMU_OF_8>(
               fma2(make_float2(v[2 * k], v[2 * k + 1]), make_float2(c, c), make_float2(-l2, -l2)), k);
           v[2 * k] = e.x;
@@ -847,27 +861,27 @@ __global__ void __launch_bounds__(320, 1)
         // keys beyond the sequence (ragged / varlen tail: K may hold the next
         // sequence's rows) and, when causal, keys > query + (lk - lq) are masked
         if ((it + 1) * 128 > w.sq.lk || (CAUSAL && it * 128 + 127 > w.iq * 128 + off)) {
-          const int k0 = it * 128 + 64 * wg;
+          const int k0 = it * 128 + CW * wg;
           const int klim = CAUSAL ? min(q + off, w.sq.lk - 1) : w.sq.lk - 1;
 #pragma unroll
-          for (int cc = 0; cc < 64; ++cc)
+          for (int cc = 0; cc < CW; ++cc)
             if (k0 + cc > klim) v[cc] = 0.f;
         }
         if (threadIdx.x == 0) hk_trace(3, g, 1);
         mbar_wait(&bar_dp, g & 1);
         tc_fence_after();
         if (threadIdx.x == 0) hk_trace(4, g, 1);
-        float dp[64];
-        tmem_ld64(tmem_addr(cP, lb, 0), dp);
+        float dp[CW];
+        tmem_ld_cols<CW>(tmem_addr(cP, lb, 0), dp);
         tmem_wait_ld();
 #pragma unroll
-        for (int cc = 0; cc < 64; cc += 2) {  // packed f32x2: half the issue slots of scalar FADD + FMUL
+        for (int cc = 0; cc < CW; cc += 2) {  // packed f32x2: half the issue slots of scalar FADD + FMUL
           const float2 r2 = mul2(make_float2(v[cc], v[cc + 1]),
                                  sub2(make_float2(dp[cc], dp[cc + 1]), make_float2(Dq, Dq)));
           dp[cc] = r2.x;
           dp[cc + 1] = r2.y;
         }
-        tmem_st_packed64(tmem_addr(cP, lb, 0), dp);
+        tmem_st_packed_cols<CW>(tmem_addr(cP, lb, 0), dp);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -875,14 +889,18 @@ __global__ void __launch_bounds__(320, 1)
         if (threadIdx.x == 0) hk_trace(5, g, 1);
       }
       ub += w.n_it + 2;
-      // ---- epilogue: dQ * (1/sqrt d); WG0 writes columns [0, D/2), WG1 [D/2, D)
+      // ---- epilogue: dQ * (1/sqrt d); warpgroup wg writes columns [QC wg, QC wg + QC)
       mbar_wait(&bar_acc, acc_ph);
       acc_ph ^= 1;
       tc_fence_after();
-      uint32_t o[D / 2];
+      uint32_t o[QC];
+      if constexpr (QC % 32 == 0) {
 #pragma unroll
-      for (int c0 = 0; c0 < D / 2; c0 += 32)
-        tmem_ld32(tmem_addr(tdQ, lb, wg * (D / 2) + c0), *reinterpret_cast<uint32_t(*)[32]>(&o[c0]));
+        for (int c0 = 0; c0 < QC; c0 += 32)
+          tmem_ld32(tmem_addr(tdQ, lb, wg * QC + c0), *reinterpret_cast<uint32_t(*)[32]>(&o[c0]));
+      } else {
+        tmem_ld16(tmem_addr(tdQ, lb, wg * QC), o);
+      }
       tmem_wait_ld();
       // the next item's Q/dO go into TMEM before dQ is stored: its S/dP start now.
       // (Its dQ MMAs, which overwrite this accumulator, follow this WG's reads.)
@@ -890,7 +908,7 @@ __global__ void __launch_bounds__(320, 1)
       if (busy(item)) copy_in();
       const float scale = rsqrtf((float)D);
 #pragma unroll
-      for (int c0 = 0; c0 < D / 2; c0 += 8) {
+      for (int c0 = 0; c0 < QC; c0 += 8) {
         uint4 o4;
         o4.x = pack_bf16(__uint_as_float(o[c0 + 0]) * scale, __uint_as_float(o[c0 + 1]) * scale);
         o4.y = pack_bf16(__uint_as_float(o[c0 + 2]) * scale, __uint_as_float(o[c0 + 3]) * scale);
@@ -902,7 +920,7 @@ __global__ void __launch_bounds__(320, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc<512>(tb);
+  if (warp == WMMA) tmem_dealloc<512>(tb);
   if (threadIdx.x == 0) sched_exit(ctr);
 }
 
@@ -1015,7 +1033,8 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   }
   if (phase < 0 || phase == 2) {
     const int items = B * Hq * (Np / 128);  // persistent: one CTA per SM
-    bwd_dq_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS, C::SMEM2, s2>>>(mQ, mdO, mK, mV, p);
+    bwd_dq_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS2, C::SMEM2, s2>>>(mQ, mdO, mK, mV,
+                                                                                             p);
   }
   if (s2 != stream) {
     cudaEventRecord(ev_join, s2);
