@@ -141,13 +141,16 @@ struct BwdCfg {
 #ifndef HK_DKDV_4WG
 #define HK_DKDV_4WG 1
 #endif
-  static constexpr int NWG1 = (D == 64 && HK_DKDV_4WG) ? 4 : 2;
+#ifndef HK_BWD_4WG128
+#define HK_BWD_4WG128 0  // the same at d=128 (experiment)
+#endif
+  static constexpr int NWG1 = ((D == 64 && HK_DKDV_4WG) || (D == 128 && HK_BWD_4WG128)) ? 4 : 2;
   static constexpr int THREADS1 = 32 * (4 * NWG1 + 2);
   // dQ pass: the same at d=64 (HK_DQ_4WG): 4 elementwise warpgroups of 32 key columns
 #ifndef HK_DQ_4WG
 #define HK_DQ_4WG 1
 #endif
-  static constexpr int NWG2 = (D == 64 && HK_DQ_4WG) ? 4 : 2;
+  static constexpr int NWG2 = ((D == 64 && HK_DQ_4WG) || (D == 128 && HK_BWD_4WG128)) ? 4 : 2;
   static constexpr int THREADS2 = 32 * (4 * NWG2 + 2);
 };
 
