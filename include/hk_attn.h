@@ -64,8 +64,10 @@ size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d);
  * (GQA group reduced inside the kernel) on `stream` and the dQ pass, which is
  * independent of it, on a library-owned non-blocking side stream forked from `stream`
  * after the preprocess and joined back into `stream` with events (one side stream per
- * device, created on first use). Work enqueued on `stream` afterwards sees all three;
- * the fork/join is CUDA-graph capturable. */
+ * device, created on first use — make the first backward call of a process outside
+ * CUDA-graph capture; if the stream cannot be created the kernels run serially on
+ * `stream`). Work enqueued on `stream` afterwards sees all three; the fork/join is
+ * CUDA-graph capturable. */
 hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                       const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
                       int B, int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream);

@@ -939,8 +939,10 @@ inline cudaStream_t side_stream() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lk(mu);
-  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
+  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
     streams[dev] = nullptr;
+    (void)cudaGetLastError();  // fall back to serial launches without leaving a sticky error behind
+  }
   return streams[dev];
 }
 
@@ -1027,6 +1029,7 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
         cudaEventRecord(ev_fork, stream) == cudaSuccess && cudaStreamWaitEvent(s2, ev_fork, 0) == cudaSuccess) {
     } else {
       s2 = stream;  // no side stream: serial launches on `stream`
+      (void)cudaGetLastError();
     }
   }
   if (phase < 0 || phase == 1) {
