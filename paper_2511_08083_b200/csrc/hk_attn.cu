@@ -556,6 +556,16 @@ hk_status hk_rope(const void* x, const float* cos, const float* sin, void* out, 
   q.N = N;
   q.H = H;
   q.d = d;
+  // inputs beyond L2 (126 MB): the head-loop form loads each position's cos/sin once for all H
+  // heads (1.08-1.13x at 268 MB / 1 GB); smaller ones stay with one thread per (row, chunk)
+  // (the head loop leaves too few threads there: 0.91x at 67 MB). Same results either way.
+  if (bytes > ((size_t)126 << 20)) {
+    const size_t threads = (size_t)B * N * (d / 16);
+    size_t blocks = (threads + 255) / 256;
+    if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
+    hk::rope_hloop_kernel<<<(unsigned)blocks, 256, 0, stream>>>(q);
+    return launched("hk_rope");
+  }
   const size_t threads = q.rows * (d / 16);
   size_t blocks = (threads + 255) / 256;
   if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;

@@ -175,4 +175,50 @@ __global__ void __launch_bounds__(256) rope_kernel(const RopeParams p) {
   }
 }
 
+// Rotary, head-loop form (HK_ROPE_HLOOP): one thread per (b, n, 8-wide chunk) walks all H heads,
+// so the position's cos/sin chunk is loaded once instead of once per head (the per-head form
+// moves twice as many cos/sin bytes through L1 as x bytes).
+__global__ void __launch_bounds__(256) rope_hloop_kernel(const RopeParams p) {
+  const int half = p.d / 2, cpr = half / 8;
+  const size_t units = p.rows / p.H * cpr;  // (b, n) positions x chunks
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < units; t += (size_t)gridDim.x * blockDim.x) {
+    const size_t bn = t / cpr;
+    const int ch = (int)(t % cpr);
+    const int n = (int)(bn % p.N);
+    const float4* cp = reinterpret_cast<const float4*>(p.cos + (size_t)n * half + ch * 8);
+    const float4* sp = reinterpret_cast<const float4*>(p.sin + (size_t)n * half + ch * 8);
+    const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
+    const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const float s[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    constexpr int HG = 4;  // heads per group: their loads go out together
+    for (int h0 = 0; h0 < p.H; h0 += HG) {
+      uint4 va[HG], vb[HG];
+#pragma unroll
+      for (int u = 0; u < HG; ++u) {
+        if (h0 + u < p.H) {
+          const __nv_bfloat16* xr = p.x + (bn * p.H + h0 + u) * p.d;
+          va[u] = __ldcs(reinterpret_cast<const uint4*>(xr) + ch);
+          vb[u] = __ldcs(reinterpret_cast<const uint4*>(xr + half) + ch);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < HG; ++u) {
+        if (h0 + u < p.H) {
+          float a[8], b[8], lo[8], hi[8];
+          unpack8(va[u], a);
+          unpack8(vb[u], b);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            lo[e] = fmaf(a[e], c[e], -b[e] * s[e]);
+            hi[e] = fmaf(b[e], c[e], a[e] * s[e]);
+          }
+          __nv_bfloat16* orow = p.out + (bn * p.H + h0 + u) * p.d;
+          __stcs(reinterpret_cast<uint4*>(orow) + ch, pack8(lo));
+          __stcs(reinterpret_cast<uint4*>(orow + half) + ch, pack8(hi));
+        }
+      }
+    }
+  }
+}
+
 }  // namespace hk
