@@ -59,14 +59,18 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
   for (size_t base = gwarp * RPW * U; base < rows; base += nwarps * RPW * U) {
     uint4 a[U], gv[U];
     float L[U];  // LSE of the row (lane sub == 0), loaded with O / dO: not a dependent round trip later
+    int hh[U], nn[U];  // (h, n) of each row: one 32-bit division per row (rows * H < 2^31, validated)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const size_t row = base + u * RPW + lrow;
       L[u] = 0.f;
+      const uint32_t r32 = (uint32_t)row;
+      nn[u] = (int)(r32 / (uint32_t)H);
+      hh[u] = (int)(r32 - (uint32_t)nn[u] * (uint32_t)H);
       if (row < rows) {
         a[u] = __ldcs(reinterpret_cast<const uint4*>(O + (row0 + row) * D) + sub);
         gv[u] = __ldcs(reinterpret_cast<const uint4*>(dO + (row0 + row) * D) + sub);
-        if (sub == 0) L[u] = __ldg(lse + lse_index(g, sq, b, H, (int)(row % H), (int)(row / H)));
+        if (sub == 0) L[u] = __ldg(lse + lse_index(g, sq, b, H, hh[u], nn[u]));
       } else {
         a[u] = gv[u] = make_uint4(0u, 0u, 0u, 0u);
       }
@@ -86,8 +90,7 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
 #pragma unroll
       for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (row < rows && sub == 0) {
-        const int h = (int)(row % H), n = (int)(row / H);
-        const size_t idx = ((size_t)b * H + h) * Np + n;  // workspace rows are padded to Np
+        const size_t idx = ((size_t)b * H + hh[u]) * Np + nn[u];  // workspace rows are padded to Np
         Dout[idx] = acc;
         lse2[idx] = L[u] == -INFINITY ? INFINITY : L[u] * 1.4426950408889634f;
       }
