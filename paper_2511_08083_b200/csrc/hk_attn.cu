@@ -563,13 +563,19 @@ hk_status hk_rope(const void* x, const float* cos, const float* sin, void* out, 
     const size_t threads = (size_t)B * N * (d / 16);
     size_t blocks = (threads + 255) / 256;
     if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
-    hk::rope_hloop_kernel<<<(unsigned)blocks, 256, 0, stream>>>(q);
+    if (threads < ((size_t)1 << 31))
+      hk::rope_hloop_kernel<uint32_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
+    else
+      hk::rope_hloop_kernel<size_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
     return launched("hk_rope");
   }
   const size_t threads = q.rows * (d / 16);
   size_t blocks = (threads + 255) / 256;
   if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
-  hk::rope_kernel<<<(unsigned)blocks, 256, 0, stream>>>(q);
+  if (threads < ((size_t)1 << 31))
+    hk::rope_kernel<uint32_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
+  else
+    hk::rope_kernel<size_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
   return launched("hk_rope");
 }
 

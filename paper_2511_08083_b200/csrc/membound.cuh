@@ -147,13 +147,16 @@ struct RopeParams {
 
 // One thread per (row, 8-wide chunk of the first half): it loads the matching
 // chunks of both halves (16 B each) and the 8 cos/sin values of its position.
+// I: index type of the chunk counter — uint32_t when the chunk count fits (32-bit divisions;
+// 64-bit ones compile to a long subroutine and made the memory-bound kernels ALU-bound).
+template <typename I>
 __global__ void __launch_bounds__(256) rope_kernel(const RopeParams p) {
   const int half = p.d / 2, cpr = half / 8;  // chunks per row
-  const size_t total = p.rows * cpr;
-  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
-    const size_t row = t / cpr;
-    const int ch = (int)(t % cpr);
-    const int n = (int)((row / p.H) % p.N);
+  const I total = (I)(p.rows * cpr);
+  for (I t = (I)(blockIdx.x * blockDim.x + threadIdx.x); t < total; t += (I)(gridDim.x * blockDim.x)) {
+    const I row = t / (I)cpr;
+    const int ch = (int)(t - row * (I)cpr);
+    const int n = (int)((row / (I)p.H) % (I)p.N);
     const __nv_bfloat16* xr = p.x + row * p.d;
     float a[8], b[8], c[8], s[8];
     unpack8(__ldcs(reinterpret_cast<const uint4*>(xr) + ch), a);
@@ -178,13 +181,14 @@ __global__ void __launch_bounds__(256) rope_kernel(const RopeParams p) {
 // Rotary, head-loop form (HK_ROPE_HLOOP): one thread per (b, n, 8-wide chunk) walks all H heads,
 // so the position's cos/sin chunk is loaded once instead of once per head (the per-head form
 // moves twice as many cos/sin bytes through L1 as x bytes).
+template <typename I>
 __global__ void __launch_bounds__(256) rope_hloop_kernel(const RopeParams p) {
   const int half = p.d / 2, cpr = half / 8;
-  const size_t units = p.rows / p.H * cpr;  // (b, n) positions x chunks
-  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < units; t += (size_t)gridDim.x * blockDim.x) {
-    const size_t bn = t / cpr;
-    const int ch = (int)(t % cpr);
-    const int n = (int)(bn % p.N);
+  const I units = (I)(p.rows / p.H * cpr);  // (b, n) positions x chunks
+  for (I t = (I)(blockIdx.x * blockDim.x + threadIdx.x); t < units; t += (I)(gridDim.x * blockDim.x)) {
+    const size_t bn = t / (I)cpr;
+    const int ch = (int)(t - (I)bn * (I)cpr);
+    const int n = (int)((I)bn % (I)p.N);
     const float4* cp = reinterpret_cast<const float4*>(p.cos + (size_t)n * half + ch * 8);
     const float4* sp = reinterpret_cast<const float4*>(p.sin + (size_t)n * half + ch * 8);
     const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);

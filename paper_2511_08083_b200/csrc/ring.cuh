@@ -34,7 +34,18 @@ __global__ void __launch_bounds__(256) attn_merge_kernel(const MergeParams p) {
     size_t li = 0;
     float wa = 0.f, wb = 1.f, L = 0.f;
     if (ok) {
-      const size_t h = row % p.H, n = (row / p.H) % p.N, b = row / ((size_t)p.H * p.N);
+      // 32-bit divisions when the row count fits (64-bit ones are a long subroutine)
+      size_t h, n, b;
+      if (rows < ((size_t)1 << 31)) {
+        const uint32_t r32 = (uint32_t)row, q = r32 / (uint32_t)p.H;
+        h = r32 - q * (uint32_t)p.H;
+        n = q % (uint32_t)p.N;
+        b = q / (uint32_t)p.N;
+      } else {
+        h = row % p.H;
+        n = (row / p.H) % p.N;
+        b = row / ((size_t)p.H * p.N);
+      }
       li = (b * p.H + h) * p.N + n;
       const float lb = p.lse_part[li];
       if (p.init) {
