@@ -55,7 +55,10 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
 #ifndef HK_PRE_U128
 #define HK_PRE_U128 2
 #endif
-  constexpr int U = D == 128 ? HK_PRE_U128 : 4;  // measured (scripts/ab.py): d=128 best at 2, d=64 at 4
+#ifndef HK_PRE_U64
+#define HK_PRE_U64 2
+#endif
+  constexpr int U = D == 128 ? HK_PRE_U128 : HK_PRE_U64;  // measured (scripts/ab.py): 2 for both since the 32-bit (h, n) division
   for (size_t base = gwarp * RPW * U; base < rows; base += nwarps * RPW * U) {
     uint4 a[U], gv[U];
     float L[U];  // LSE of the row (lane sub == 0), loaded with O / dO: not a dependent round trip later
