@@ -63,11 +63,13 @@ size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d);
  * (bf16, fully overwritten). Runs three kernels: D-preprocess, then the dK/dV pass
  * (GQA group reduced inside the kernel) on `stream` and the dQ pass, which is
  * independent of it, on a library-owned non-blocking side stream forked from `stream`
- * after the preprocess and joined back into `stream` with events (one side stream per
- * device, created on first use — make the first backward call of a process outside
- * CUDA-graph capture; if the stream cannot be created the kernels run serially on
- * `stream`). Work enqueued on `stream` afterwards sees all three; the fork/join is
- * CUDA-graph capturable. */
+ * after the preprocess and joined back into `stream` with events. There is one side
+ * stream per (device, caller stream), created on first use with the caller stream's
+ * priority, so concurrent backward calls on different streams stay independent — make
+ * the first backward call on a given stream outside CUDA-graph capture; if the side
+ * stream cannot be created (or more than 256 caller streams were seen) the kernels
+ * run serially on `stream`. Work enqueued on `stream` afterwards sees all three; the
+ * fork/join is CUDA-graph capturable. */
 hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                       const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
                       int B, int Hq, int Hkv, int N, int d, int causal, cudaStream_t stream);
@@ -102,8 +104,10 @@ hk_status hk_attn_bwd_qk(const void* Q, const void* K, const void* V, const void
  *   max_seqlen_q / max_seqlen_k : >= every sequence's length (sizes the grid).
  * total_q, total_k, max_seqlen_* >= 1. The cu_seqlens contents live on the
  * device and are NOT validated (that would need a host sync): offsets that
- * break the contract give undefined results, and rows beyond a sequence's
- * max_seqlen are not computed. A query sequence with no keys gets O = 0,
+ * break the contract give undefined results. Each sequence's lengths are
+ * clamped to [0, max_seqlen] on the device, so query rows / keys beyond a
+ * sequence's max_seqlen are not computed (their output rows are left
+ * untouched) and the backward never indexes past its padded workspace. A query sequence with no keys gets O = 0,
  * LSE = -inf, dQ = 0; keys no query sees get dK = dV = 0. */
 /* workspace: NULL (the forward's CTAs take work items in a static order) or >= 256 bytes of
  * device memory, 16-B aligned, for the dynamic scheduler's counters (CTAs draw items from a

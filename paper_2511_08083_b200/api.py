@@ -31,6 +31,18 @@ def _check_tensor(name, t, dtype=torch.bfloat16):
         raise ValueError(f"{name} must live on the current CUDA device")
 
 
+def _expect_shape(name, t, shape):
+    """Caller-supplied buffers reach the C ABI as raw pointers, so their sizes are checked here."""
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+def _check_workspace(ws, nbytes):
+    _check_tensor("workspace", ws, torch.float32)
+    if ws.numel() * ws.element_size() < nbytes:
+        raise ValueError(f"workspace must hold >= {nbytes} bytes, got {ws.numel() * ws.element_size()}")
+
+
 def _shapes(q, k, v):
     """Returns B, Nq, Nk, Hq, Hkv, d (Nq != Nk allowed: bottom-right causal, hk_attn.h)."""
     if q.dim() != 4 or k.dim() != 4 or v.shape != k.shape:
@@ -52,6 +64,8 @@ def attn_fwd(q, k, v, causal: bool = False, out=None, lse=None):
     L = torch.empty((B, Hq, N), dtype=torch.float32, device=q.device) if lse is None else lse
     _check_tensor("out", o)
     _check_tensor("lse", L, torch.float32)
+    _expect_shape("out", o, q.shape)
+    _expect_shape("lse", L, (B, Hq, N))
     if N == Nk:
         check(lib().hk_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, Hq, Hkv, N, d, int(bool(causal)),
                                 _stream()))
@@ -74,11 +88,18 @@ def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None,
         _check_tensor(n, t)
     _check_tensor("lse", lse, torch.float32)
     B, N, Nk, Hq, Hkv, d = _shapes(q, k, v)
+    _expect_shape("o", o, q.shape)
+    _expect_shape("do", do, q.shape)
+    _expect_shape("lse", lse, (B, Hq, N))
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
+    for n, t, ref in (("dq", dq, q), ("dk", dk, k), ("dv", dv, v)):
+        _check_tensor(n, t)
+        _expect_shape(n, t, ref.shape)
     nbytes = bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk)
     ws = torch.empty(nbytes // 4, dtype=torch.float32, device=q.device) if workspace is None else workspace
+    _check_workspace(ws, nbytes)
     if N == Nk:
         check(lib().hk_attn_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
                                 _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), B, Hq, Hkv, N, d,
@@ -130,9 +151,13 @@ def attn_fwd_varlen(q, k, v, cu_seqlens_q, cu_seqlens_k, max_seqlen_q: int, max_
     L = torch.empty((Hq, tq), dtype=torch.float32, device=q.device) if lse is None else lse
     _check_tensor("out", o)
     _check_tensor("lse", L, torch.float32)
+    _expect_shape("out", o, q.shape)
+    _expect_shape("lse", L, (Hq, tq))
     ws = None
     if dynamic:
         ws = torch.empty(64, dtype=torch.int32, device=q.device) if workspace is None else workspace
+        if not ws.is_cuda or not ws.is_contiguous() or ws.numel() * ws.element_size() < 256:
+            raise ValueError("workspace must be a contiguous CUDA tensor of >= 256 bytes")
     check(lib().hk_attn_fwd_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), _ptr(cu_seqlens_q),
                                    _ptr(cu_seqlens_k), B, Hq, Hkv, tq, tk, int(max_seqlen_q), int(max_seqlen_k), d,
                                    int(bool(causal)), _ptr(ws) if ws is not None else None,
@@ -146,12 +171,18 @@ def attn_bwd_varlen(q, k, v, o, lse, do, cu_seqlens_q, cu_seqlens_k, max_seqlen_
     B, tq, tk, Hq, Hkv, d = _varlen_args(q, k, v, cu_seqlens_q, cu_seqlens_k)
     for n, t in (("o", o), ("do", do)):
         _check_tensor(n, t)
+        _expect_shape(n, t, q.shape)
     _check_tensor("lse", lse, torch.float32)
+    _expect_shape("lse", lse, (Hq, tq))
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
+    for n, t, ref in (("dq", dq, q), ("dk", dk, k), ("dv", dv, v)):
+        _check_tensor(n, t)
+        _expect_shape(n, t, ref.shape)
     nbytes = int(lib().hk_attn_bwd_varlen_workspace_bytes(B, Hq, Hkv, int(max_seqlen_q), int(max_seqlen_k), d))
     ws = torch.empty(nbytes // 4, dtype=torch.float32, device=q.device) if workspace is None else workspace
+    _check_workspace(ws, nbytes)
     check(lib().hk_attn_bwd_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
                                    _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), _ptr(cu_seqlens_q),
                                    _ptr(cu_seqlens_k), B, Hq, Hkv, tq, tk, int(max_seqlen_q), int(max_seqlen_k), d,
@@ -171,6 +202,7 @@ def gemm(a, b, out=None):
     N = b.shape[0]
     c = torch.empty((M, N), dtype=torch.bfloat16, device=a.device) if out is None else out
     _check_tensor("out", c)
+    _expect_shape("out", c, (M, N))
     check(lib().hk_gemm_bf16(_ptr(a), _ptr(b), _ptr(c), M, N, K, _stream()))
     return c
 
@@ -187,6 +219,9 @@ def ln_dropout_residual(x, residual, weight, bias, p: float = 0.0, seed: int = 0
     rows = x.numel() // D
     o = torch.empty_like(x) if out is None else out
     r = torch.empty_like(x) if out_resid is None else out_resid
+    for n, t in (("out", o), ("out_resid", r)):
+        _check_tensor(n, t)
+        _expect_shape(n, t, x.shape)
     check(lib().hk_ln_dropout_residual(_ptr(x), _ptr(residual), _ptr(weight), _ptr(bias), _ptr(o), _ptr(r), rows, D,
                                        float(p), int(seed) & 0xFFFFFFFF, float(eps), _stream()))
     return o, r
@@ -202,6 +237,8 @@ def rope(x, cos, sin, out=None):
     if cos.shape != (N, d // 2) or sin.shape != (N, d // 2):
         raise ValueError("cos and sin must be [N, d/2]")
     o = torch.empty_like(x) if out is None else out
+    _check_tensor("out", o)
+    _expect_shape("out", o, x.shape)
     check(lib().hk_rope(_ptr(x), _ptr(cos), _ptr(sin), _ptr(o), B, N, H, d, _stream()))
     return o
 

@@ -17,7 +17,10 @@
 #pragma once
 #include <cstddef>
 #include <cstdio>
+#include <map>
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include "../../include/hk_attn.h"
 #include "ptx.cuh"
@@ -937,19 +940,30 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS2, 1)
 #ifndef HK_BWD_FORK
 #define HK_BWD_FORK 1
 #endif
-// One non-blocking side stream per device for the forked dQ pass (created on first use, never
-// destroyed; the library otherwise keeps no state between calls).
-inline cudaStream_t side_stream() {
+// One non-blocking side stream per (device, caller stream) for the forked dQ pass, created on
+// first use with the caller stream's priority and never destroyed. Keying by the caller's
+// stream keeps concurrent backward calls on different streams independent (no false
+// cross-stream dependencies, and a graph capture on one stream never pulls in another
+// caller's work). Beyond 256 distinct caller streams the call runs serially on `stream`.
+inline cudaStream_t side_stream(cudaStream_t caller) {
   static std::mutex mu;
-  static cudaStream_t streams[64] = {};
+  static std::map<std::pair<int, cudaStream_t>, cudaStream_t> streams;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> lk(mu);
-  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
-    streams[dev] = nullptr;
+  const auto key = std::make_pair(dev, caller);
+  const auto it = streams.find(key);
+  if (it != streams.end()) return it->second;
+  if (streams.size() >= 256) return nullptr;
+  int prio = 0;
+  if (cudaStreamGetPriority(caller, &prio) != cudaSuccess) prio = 0;
+  cudaStream_t s2 = nullptr;
+  if (cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, prio) != cudaSuccess) {
     (void)cudaGetLastError();  // fall back to serial launches without leaving a sticky error behind
+    return nullptr;
   }
-  return streams[dev];
+  streams.emplace(key, s2);
+  return s2;
 }
 
 template <typename F>
@@ -987,15 +1001,19 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     snprintf(err, errlen, "cuTensorMapEncodeTiled failed (CUresult %d)", last_encode_result());
     return HK_ERR_DEVICE;
   }
-  static bool attr_done[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 64 || !attr_done[dev]) {
-    if (!set_smem(bwd_dkdv_kernel<D, CAUSAL>, C::SMEM1) || !set_smem(bwd_dq_kernel<D, CAUSAL>, C::SMEM2)) {
-      snprintf(err, errlen, "cudaFuncSetAttribute(max dynamic smem) failed");
-      return HK_ERR_DEVICE;
+  {  // max dynamic smem, once per (instantiation, device), under a lock (concurrent first calls)
+    static std::mutex mu;
+    static std::set<int> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done.count(dev)) {
+      if (!set_smem(bwd_dkdv_kernel<D, CAUSAL>, C::SMEM1) || !set_smem(bwd_dq_kernel<D, CAUSAL>, C::SMEM2)) {
+        snprintf(err, errlen, "cudaFuncSetAttribute(max dynamic smem) failed");
+        return HK_ERR_DEVICE;
+      }
+      done.insert(dev);
     }
-    if (dev < 64) attr_done[dev] = true;
   }
   unsigned* sched = reinterpret_cast<unsigned*>(ws + (size_t)2 * B * Hq * Np);  // 4 counters after D, LSE2
   SeqGeom g{sh.cu_q, sh.cu_k, sh.Nq, sh.Nk, sh.total_q};
@@ -1029,7 +1047,7 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   cudaStream_t s2 = stream;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   if (HK_BWD_FORK && phase < 0) {
-    s2 = side_stream();
+    s2 = side_stream(stream);
     if (s2 && cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) == cudaSuccess &&
         cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) == cudaSuccess &&
         cudaEventRecord(ev_fork, stream) == cudaSuccess && cudaStreamWaitEvent(s2, ev_fork, 0) == cudaSuccess) {

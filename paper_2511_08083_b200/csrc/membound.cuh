@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) rope_kernel(const RopeParams p) {
     const I row = t / (I)cpr;
     const int ch = (int)(t - row * (I)cpr);
     const int n = (int)((row / (I)p.H) % (I)p.N);
-    const __nv_bfloat16* xr = p.x + row * p.d;
+    const __nv_bfloat16* xr = p.x + (size_t)row * p.d;  // 64-bit offset whatever I is
     float a[8], b[8], c[8], s[8];
     unpack8(__ldcs(reinterpret_cast<const uint4*>(xr) + ch), a);
     unpack8(__ldcs(reinterpret_cast<const uint4*>(xr + half) + ch), b);
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) rope_kernel(const RopeParams p) {
       lo[e] = fmaf(a[e], c[e], -b[e] * s[e]);
       hi[e] = fmaf(b[e], c[e], a[e] * s[e]);
     }
-    __nv_bfloat16* orow = p.out + row * p.d;
+    __nv_bfloat16* orow = p.out + (size_t)row * p.d;
     __stcs(reinterpret_cast<uint4*>(orow) + ch, pack8(lo));
     __stcs(reinterpret_cast<uint4*>(orow + half) + ch, pack8(hi));
   }

@@ -38,8 +38,10 @@ __device__ __forceinline__ Seq seq_of(const SeqGeom& g, int b) {
     s.tb = 0;
     s.q0 = s.gq0 = __ldg(g.cu_q + b);
     s.k0 = s.gk0 = __ldg(g.cu_k + b);
-    s.lq = __ldg(g.cu_q + b + 1) - s.q0;
-    s.lk = __ldg(g.cu_k + b + 1) - s.k0;
+    // lengths clamped to [0, max_seqlen]: rows beyond a sequence's max_seqlen are not computed
+    // (hk_attn.h), and offsets that break the contract cannot index past the padded workspace
+    s.lq = min(max(__ldg(g.cu_q + b + 1) - s.q0, 0), g.Nq);
+    s.lk = min(max(__ldg(g.cu_k + b + 1) - s.k0, 0), g.Nk);
   }
   return s;
 }

@@ -51,3 +51,13 @@ def test_check_cu_seqlens():
         api.check_cu_seqlens(cu(0, 3, 3, 10), cu(0, 5, 9, 9), 11, 9, 8, 5)
     with pytest.raises(ValueError, match="max_seqlen_q"):
         api.check_cu_seqlens(cu(0, 3, 3, 10), cu(0, 5, 9, 9), 10, 9, 6, 5)
+
+
+def test_caller_buffer_shapes_are_checked():
+    """Caller-supplied outputs / workspaces reach the C ABI as raw pointers: a wrongly
+    shaped one must be a ValueError in the binding, not an out-of-bounds write."""
+    api._expect_shape("out", t(1, 128, 2, 64), (1, 128, 2, 64))
+    with pytest.raises(ValueError, match="shape"):
+        api._expect_shape("out", t(1, 128, 2, 32), (1, 128, 2, 64))
+    with pytest.raises(ValueError, match="shape"):
+        api._expect_shape("lse", t(1, 2, 127, dtype=torch.float32), (1, 2, 128))

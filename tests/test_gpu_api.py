@@ -73,3 +73,46 @@ def test_cuda_graph_capture_fwd_bwd():
     torch.cuda.synchronize()
     for a, b in zip(eager, (o, lse, *g3)):
         assert torch.equal(a, b)
+
+
+def test_wrong_buffer_shapes_raise():
+    """caller buffers of the wrong shape or size are rejected before any launch."""
+    from paper_2511_08083_b200 import attn_bwd, attn_fwd, bwd_workspace_bytes
+    B, N, Hq, Hkv, d = 1, 256, 4, 2, 64
+    x = make_inputs(B, N, Hq, Hkv, d, seed=1, device="cuda")
+    q, k, v, do = x["Q"], x["K"], x["V"], x["dO"]
+    with pytest.raises(ValueError, match="shape"):
+        attn_fwd(q, k, v, out=torch.empty((B, N - 128, Hq, d), dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(ValueError, match="shape"):
+        attn_fwd(q, k, v, lse=torch.empty((B, Hq, N - 1), dtype=torch.float32, device="cuda"))
+    o, lse = attn_fwd(q, k, v)
+    with pytest.raises(ValueError, match="shape"):
+        attn_bwd(q, k, v, o, lse, do, dk=torch.empty_like(q))
+    with pytest.raises(ValueError, match="shape"):
+        attn_bwd(q, k, v, o[:, :128], lse, do)
+    small = torch.empty(bwd_workspace_bytes(B, Hq, Hkv, N, d) // 4 - 1, dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError, match="workspace"):
+        attn_bwd(q, k, v, o, lse, do, workspace=small)
+
+
+def test_concurrent_backward_streams_independent():
+    """the forked dQ pass has one side stream per caller stream, so two backward
+    calls on two streams neither serialise on a shared side stream nor mix their results:
+    each equals the same call made alone (bitwise)."""
+    from paper_2511_08083_b200 import attn_bwd, attn_fwd
+    B, N, Hq, Hkv, d, causal = 2, 512, 8, 2, 128, True
+    xs = [make_inputs(B, N, Hq, Hkv, d, seed=s, device="cuda") for s in (5, 6)]
+    fw = [attn_fwd(x["Q"], x["K"], x["V"], causal) for x in xs]
+    alone = [attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal) for x, (o, lse) in zip(xs, fw)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [None, None]
+    for rep in range(3):
+        for i, (x, (o, lse)) in enumerate(zip(xs, fw)):
+            streams[i].wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(streams[i]):
+                outs[i] = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal)
+        torch.cuda.synchronize()
+        for a, b in zip(alone, outs):
+            for u, w in zip(a, b):
+                assert torch.equal(u, w)

@@ -211,3 +211,41 @@ def test_varlen_dynamic_schedule_equals_static_bitwise(causal):
         o1, l1 = attn_fwd_varlen(*args, workspace=ws)
         torch.cuda.synchronize()
         assert torch.equal(o0, o1) and torch.equal(l0, l1)
+
+
+def test_varlen_lengths_beyond_max_seqlen_are_clamped():
+    """a sequence longer than max_seqlen (a broken offset contract) must not write
+    past the padded workspace; per hk_attn.h its lengths are clamped to max_seqlen, so its
+    first max_seqlen rows equal the oracle on the truncated sequence and the others are exact."""
+    from paper_2511_08083_b200 import attn_bwd_varlen, attn_fwd_varlen
+    from paper_2511_08083_b200.inputs import make_varlen_inputs
+    lens = [300, 130, 64]
+    mx = 256  # < lens[0]
+    Hq, Hkv, d = 4, 2, 64
+    v = make_varlen_inputs(lens, lens, Hq, Hkv, d, seed=7, device="cuda")
+    tq = sum(lens)
+    o = torch.zeros_like(v["Q"])
+    lse = torch.zeros((Hq, tq), dtype=torch.float32, device="cuda")
+    o, lse = attn_fwd_varlen(v["Q"], v["K"], v["V"], v["cu_q"], v["cu_k"], mx, mx, True, out=o, lse=lse)
+    from paper_2511_08083_b200 import _lib
+    nbytes = int(_lib.lib().hk_attn_bwd_varlen_workspace_bytes(len(lens), Hq, Hkv, mx, mx, d))
+    ws_and_guard = torch.full((nbytes // 4 + 4096,), 7.0, dtype=torch.float32, device="cuda")
+    dq = torch.zeros_like(v["Q"]); dk = torch.zeros_like(v["K"]); dv = torch.zeros_like(v["V"])
+    attn_bwd_varlen(v["Q"], v["K"], v["V"], o, lse, v["dO"], v["cu_q"], v["cu_k"], mx, mx, True,
+                    workspace=ws_and_guard[: nbytes // 4], dq=dq, dk=dk, dv=dv)
+    torch.cuda.synchronize()
+    assert torch.all(ws_and_guard[nbytes // 4:] == 7.0), "backward wrote past its workspace"
+    cut = [min(n, mx) for n in lens]
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    for b, n in enumerate(cut):
+        s0 = offs[b]
+        sl = slice(s0, s0 + n)
+        ref = oracle.attn_fwd_bwd(np64(v["Q"][sl])[None], np64(v["K"][sl])[None], np64(v["V"][sl])[None],
+                                  np64(v["dO"][sl])[None], True)
+        assert np.abs(np64(o[sl]) - ref["O"][0]).max() <= TOL_MAXABS
+        assert np.abs(np64(lse[:, sl]) - ref["LSE"][0]).max() <= TOL_MAXABS
+        for nm, t in (("dQ", dq), ("dK", dk), ("dV", dv)):
+            assert rel_l2(np64(t[sl]), ref[nm][0]) <= TOL_RELL2, (b, nm)
+        if lens[b] > n:  # rows beyond max_seqlen are left untouched
+            tail = slice(s0 + n, s0 + lens[b])
+            assert torch.all(dq[tail] == 0) and torch.all(dk[tail] == 0)
