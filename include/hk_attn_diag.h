@@ -1,4 +1,7 @@
-/* hk_attn_diag.h — diagnostic entry points of libhkattn.so (not the hot path).
+/* hk_attn_diag.h — diagnostic entry points of libhkattn_diag.so (not the hot path; kept
+ * out of libhkattn.so, whose C ABI allocates nothing).
+ *
+ * hk_diag_last_error: thread-local text of this library's last non-OK status.
  *
  * hk_diag_umma: one 128 x N output tile through tcgen05, to pin the
  * UMMA instruction/shared-memory descriptor encodings the attention kernels
@@ -24,6 +27,9 @@
  * kind 3: forward softmax step, param = 10 * (emulated exps per 8) + warpgroups.
  * kind 4: TMA load throughput per SM with boxes of `param` rows x 128 B.
  * kind 5: fp32 red.global.add.v4 throughput into a `param` x 64 KB region.
+ * kind 6: bulk-async (TMA) fp32 reduce-add of 128 x 128 tiles (64 KB) from shared memory
+ * into a [row_tiles*128][32][128] fp32 region (dQ-like), param = mode * 100000 + row_tiles;
+ * mode 0 = one cp.reduce.async.bulk.tensor.2d per tile, 1 = 128 row-wise cp.reduce.async.bulk.
  * kind 1: tcgen05.mma pacing, mode = param / 1000 (0 SS, 1 TS, 2 SS with B
  * MN-major), N = param % 1000 in {64,128,256}; out[cta] = cycles per MMA.
  * `out` is a device pointer to >= 148 floats.
@@ -39,6 +45,7 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+const char* hk_diag_last_error(void);
 hk_status hk_diag_umma(const void* A, const void* B, float* D, int N, int K, int a_tmem, int b_mn,
                        cudaStream_t stream);
 hk_status hk_diag_bwd_phase(int phase, const void* Q, const void* K, const void* V, const void* O, const float* LSE,

@@ -11,15 +11,20 @@ import os
 # HK_LIB=debug selects the -DHK_DEBUG_HANG build (barrier waits trap with a message).
 # HK_LIB=trace selects the -DHK_TRACE build (in-kernel event trace, hk_diag_trace_read).
 # Any other HK_LIB=<name> loads libhkattn_<name>.so (A/B timing of a saved build).
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
-                         f"libhkattn_{os.environ['HK_LIB']}.so" if os.environ.get("HK_LIB") else "libhkattn.so")
+# Those development builds hold the diagnostics too; the release build splits them into
+# libhkattn_diag.so (include/hk_attn_diag.h), which the product path never loads.
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_DEV = os.environ.get("HK_LIB")
+_LIB_PATH = os.path.join(_PKG, f"libhkattn_{_DEV}.so" if _DEV else "libhkattn.so")
+_DIAG_PATH = _LIB_PATH if _DEV else os.path.join(_PKG, "libhkattn_diag.so")
 _lib = None
+_diag = None
 
 HK_STATUS = {0: "HK_OK", 1: "HK_ERR_INVALID_ARGUMENT", 2: "HK_ERR_UNSUPPORTED",
              3: "HK_ERR_DEVICE", 4: "HK_ERR_LAUNCH"}
 
-# (name, restype, argtypes) for every symbol declared in include/hk_attn.h and hk_attn_diag.h
 _P, _I, _Z = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+# (restype, argtypes) for every symbol declared in include/hk_attn.h, hk_gemm.h, hk_membound.h, hk_ring.h
 SIGNATURES = {
     "hk_attn_fwd": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "hk_attn_bwd_workspace_bytes": (_Z, [_I, _I, _I, _I, _I]),
@@ -36,12 +41,16 @@ SIGNATURES = {
     "hk_attn_last_error": (ctypes.c_char_p, []),
     "hk_status_string": (ctypes.c_char_p, [_I]),
     "hk_attn_abi_version": (_I, []),
-    "hk_diag_umma": (_I, [_P, _P, _P, _I, _I, _I, _I, _P]),
-    "hk_diag_rates": (_I, [_I, _I, _I, _P, _P]),
-    "hk_diag_trace_read": (_I, [_P, _Z, _I]),
     "hk_gemm_bf16": (_I, [_P, _P, _P, _I, _I, _I, _P]),
     "hk_ln_dropout_residual": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, ctypes.c_float, ctypes.c_uint, ctypes.c_float, _P]),
     "hk_rope": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _P]),
+}
+# include/hk_attn_diag.h (libhkattn_diag.so)
+DIAG_SIGNATURES = {
+    "hk_diag_last_error": (ctypes.c_char_p, []),
+    "hk_diag_umma": (_I, [_P, _P, _P, _I, _I, _I, _I, _P]),
+    "hk_diag_rates": (_I, [_I, _I, _I, _P, _P]),
+    "hk_diag_trace_read": (_I, [_P, _Z, _I]),
     "hk_diag_bwd_phase": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _I, _I, _I, _I, _I, _I, _P]),
 }
 
@@ -52,19 +61,37 @@ class HKError(RuntimeError):
         self.status = status
 
 
+def _load(path, sigs):
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} not built: run `python -m paper_2511_08083_b200.build`")
+    L = ctypes.CDLL(path)
+    for name, (res, args) in sigs.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    return L
+
+
 def lib():
+    """libhkattn.so, the product C ABI."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            raise RuntimeError(f"{_LIB_PATH} not built: run `python -m paper_2511_08083_b200.build`")
-        L = ctypes.CDLL(_LIB_PATH)
-        for name, (res, args) in SIGNATURES.items():
-            f = getattr(L, name)
-            f.restype, f.argtypes = res, args
-        _lib = L
+        _lib = _load(_LIB_PATH, {**SIGNATURES, **(DIAG_SIGNATURES if _DEV else {})})
     return _lib
+
+
+def diag():
+    """libhkattn_diag.so (or the development build holding both): diagnostics only."""
+    global _diag
+    if _diag is None:
+        _diag = lib() if _DEV else _load(_DIAG_PATH, DIAG_SIGNATURES)
+    return _diag
 
 
 def check(status: int):
     if status != 0:
         raise HKError(status, lib().hk_attn_last_error().decode())
+
+
+def check_diag(status: int):
+    if status != 0:
+        raise HKError(status, diag().hk_diag_last_error().decode())

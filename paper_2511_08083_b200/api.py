@@ -9,7 +9,7 @@ import ctypes
 
 import torch
 
-from ._lib import HKError, check, lib  # noqa: F401
+from ._lib import HKError, check, check_diag, diag, lib  # noqa: F401
 
 
 def _ptr(t):
@@ -278,9 +278,9 @@ class AttentionVarlen(torch.autograd.Function):
 
 
 def diag_umma(a, b, n, k, a_tmem: bool, b_mn: bool):
-    """Diagnostic single-tile tcgen05 GEMM (include/hk_attn_diag.h)."""
+    """Diagnostic single-tile tcgen05 GEMM (include/hk_attn_diag.h, libhkattn_diag.so)."""
     _check_tensor("a", a)
     _check_tensor("b", b)
     d = torch.empty((128, n), dtype=torch.float32, device=a.device)
-    check(lib().hk_diag_umma(_ptr(a), _ptr(b), _ptr(d), n, k, int(a_tmem), int(b_mn), _stream()))
+    check_diag(diag().hk_diag_umma(_ptr(a), _ptr(b), _ptr(d), n, k, int(a_tmem), int(b_mn), _stream()))
     return d

@@ -8,10 +8,13 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libhkattn.so")
+LIB = os.path.join(PKG, "libhkattn.so")            # the product C ABI (include/hk_attn.h & co.)
+LIB_DIAG = os.path.join(PKG, "libhkattn_diag.so")  # diagnostics (include/hk_attn_diag.h)
 LIB_DEBUG = os.path.join(PKG, "libhkattn_debug.so")  # -DHK_DEBUG_HANG: barrier waits trap instead of hanging
 LIB_TRACE = os.path.join(PKG, "libhkattn_trace.so")  # -DHK_TRACE: in-kernel clock64 event trace
 SOURCES = [os.path.join(CSRC, "hk_attn.cu")]
+SOURCES_DIAG = [os.path.join(CSRC, "hk_diag.cu")]
+SOURCES_DEV = [os.path.join(CSRC, "hk_dev.cu")]  # debug / trace / variant builds: both in one library
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
          "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden", "-I", os.path.join(ROOT, "include")]
@@ -25,34 +28,51 @@ def _deps():
 
 
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(f) > t for f in _deps())
+    for lib in (LIB, LIB_DIAG):
+        if not os.path.exists(lib):
+            return True
+        t = os.path.getmtime(lib)
+        if any(os.path.getmtime(f) > t for f in _deps()):
+            return True
+    return False
+
+
+def _nvcc(sources, out, extra):
+    tmp = out + ".tmp"
+    return tmp, subprocess.Popen([NVCC, *FLAGS, *extra, "-o", tmp, *sources], stdout=subprocess.PIPE,
+                                 stderr=subprocess.PIPE, text=True)
 
 
 def build(force: bool = False, verbose: bool = False, debug: bool = False, trace: bool = False,
           variant: str = "") -> str:
-    """variant: build libhkattn_<variant>.so instead (A/B experiments with HK_EXTRA flags)."""
+    """Release: libhkattn.so + libhkattn_diag.so (compiled in parallel). debug / trace / variant
+    (libhkattn_<variant>.so, A/B experiments with HK_EXTRA flags): one library holding both."""
+    dev = debug or trace or bool(variant)
     lib = LIB_DEBUG if debug else LIB_TRACE if trace else LIB
     if variant:
         lib = os.path.join(PKG, f"libhkattn_{variant}.so")
-    if not force and not (debug or trace or variant) and not needs_build():
+    if not force and not dev and not needs_build():
         return LIB
-    tmp = lib + ".tmp"
     extra = (["-DHK_DEBUG_HANG"] if debug else []) + (["-DHK_TRACE"] if trace else [])
     extra += os.environ.get("HK_EXTRA", "").split()  # e.g. tuning -D flags
-    cmd = [NVCC, *FLAGS, *extra, "-o", tmp, *SOURCES]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libhkattn.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
-    if not (debug or trace or variant):
-        with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
-            f.write(r.stderr)
-    os.replace(tmp, lib)
+    jobs = [(lib, *_nvcc(SOURCES_DEV if dev else SOURCES, lib, extra))]
+    if not dev:
+        jobs.append((LIB_DIAG, *_nvcc(SOURCES_DIAG, LIB_DIAG, extra)))
+    errs = []
+    for out, tmp, proc in jobs:
+        so, se = proc.communicate()
+        if proc.returncode != 0:
+            errs.append(so + se)
+            continue
+        if verbose:
+            sys.stderr.write(se)
+        if out == LIB and not dev:
+            with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+                f.write(se)
+        os.replace(tmp, out)
+    if errs:
+        sys.stderr.write("\n".join(errs))
+        raise RuntimeError("nvcc failed building " + ", ".join(os.path.basename(j[0]) for j in jobs))
     return lib
 
 

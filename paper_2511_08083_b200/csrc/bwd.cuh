@@ -255,7 +255,7 @@ __device__ __forceinline__ KvItem kv_decode(const BwdParams& p, int item) {
   it.kvh = rest % p.Hkv;
   it.b = rest / p.Hkv;
   it.sq = seq_of(p.g, it.b);
-  it.jt = CAUSAL ? T - 1 - tr : tr;              // heaviest first
+  it.jt = tr;  // heaviest first when causal: key tile jt is seen by the query tiles i >= jt
   it.i0 = first_q_tile_for<CAUSAL>(it.sq, it.jt);  // first query block that sees key tile jt
   it.nqt = (it.sq.lq + 127) / 128;
   const bool live = it.jt * 128 < it.sq.lk && it.i0 < it.nqt;

@@ -243,4 +243,46 @@ __global__ void __launch_bounds__(256) red_rate_kernel(float* dst, int tiles, in
   if (threadIdx.x == 0) out_cycles[blockIdx.x] = (float)(t1 - t0);
 }
 
+// fp32 reduce-add of whole 128 x 128 tiles (64 KB) from shared memory into global memory by the
+// bulk-async (TMA) engine: the instruction SURVEY §8(f) NEXT #1 names for accumulating dQ inside
+// the dK/dV pass. The destination mimics dQ [rows][H][128] fp32 of one (b, kvh) window: a tile
+// is 128 rows of one head, rows H * 512 B apart. MODE 0: one cp.reduce.async.bulk.tensor.2d
+// per tile (box 128 x 128 fp32, no swizzle); MODE 1: 128 row-wise cp.reduce.async.bulk (512 B
+// each). One thread per CTA issues, keeping up to INFLIGHT tiles outstanding. out[cta] = cycles.
+template <int MODE>
+__global__ void __launch_bounds__(128) bulk_red_rate_kernel(const __grid_constant__ CUtensorMap map, float* dst,
+                                                            int row_tiles, int H, int iters, float* out_cycles) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  float* sm = reinterpret_cast<float*>(sm_raw);
+  for (int i = threadIdx.x; i < 128 * 128; i += blockDim.x) sm[i] = 1e-3f * (i & 7);
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int t = (blockIdx.x * 7 + it * 13) % (row_tiles * H);
+      const int rt = t / H, h = t % H;
+      if (MODE == 0) {
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                reinterpret_cast<uint64_t>(&map)),
+            "r"(smem_u32(sm)), "r"(h * 128), "r"(rt * 128)
+            : "memory");
+      } else {
+        float* base = dst + ((size_t)rt * 128 * H + h) * 128;
+        for (int r = 0; r < 128; ++r)
+          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], 512;" ::"l"(
+                           base + (size_t)r * H * 128),
+                       "r"(smem_u32(sm + r * 128))
+                       : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 6;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    const long long t1 = clock64();
+    out_cycles[blockIdx.x] = (float)(t1 - t0);
+  }
+}
+
 }  // namespace hk

@@ -38,12 +38,14 @@ def _block(shape, seed, device, std):
 
 
 def make_inputs(B, N, Hq, Hkv, d, seed=0, device="cpu", std=1.0, batches=None,
-                tensors=("Q", "K", "V", "dO"), std_qk=None):
-    """Return dict name -> bf16 tensor. Q/dO [B', N, Hq, d], K/V [B', N, Hkv, d].
+                tensors=("Q", "K", "V", "dO"), std_qk=None, kv_heads=None):
+    """Return dict name -> bf16 tensor. Q/dO [B', N, Hq', d], K/V [B', N, Hkv', d].
 
     `batches` (default all of range(B)) selects which global batch indices to
-    generate, in order; the values for batch b do not depend on which other
-    batches are generated. `std` scales all four tensors; `std_qk` (if given)
+    generate, in order; `kv_heads` (default all of range(Hkv)) which KV heads
+    (Hkv' = len(kv_heads), Hq' = G * Hkv': each KV head brings its G query
+    heads). The values of a (b, kvh) unit do not depend on which other units
+    are generated. `std` scales all four tensors; `std_qk` (if given)
     overrides it for Q and K only — the stress recipe Q, K ~ N(0, 4^2) with
     V, dO ~ N(0, 1) (SURVEY §8(c).4 "Stress distributions").
     """
@@ -51,20 +53,21 @@ def make_inputs(B, N, Hq, Hkv, d, seed=0, device="cpu", std=1.0, batches=None,
         raise ValueError("Hq must be a multiple of Hkv")
     G = Hq // Hkv
     batches = list(range(B)) if batches is None else list(batches)
+    kv_heads = list(range(Hkv)) if kv_heads is None else list(kv_heads)
     out = {}
     for name in tensors:
         t = TENSOR_IDS[name]
         sd = std_qk if (std_qk is not None and name in ("Q", "K")) else std
-        heads = Hq if name in ("Q", "dO") else Hkv
+        heads = G * len(kv_heads) if name in ("Q", "dO") else len(kv_heads)
         x = torch.empty((len(batches), N, heads, d), dtype=torch.bfloat16, device=device)
         for bi, b in enumerate(batches):
-            for kvh in range(Hkv):
+            for ki, kvh in enumerate(kv_heads):
                 if name in ("Q", "dO"):
                     blk = _block((N, G, d), splitmix64(seed, t, b, kvh), device, sd)
-                    x[bi, :, kvh * G:(kvh + 1) * G, :] = blk
+                    x[bi, :, ki * G:(ki + 1) * G, :] = blk
                 else:
                     blk = _block((N, d), splitmix64(seed, t, b, kvh), device, sd)
-                    x[bi, :, kvh, :] = blk
+                    x[bi, :, ki, :] = blk
         out[name] = x
     return out
 

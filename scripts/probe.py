@@ -64,12 +64,12 @@ def main():
                 import ctypes
                 from paper_2511_08083_b200 import _lib
                 from paper_2511_08083_b200.api import bwd_workspace_bytes
-                L = _lib.lib()
+                L = _lib.diag()
                 ws = torch.empty(bwd_workspace_bytes(B, Hq, Hkv, N, d) // 4, device="cuda", dtype=torch.float32)
                 P = lambda t: ctypes.c_void_p(t.data_ptr())
                 sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
                 for ph, name, fl in ((0, "pre", 0), (1, "dkdv", 2.0), (2, "dq", 1.5)):
-                    f = lambda: _lib.check(L.hk_diag_bwd_phase(ph, P(x["Q"]), P(x["K"]), P(x["V"]), P(o), P(lse),
+                    f = lambda: _lib.check_diag(L.hk_diag_bwd_phase(ph, P(x["Q"]), P(x["K"]), P(x["V"]), P(o), P(lse),
                                                                P(x["dO"]), P(dq), P(dk), P(dv), P(ws), ws.numel() * 4,
                                                                B, Hq, Hkv, N, d, int(causal), sp))
                     t = timeit(f, a.iters, 2)

@@ -19,7 +19,7 @@ shapes = {"C2-nc": (16, 4096, 16, 16, 128, False), "C3": (16, 8192, 32, 8, 128, 
           "C4-8192": (16, 8192, 32, 32, 64, True), "C5-4096-nc": (16, 4096, 64, 8, 128, False)}
 B, N, Hq, Hkv, d, causal = shapes[cfg]
 x = make_inputs(B, N, Hq, Hkv, d, seed=0, device="cuda")
-L = _lib.lib()
+L = _lib.diag()
 o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
 dq, dk, dv = torch.empty_like(x["Q"]), torch.empty_like(x["K"]), torch.empty_like(x["V"])
 ws = torch.empty(bwd_workspace_bytes(B, Hq, Hkv, N, d) // 4, device="cuda")
@@ -28,7 +28,7 @@ buf = np.zeros(64 * 1024, dtype=np.uint64)
 
 
 def run(phase):
-    _lib.check(L.hk_diag_bwd_phase(phase, P(x["Q"]), P(x["K"]), P(x["V"]), P(o), P(lse), P(x["dO"]), P(dq), P(dk),
+    _lib.check_diag(L.hk_diag_bwd_phase(phase, P(x["Q"]), P(x["K"]), P(x["V"]), P(o), P(lse), P(x["dO"]), P(dq), P(dk),
                                    P(dv), P(ws), ws.numel() * 4, B, Hq, Hkv, N, d, int(causal), None))
     torch.cuda.synchronize()
 
@@ -39,7 +39,7 @@ for phase, name in ((1, "dkdv"), (2, "dq")):
     run(phase)
     L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1)
     run(phase)
-    _lib.check(L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1))
+    _lib.check_diag(L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1))
     tab = buf.reshape(64, 1024)
     ev = {(e, a): int(tab[e, a]) for e in range(64) for a in range(1024) if tab[e, a]}
     its = sorted(a for (e, a) in ev if e == 2)

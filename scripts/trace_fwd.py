@@ -21,14 +21,14 @@ shapes = {"C2-nc": (16, 4096, 16, 16, 128, False), "C3": (16, 8192, 32, 8, 128, 
           "C4-8192": (16, 8192, 32, 32, 64, True)}
 B, N, Hq, Hkv, d, causal = shapes[cfg]
 x = make_inputs(B, N, Hq, Hkv, d, seed=0, device="cuda")
-L = _lib.lib()
+L = _lib.diag()
 attn_fwd(x["Q"], x["K"], x["V"], causal)
 torch.cuda.synchronize()
 buf = np.zeros(64 * 1024, dtype=np.uint64)
 L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1)
 attn_fwd(x["Q"], x["K"], x["V"], causal)
 torch.cuda.synchronize()
-_lib.check(L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1))
+_lib.check_diag(L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1))
 tab = buf.reshape(64, 1024)
 ev = {(e, a): int(tab[e, a]) for e in range(64) for a in range(1024) if tab[e, a]}
 res = {}

@@ -25,14 +25,14 @@ for cfg in sys.argv[1:]:
         x = make_qk_inputs(B, N, shapes[cfg][6], Hq, Hkv, d, seed=0, device="cuda")
     else:
         x = make_inputs(B, N, Hq, Hkv, d, seed=0, device="cuda")
-    L = _lib.lib()
+    L = _lib.diag()
     attn_fwd(x["Q"], x["K"], x["V"], causal)
     torch.cuda.synchronize()
     buf = np.zeros(64 * 1024, dtype=np.uint64)
     L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1)
     attn_fwd(x["Q"], x["K"], x["V"], causal)
     torch.cuda.synchronize()
-    _lib.check(L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1))
+    _lib.check_diag(L.hk_diag_trace_read(ctypes.c_void_p(buf.ctypes.data), buf.nbytes, 1))
     tab = buf.reshape(64, 1024)
     out = {"config": cfg}
     for t in (0, 1):

@@ -9,12 +9,17 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2511_08083_b200", "libhkattn.so")
+LIB_DIAG = os.path.join(ROOT, "paper_2511_08083_b200", "libhkattn_diag.so")
 
 
-def declared_symbols():
+def declared_symbols(which="all"):
+    """hk_* functions declared in include/*.h: "diag" = hk_attn_diag.h (libhkattn_diag.so),
+    "product" = every other header (libhkattn.so)."""
     names = set()
     inc = os.path.join(ROOT, "include")
     for f in os.listdir(inc):
+        if which == "diag" and f != "hk_attn_diag.h" or which == "product" and f == "hk_attn_diag.h":
+            continue
         if f.endswith(".h"):
             src = open(os.path.join(inc, f)).read()
             src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
@@ -30,15 +35,20 @@ def lib():
 
 
 def test_exports_every_declared_symbol(lib):
-    names = declared_symbols()
+    names = declared_symbols("product")
     assert {"hk_attn_fwd", "hk_attn_bwd", "hk_attn_bwd_workspace_bytes", "hk_attn_last_error"} <= names
     for n in names:
         assert hasattr(lib, n), f"{n} not exported"
+    diag = ctypes.CDLL(LIB_DIAG)
+    for n in declared_symbols("diag"):
+        assert hasattr(diag, n), f"{n} not exported by libhkattn_diag.so"
+        assert not hasattr(lib, n), f"diagnostic {n} must not be in the product library"
 
 
 def test_binding_covers_header():
-    from paper_2511_08083_b200._lib import SIGNATURES
-    assert declared_symbols() == set(SIGNATURES)
+    from paper_2511_08083_b200._lib import DIAG_SIGNATURES, SIGNATURES
+    assert declared_symbols("product") == set(SIGNATURES)
+    assert declared_symbols("diag") == set(DIAG_SIGNATURES)
 
 
 def test_host_only_validation(lib):

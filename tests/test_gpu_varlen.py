@@ -174,13 +174,21 @@ def test_varlen_full_size_sampled():
         a, e = cu[b], cu[b + 1]
         n = e - a
         Q, K, V, dO = (np64(x[k][a:e])[None] for k in ("Q", "K", "V", "dO"))
-        rows = sample_rows(n, 48, seed=b)  # first/last 8, tile edges, random (as the dense full-size tests)
+        # ROW mode: 256 rows — first/last 8, tile edges, random. Relative L2 is
+        # over the sample (reading #16); per-row errors are a logged diagnostic (reading #24: rows
+        # with few visible keys carry the D-from-bf16-O residue of reading #11).
+        rows = sample_rows(n, 256, seed=b)
         kvh = 3
         for h in (kvh * G, kvh * G + G - 1):
             r = oracle.attn_rows(Q, K, V, dO, causal, 0, h, rows)
             assert np.abs(np64(o)[a:e][rows, h] - r["O"]).max() <= TOL_MAXABS
             assert np.abs(np64(lse)[h, a:e][rows] - r["LSE"]).max() <= TOL_MAXABS
-            assert rel_l2(np64(dq)[a:e][rows, h], r["dQ"]) <= TOL_RELL2
+            got = np64(dq)[a:e][rows, h]
+            row_rel = np.linalg.norm(got - r["dQ"], axis=1) / np.maximum(np.linalg.norm(r["dQ"], axis=1), 1e-30)
+            worst = np.argsort(row_rel)[::-1][:3]
+            print({"doc": b, "len": n, "head": h, "dQ_rel_l2": rel_l2(got, r["dQ"]),
+                   "worst_rows_dQ_rel": [[int(rows[i]), float(row_rel[i])] for i in worst]})
+            assert rel_l2(got, r["dQ"]) <= TOL_RELL2
         LSEf = np.zeros((1, Hq, n))
         Df = np.zeros((1, Hq, n))
         for h in range(kvh * G, kvh * G + G):
