@@ -565,7 +565,9 @@ def multi_gpu_checks(pb, args, rank, world):
         # (2) oracle on sampled rows of the gathered unit (inputs regenerated on the host)
         import oracle
         from paper_2511_08083_b200.inputs import make_inputs, sample_rows
-        xi = make_inputs(pb.B_global, N, Hq, Hkv, d, seed=args.seed, batches=[unit[0]], kv_heads=[unit[1]])
+        # regenerated on the GPU (the CUDA generator's stream, as every rank drew it), then copied
+        xi = make_inputs(pb.B_global, N, Hq, Hkv, d, seed=args.seed, device="cuda", batches=[unit[0]],
+                         kv_heads=[unit[1]])
         f = lambda t: t.float().cpu().numpy().astype(np.float64)
         Q, K, V, dO = f(xi["Q"]), f(xi["K"]), f(xi["V"]), f(xi["dO"])
         o_u, lse_u, dq_u = (f(t) for t in recv[:3])

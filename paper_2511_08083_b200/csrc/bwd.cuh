@@ -40,8 +40,8 @@ template <int D>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ O,
                                                       const __nv_bfloat16* __restrict__ dO,
                                                       const float* __restrict__ lse, float* __restrict__ Dout,
-                                                      float* __restrict__ lse2, SeqGeom g, int H, int Np,
-                                                      unsigned* __restrict__ sched) {
+                                                      float* __restrict__ lse2, SeqGeom g, int H, int hshift,
+                                                      int Np, unsigned* __restrict__ sched) {
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 4) sched[threadIdx.x] = 0u;
   constexpr int LPR = D / 8;  // lanes per row
   constexpr int RPW = 32 / LPR;
@@ -71,8 +71,13 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
       const size_t row = base + u * RPW + lrow;
       L[u] = 0.f;
       const uint32_t r32 = (uint32_t)row;
-      nn[u] = (int)(r32 / (uint32_t)H);
-      hh[u] = (int)(r32 - (uint32_t)nn[u] * (uint32_t)H);
+      if (hshift >= 0) {  // H a power of two (every BASELINE config): shift and mask
+        nn[u] = (int)(r32 >> hshift);
+        hh[u] = (int)(r32 & (uint32_t)(H - 1));
+      } else {
+        nn[u] = (int)(r32 / (uint32_t)H);
+        hh[u] = (int)(r32 - (uint32_t)nn[u] * (uint32_t)H);
+      }
       if (row < rows) {
         a[u] = __ldcs(reinterpret_cast<const uint4*>(O + (row0 + row) * D) + sub);
         gv[u] = __ldcs(reinterpret_cast<const uint4*>(dO + (row0 + row) * D) + sub);
@@ -1040,7 +1045,7 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   if (phase < 0 || phase == 0)
     bwd_pre_kernel<D><<<dim3((unsigned)bx, (unsigned)B), 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(O), reinterpret_cast<const __nv_bfloat16*>(dO), LSE, Dv, lse2, g, Hq,
-        Np, sched);
+        (Hq & (Hq - 1)) == 0 ? __builtin_ctz((unsigned)Hq) : -1, Np, sched);
   // B1, B2. They are independent (both only read the preprocess output): with HK_BWD_FORK the dQ
   // pass goes on a side stream forked from `stream` after B0 and joined back after it, so its
   // CTAs take the SMs the dK/dV pass's last CTAs free instead of waiting for the whole pass.

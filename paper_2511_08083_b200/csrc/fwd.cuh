@@ -66,6 +66,10 @@ struct FwdCfg {
 #define HK_FWD_EMU64 3
 #endif
   static constexpr int EMU_OF_8 = (D == 128) ? HK_FWD_EMU128 : HK_FWD_EMU64;  // exps per 8 on the FMA pipe
+#ifndef HK_FWD_ALT
+#define HK_FWD_ALT 0
+#endif
+  static constexpr bool ALT = HK_FWD_ALT != 0;  // the two tiles' exponential phases take turns
 };
 
 // One work item = (b, h, pair of 128-row Q tiles). Items are numbered so that
@@ -378,6 +382,9 @@ __global__ void __launch_bounds__(384, 1)
     const float c = 1.4426950408889634f / sqrtf((float)D);  // (1/sqrt d) log2 e
     uint32_t s_ph = 0, o_ph = 0;
     int step = 0;  // running KV-step count (trace index only)
+    // turn-taking (C::ALT): tile 0 waits on barrier 1 and releases barrier 2, tile 1 the reverse;
+    // tile 1 opens the first turn. Only steps both tiles have take turns (the counts agree).
+    if (C::ALT && t == 1) named_bar_arrive(1, 256);
     for (int rr = 0;; ++rr) {
       const int item = dyn ? sched_take(sched, rr) : fwd_item_index<CAUSAL>(rr, cta, ctas);
       if (item >= p.num_items) break;
@@ -408,9 +415,11 @@ __global__ void __launch_bounds__(384, 1)
         const int shift = CAUSAL ? qt * 128 + off - j * 128 : (1 << 20);
         const int kleft = it.sq.lk - j * 128;
         const int kvalid = kleft < 128 ? kleft : 128;
+        const bool turn = C::ALT && j < min(it.nkv0, it.nkv1);
         softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, shift, j > 0, kvalid, 40 + 4 * t, step,
                                      &bar_pl[t], tP, C::SPLIT_P && j + 1 < nk ? &bar_sfree[t] : nullptr,
-                                     C::SPLIT_P && j > 0 ? &bar_pv[t] : nullptr, &pv_ph);
+                                     C::SPLIT_P && j > 0 ? &bar_pv[t] : nullptr, &pv_ph, turn ? 1 + t : -1,
+                                     turn ? 2 - t : -1);
         tmem_wait_st();
         if (threadIdx.x % 128 == 0) hk_trace(43 + 4 * t, step, 0);  // P stores complete
         tc_fence_before();
@@ -452,6 +461,7 @@ __global__ void __launch_bounds__(384, 1)
     }
   }
 
+  if (C::ALT && warp < 4) named_bar_sync(1, 256);  // tile 1's opening arrive (or its last turn's)
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc<512>(tbase);

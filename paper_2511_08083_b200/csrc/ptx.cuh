@@ -190,6 +190,9 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // ------------------------------------------------------------------ register reallocation
 template <uint32_t N>
@@ -303,6 +306,12 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
 __host__ __device__ constexpr uint64_t sdesc_sw128_const(uint32_t lbo_bytes, uint32_t sbo_bytes) {
   return ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) | ((uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// Constant part of a descriptor of any layout type (0 none, 2 SW128, 4 SW64, 6 SW32).
+__host__ __device__ constexpr uint64_t sdesc_const(uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
+  return ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) | ((uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
 }
 
 // D[tmem] (+)= A[smem] * B[smem]

@@ -62,7 +62,8 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
                                              float& m, float& l, int shift, bool o_live, int kvalid = 128,
                                              int trace_ev = -1, uint32_t trace_idx = 0, uint64_t* bar_lo = nullptr,
                                              uint32_t tP = 0, uint64_t* bar_sfree = nullptr,
-                                             uint64_t* bar_pv = nullptr, uint32_t* pv_phase = nullptr) {
+                                             uint64_t* bar_pv = nullptr, uint32_t* pv_phase = nullptr,
+                                             int alt_wait = -1, int alt_arrive = -1) {
   if (tP == 0) tP = tS;
 #ifdef HK_TRACE
   const bool tr = trace_ev >= 0 && (threadIdx.x % 128) == 0;
@@ -134,6 +135,10 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
     tmem_wait_st();
   }
   float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  // Exponential phases of the two Q tiles' warpgroups take turns (named barriers alt_wait /
+  // alt_arrive, 256 threads = both warpgroups): each runs with the SM's MUFU and FMA pipes to
+  // itself, in the order the MMA warp consumes P (tile 0, then tile 1).
+  if (alt_wait >= 0) named_bar_sync(alt_wait, 256);
 #pragma unroll
   for (int c0 = 0; c0 < 128; c0 += 32) {
     uint32_t pk[16];
@@ -149,6 +154,7 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
       if ((threadIdx.x & 31) == 0) mbar_arrive(bar_lo);
     }
   }
+  if (alt_arrive >= 0) named_bar_arrive(alt_arrive, 256);
   HK_SM_TRACE(2)  // exps done, P stores issued
   const float2 rs2 = add2(acc[0], acc[1]);
   l = l * alpha + (rs2.x + rs2.y);

@@ -46,12 +46,13 @@ def main():
         o = torch.empty_like(x["Q"])
         lse = torch.empty(B, Hq, N, device="cuda", dtype=torch.float32)
         dq, dk, dv = torch.empty_like(x["Q"]), torch.empty_like(x["K"]), torch.empty_like(x["V"])
-        wsb = libs["A"].hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d)
-        ws = torch.zeros(max(wsb, libs["B"].hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d)) // 4 + 64,
-                         device="cuda", dtype=torch.float32)
+        # one workspace per build: their layouts may differ (e.g. r2's augmented K-step rows)
+        wss = {t: torch.zeros(libs[t].hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d) // 4 + 64, device="cuda",
+                              dtype=torch.float32) for t in libs}
         sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
         def run(L, ph):
+            ws = wss["A"] if L is libs["A"] else wss["B"]
             if ph == "fwd":
                 r = L.hk_attn_fwd(P(x["Q"]), P(x["K"]), P(x["V"]), P(o), P(lse), B, Hq, Hkv, N, d, int(causal), sp)
             else:
@@ -62,7 +63,7 @@ def main():
 
         run(libs["A"], "fwd")
         run(libs["A"], "pre")
-        run(libs["B"], "pre")  # either build's pre-kernel leaves the same D / LSE2
+        run(libs["B"], "pre")  # each build's own workspace
         res = {}
         for ph in a.phases.split(","):
             t = {"A": [], "B": []}
