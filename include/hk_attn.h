@@ -54,7 +54,8 @@ hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, floa
 
 /* Bytes of workspace hk_attn_bwd needs: D = rowsum(dO * O) and LSE*log2(e),
  * each [B][Hq][Np] fp32 with Np = N rounded up to a multiple of 128, then 256 bytes
- * of work counters for the persistent kernels: 2*B*Hq*Np*4 + 256. The call
+ * of work counters for the persistent kernels, then for d = 64 the fused backward's fp32 dQ
+ * accumulator (B*Np*Hq*64 floats): 2*B*Hq*Np*4 + 256 (+ B*Np*Hq*256 when d == 64). The call
  * initialises all of it (no zeroing needed); calls sharing one workspace must be
  * stream-ordered. */
 size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d);
@@ -88,7 +89,7 @@ hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O
  * LSE: [B][Hq][Nq] fp32. Nq, Nk >= 1. Errors and ownership as above. */
 hk_status hk_attn_fwd_qk(const void* Q, const void* K, const void* V, void* O, float* LSE, int B, int Hq,
                          int Hkv, int Nq, int Nk, int d, int causal, cudaStream_t stream);
-/* = 2*B*Hq*Nqp*4 + 256, Nqp = Nq rounded up to a multiple of 128. */
+/* = 2*B*Hq*Nqp*4 + 256 (+ B*Nqp*Hq*256 when d == 64), Nqp = Nq rounded up to a multiple of 128. */
 size_t hk_attn_bwd_qk_workspace_bytes(int B, int Hq, int Hkv, int Nq, int Nk, int d);
 hk_status hk_attn_bwd_qk(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                          const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
@@ -117,13 +118,34 @@ hk_status hk_attn_fwd_varlen(const void* Q, const void* K, const void* V, void* 
                              const int* cu_seqlens_q, const int* cu_seqlens_k, int B, int Hq, int Hkv,
                              int total_q, int total_k, int max_seqlen_q, int max_seqlen_k, int d, int causal,
                              void* workspace, size_t workspace_bytes, cudaStream_t stream);
-/* = 2*B*Hq*Mp*4 + 256, Mp = max_seqlen_q rounded up to a multiple of 128. */
+/* = 2*B*Hq*Mp*4 + 256 (+ B*Mp*Hq*256 when d == 64), Mp = max_seqlen_q rounded up to 128. */
 size_t hk_attn_bwd_varlen_workspace_bytes(int B, int Hq, int Hkv, int max_seqlen_q, int max_seqlen_k, int d);
 hk_status hk_attn_bwd_varlen(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                              const void* dO, void* dQ, void* dK, void* dV, void* workspace,
                              size_t workspace_bytes, const int* cu_seqlens_q, const int* cu_seqlens_k, int B,
                              int Hq, int Hkv, int total_q, int total_k, int max_seqlen_q, int max_seqlen_k, int d,
                              int causal, cudaStream_t stream);
+
+/* ---- Backward with flags (ABI 4).
+ * At d = 64 the default backward is the fused single pass (DESIGN.md
+ * §6 "Fused backward"): the dK/dV pass also forms dQ_partial = dS K_j per 128 x 128 block on the
+ * tensor core and adds it into an fp32 accumulator in the workspace with the bulk-async tensor
+ * reduce (cp.reduce.async.bulk.tensor .add.f32), then one pass scales and rounds it to bf16; the
+ * separate dQ pass (which recomputes S and dP) is not run. The fp32 additions of the
+ * partials land in L2 in whatever order the CTAs reach them, so dQ is reproducible only up to
+ * fp32 reordering (dK, dV stay bitwise reproducible). HK_BWD_DETERMINISTIC selects the two-pass
+ * backward (bitwise reproducible dQ, the d = 128 path) at d = 64; at d = 128 flags change nothing.
+ * hk_attn_bwd* without _ex use flags = 0. Unknown flag bits: HK_ERR_INVALID_ARGUMENT. */
+#define HK_BWD_DETERMINISTIC 1u
+hk_status hk_attn_bwd_ex(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                         const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
+                         int B, int Hq, int Hkv, int Nq, int Nk, int d, int causal, unsigned flags,
+                         cudaStream_t stream);
+hk_status hk_attn_bwd_varlen_ex(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                                const void* dO, void* dQ, void* dK, void* dV, void* workspace,
+                                size_t workspace_bytes, const int* cu_seqlens_q, const int* cu_seqlens_k, int B,
+                                int Hq, int Hkv, int total_q, int total_k, int max_seqlen_q, int max_seqlen_k,
+                                int d, int causal, unsigned flags, cudaStream_t stream);
 
 const char* hk_attn_last_error(void);
 const char* hk_status_string(hk_status s);

@@ -36,6 +36,21 @@ hk_status hk_ln_dropout_residual(const void* x, const void* residual, const void
 
 hk_status hk_rope(const void* x, const float* cos, const float* sin, void* out, int B, int N, int H, int d,
                   cudaStream_t stream);
+/* inverse != 0: the inverse rotation (sin negated): out_i = x_i cos + x_{i+d/2} sin,
+ * out_{i+d/2} = x_{i+d/2} cos - x_i sin — the gradient of a rotated tensor maps back through it. */
+hk_status hk_rope_ex(const void* x, const float* cos, const float* sin, void* out, int B, int N, int H, int d,
+                     int inverse, cudaStream_t stream);
+
+/* hk_attn_fwd_rope — rotary fused into the attention forward (SURVEY §8(f) NEXT #3, P:559,
+ * P:583): O, LSE = attention(rope(Q), rope(K), V), dense self-attention (Nq = Nk = N), positions
+ * 0..N-1, cos / sin [N][d/2] fp32 as hk_rope. Q tiles are rotated in shared memory by the
+ * forward kernel (each is read once per CTA, so the rotation costs no HBM pass); K, re-read by
+ * every query tile of its group, is rotated once into the caller's Kr [B][N][Hkv][d] bf16 (an
+ * output: the backward and a KV cache need the rotated keys). Bitwise equal to hk_rope on Q and K
+ * followed by hk_attn_fwd. Other arguments, layouts and errors as hk_attn_fwd. */
+hk_status hk_attn_fwd_rope(const void* Q, const void* K, const void* V, const float* cos, const float* sin, void* O,
+                           float* LSE, void* Kr, int B, int Hq, int Hkv, int N, int d, int causal,
+                           cudaStream_t stream);
 
 #ifdef __cplusplus
 }

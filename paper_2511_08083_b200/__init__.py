@@ -4,6 +4,6 @@ The data-parallel hot path of HipKittens (arXiv 2511.08083): MHA/GQA,
 causal and non-causal, head dim 64/128, behind the C ABI in include/hk_attn.h.
 """
 from .api import (  # noqa: F401
-    Attention, AttentionVarlen, HKError, attn_bwd, attn_bwd_varlen, attn_fwd, attn_fwd_varlen, bwd_workspace_bytes,
-    gemm, ln_dropout_residual, rope,
+    Attention, AttentionRope, AttentionVarlen, HKError, attn_bwd, attn_bwd_rope, attn_bwd_varlen, attn_fwd,
+    attn_fwd_rope, attn_fwd_varlen, bwd_workspace_bytes, gemm, ln_dropout_residual, rope,
 )

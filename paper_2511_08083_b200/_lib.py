@@ -36,6 +36,10 @@ SIGNATURES = {
     "hk_attn_bwd_varlen_workspace_bytes": (_Z, [_I, _I, _I, _I, _I, _I]),
     "hk_attn_bwd_varlen": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P, _P, _I, _I, _I, _I, _I, _I, _I,
                                 _I, _I, _P]),
+    "hk_attn_bwd_ex": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _I, _I, _I, _I, _I, _I, _I, ctypes.c_uint,
+                            _P]),
+    "hk_attn_bwd_varlen_ex": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P, _P, _I, _I, _I, _I, _I, _I, _I,
+                                   _I, _I, ctypes.c_uint, _P]),
     "hk_attn_merge": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P]),
     "hk_accum_bf16": (_I, [_P, _P, _P, _Z, _I, _P]),
     "hk_attn_last_error": (ctypes.c_char_p, []),
@@ -44,6 +48,8 @@ SIGNATURES = {
     "hk_gemm_bf16": (_I, [_P, _P, _P, _I, _I, _I, _P]),
     "hk_ln_dropout_residual": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, ctypes.c_float, ctypes.c_uint, ctypes.c_float, _P]),
     "hk_rope": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _P]),
+    "hk_rope_ex": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P]),
+    "hk_attn_fwd_rope": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
 }
 # include/hk_attn_diag.h (libhkattn_diag.so)
 DIAG_SIGNATURES = {

@@ -81,9 +81,15 @@ def bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk=None) -> int:
     return int(lib().hk_attn_bwd_qk_workspace_bytes(B, Hq, Hkv, N, Nk, d))
 
 
-def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None, dk=None, dv=None):
+HK_BWD_DETERMINISTIC = 1  # include/hk_attn.h
+
+
+def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None, dk=None, dv=None,
+             deterministic: bool = False):
     """dQ, dK, dV of L = sum(O * dO) for O = attention(q, k, v).
-    Returns (dq, dk, dv) bf16, plus the workspace holds D = rowsum(dO*O) then LSE*log2e."""
+    Returns (dq, dk, dv) bf16, plus the workspace holds D = rowsum(dO*O) then LSE*log2e.
+    d = 64 runs the fused single-pass backward unless `deterministic` (hk_attn.h: dQ is then
+    reproducible only up to fp32 reordering; dK, dV stay bitwise)."""
     for n, t in (("q", q), ("k", k), ("v", v), ("o", o), ("do", do)):
         _check_tensor(n, t)
     _check_tensor("lse", lse, torch.float32)
@@ -100,14 +106,9 @@ def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None,
     nbytes = bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk)
     ws = torch.empty(nbytes // 4, dtype=torch.float32, device=q.device) if workspace is None else workspace
     _check_workspace(ws, nbytes)
-    if N == Nk:
-        check(lib().hk_attn_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
-                                _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), B, Hq, Hkv, N, d,
-                                int(bool(causal)), _stream()))
-    else:
-        check(lib().hk_attn_bwd_qk(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
-                                   _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), B, Hq, Hkv, N, Nk, d,
-                                   int(bool(causal)), _stream()))
+    check(lib().hk_attn_bwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
+                               _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), B, Hq, Hkv, N, Nk, d,
+                               int(bool(causal)), HK_BWD_DETERMINISTIC if deterministic else 0, _stream()))
     return dq, dk, dv
 
 
@@ -166,8 +167,9 @@ def attn_fwd_varlen(q, k, v, cu_seqlens_q, cu_seqlens_k, max_seqlen_q: int, max_
 
 
 def attn_bwd_varlen(q, k, v, o, lse, do, cu_seqlens_q, cu_seqlens_k, max_seqlen_q: int, max_seqlen_k: int,
-                    causal: bool = False, workspace=None, dq=None, dk=None, dv=None):
-    """Backward of attn_fwd_varlen (hk_attn_bwd_varlen). Returns (dq, dk, dv) bf16."""
+                    causal: bool = False, workspace=None, dq=None, dk=None, dv=None, deterministic: bool = False):
+    """Backward of attn_fwd_varlen (hk_attn_bwd_varlen_ex). Returns (dq, dk, dv) bf16. `deterministic`
+    as in attn_bwd."""
     B, tq, tk, Hq, Hkv, d = _varlen_args(q, k, v, cu_seqlens_q, cu_seqlens_k)
     for n, t in (("o", o), ("do", do)):
         _check_tensor(n, t)
@@ -183,10 +185,11 @@ def attn_bwd_varlen(q, k, v, o, lse, do, cu_seqlens_q, cu_seqlens_k, max_seqlen_
     nbytes = int(lib().hk_attn_bwd_varlen_workspace_bytes(B, Hq, Hkv, int(max_seqlen_q), int(max_seqlen_k), d))
     ws = torch.empty(nbytes // 4, dtype=torch.float32, device=q.device) if workspace is None else workspace
     _check_workspace(ws, nbytes)
-    check(lib().hk_attn_bwd_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
-                                   _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), _ptr(cu_seqlens_q),
-                                   _ptr(cu_seqlens_k), B, Hq, Hkv, tq, tk, int(max_seqlen_q), int(max_seqlen_k), d,
-                                   int(bool(causal)), _stream()))
+    check(lib().hk_attn_bwd_varlen_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq),
+                                      _ptr(dk), _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(),
+                                      _ptr(cu_seqlens_q), _ptr(cu_seqlens_k), B, Hq, Hkv, tq, tk, int(max_seqlen_q),
+                                      int(max_seqlen_k), d, int(bool(causal)),
+                                      HK_BWD_DETERMINISTIC if deterministic else 0, _stream()))
     return dq, dk, dv
 
 
@@ -227,9 +230,9 @@ def ln_dropout_residual(x, residual, weight, bias, p: float = 0.0, seed: int = 0
     return o, r
 
 
-def rope(x, cos, sin, out=None):
+def rope(x, cos, sin, out=None, inverse: bool = False):
     """Rotary embedding (rotate-half) of x [B, N, H, d] bf16 with cos/sin [N, d/2] fp32
-    (include/hk_membound.h). `out` may be `x` (in place)."""
+    (include/hk_membound.h). `out` may be `x` (in place). inverse: rotate by -theta (hk_rope_ex)."""
     _check_tensor("x", x)
     _check_tensor("cos", cos, torch.float32)
     _check_tensor("sin", sin, torch.float32)
@@ -239,25 +242,76 @@ def rope(x, cos, sin, out=None):
     o = torch.empty_like(x) if out is None else out
     _check_tensor("out", o)
     _expect_shape("out", o, x.shape)
-    check(lib().hk_rope(_ptr(x), _ptr(cos), _ptr(sin), _ptr(o), B, N, H, d, _stream()))
+    check(lib().hk_rope_ex(_ptr(x), _ptr(cos), _ptr(sin), _ptr(o), B, N, H, d, int(bool(inverse)), _stream()))
     return o
 
 
+def attn_fwd_rope(q, k, v, cos, sin, causal: bool = False, out=None, lse=None, k_rot=None):
+    """O, LSE = attention(rope(q), rope(k), v) with the Q rotation fused into the forward kernel
+    (hk_attn_fwd_rope). q [B,N,Hq,d], k/v [B,N,Hkv,d] bf16; cos/sin [N, d/2] fp32. Returns
+    (o, lse, k_rot): k_rot = rope(k), which the backward (attn_bwd_rope) takes."""
+    for n, t in (("q", q), ("k", k), ("v", v)):
+        _check_tensor(n, t)
+    B, N, Nk, Hq, Hkv, d = _shapes(q, k, v)
+    if N != Nk:
+        raise ValueError("attn_fwd_rope is self-attention: q and k need the same N")
+    _check_tensor("cos", cos, torch.float32)
+    _check_tensor("sin", sin, torch.float32)
+    if cos.shape != (N, d // 2) or sin.shape != (N, d // 2):
+        raise ValueError("cos and sin must be [N, d/2]")
+    o = torch.empty_like(q) if out is None else out
+    L = torch.empty((B, Hq, N), dtype=torch.float32, device=q.device) if lse is None else lse
+    kr = torch.empty_like(k) if k_rot is None else k_rot
+    for n, t, shp, dt in (("out", o, q.shape, torch.bfloat16), ("lse", L, (B, Hq, N), torch.float32),
+                          ("k_rot", kr, k.shape, torch.bfloat16)):
+        _check_tensor(n, t, dt)
+        _expect_shape(n, t, shp)
+    check(lib().hk_attn_fwd_rope(_ptr(q), _ptr(k), _ptr(v), _ptr(cos), _ptr(sin), _ptr(o), _ptr(L), _ptr(kr), B, Hq,
+                                 Hkv, N, d, int(bool(causal)), _stream()))
+    return o, L, kr
+
+
+def attn_bwd_rope(q, k_rot, v, o, lse, do, cos, sin, causal: bool = False, deterministic: bool = False):
+    """Gradients of attention(rope(q), rope(k), v) w.r.t. the UNrotated q, k and v: the backward
+    runs on rope(q) and k_rot (from attn_fwd_rope) and maps dQ, dK back through the inverse
+    rotation (R^T = R(-theta)). Every step is a libhkattn kernel. Returns (dq, dk, dv)."""
+    qr = rope(q, cos, sin)
+    dqr, dkr, dv = attn_bwd(qr, k_rot, v, o, lse, do, causal, deterministic=deterministic)
+    return rope(dqr, cos, sin, out=dqr, inverse=True), rope(dkr, cos, sin, out=dkr, inverse=True), dv
+
+
 class Attention(torch.autograd.Function):
-    """autograd wrapper: Attention.apply(q, k, v, causal) -> o."""
+    """autograd wrapper: Attention.apply(q, k, v, causal, deterministic=False) -> o."""
 
     @staticmethod
-    def forward(ctx, q, k, v, causal=False):
+    def forward(ctx, q, k, v, causal=False, deterministic=False):
         o, lse = attn_fwd(q, k, v, causal)
         ctx.save_for_backward(q, k, v, o, lse)
-        ctx.causal = causal
+        ctx.causal, ctx.deterministic = causal, deterministic
         return o
 
     @staticmethod
     def backward(ctx, do):
         q, k, v, o, lse = ctx.saved_tensors
-        dq, dk, dv = attn_bwd(q, k, v, o, lse, do.contiguous(), ctx.causal)
-        return dq, dk, dv, None
+        dq, dk, dv = attn_bwd(q, k, v, o, lse, do.contiguous(), ctx.causal, deterministic=ctx.deterministic)
+        return dq, dk, dv, None, None
+
+
+class AttentionRope(torch.autograd.Function):
+    """autograd wrapper: AttentionRope.apply(q, k, v, cos, sin, causal) -> attention(rope(q), rope(k), v)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, cos, sin, causal=False):
+        o, lse, kr = attn_fwd_rope(q, k, v, cos, sin, causal)
+        ctx.save_for_backward(q, kr, v, o, lse, cos, sin)
+        ctx.causal = causal
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, kr, v, o, lse, cos, sin = ctx.saved_tensors
+        dq, dk, dv = attn_bwd_rope(q, kr, v, o, lse, do.contiguous(), cos, sin, ctx.causal)
+        return dq, dk, dv, None, None, None
 
 
 class AttentionVarlen(torch.autograd.Function):

@@ -41,7 +41,8 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
                                                       const __nv_bfloat16* __restrict__ dO,
                                                       const float* __restrict__ lse, float* __restrict__ Dout,
                                                       float* __restrict__ lse2, SeqGeom g, int H, int hshift,
-                                                      int Np, unsigned* __restrict__ sched) {
+                                                      int Np, unsigned* __restrict__ sched,
+                                                      float* __restrict__ dq_acc) {
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 4) sched[threadIdx.x] = 0u;
   constexpr int LPR = D / 8;  // lanes per row
   constexpr int RPW = 32 / LPR;
@@ -62,36 +63,41 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
 #define HK_PRE_U64 2
 #endif
   constexpr int U = D == 128 ? HK_PRE_U128 : HK_PRE_U64;  // measured (scripts/ab.py): 2 for both since the 32-bit (h, n) division
-  for (size_t base = gwarp * RPW * U; base < rows; base += nwarps * RPW * U) {
+  // One warp iteration's rows: their O / dO vectors, LSE and (h, n).
+  struct Grp {
     uint4 a[U], gv[U];
-    float L[U];  // LSE of the row (lane sub == 0), loaded with O / dO: not a dependent round trip later
-    int hh[U], nn[U];  // (h, n) of each row: one 32-bit division per row (rows * H < 2^31, validated)
+    float L[U];        // LSE of the row (lane sub == 0), loaded with O / dO: not a dependent round trip later
+    int hh[U], nn[U];  // (h, n) of each row (rows * H < 2^31, validated)
+  };
+  auto load = [&](size_t base, Grp& q) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const size_t row = base + u * RPW + lrow;
-      L[u] = 0.f;
+      q.L[u] = 0.f;
       const uint32_t r32 = (uint32_t)row;
       if (hshift >= 0) {  // H a power of two (every BASELINE config): shift and mask
-        nn[u] = (int)(r32 >> hshift);
-        hh[u] = (int)(r32 & (uint32_t)(H - 1));
+        q.nn[u] = (int)(r32 >> hshift);
+        q.hh[u] = (int)(r32 & (uint32_t)(H - 1));
       } else {
-        nn[u] = (int)(r32 / (uint32_t)H);
-        hh[u] = (int)(r32 - (uint32_t)nn[u] * (uint32_t)H);
+        q.nn[u] = (int)(r32 / (uint32_t)H);
+        q.hh[u] = (int)(r32 - (uint32_t)q.nn[u] * (uint32_t)H);
       }
       if (row < rows) {
-        a[u] = __ldcs(reinterpret_cast<const uint4*>(O + (row0 + row) * D) + sub);
-        gv[u] = __ldcs(reinterpret_cast<const uint4*>(dO + (row0 + row) * D) + sub);
-        if (sub == 0) L[u] = __ldg(lse + lse_index(g, sq, b, H, hh[u], nn[u]));
+        q.a[u] = __ldcs(reinterpret_cast<const uint4*>(O + (row0 + row) * D) + sub);
+        q.gv[u] = __ldcs(reinterpret_cast<const uint4*>(dO + (row0 + row) * D) + sub);
+        if (sub == 0) q.L[u] = __ldg(lse + lse_index(g, sq, b, H, q.hh[u], q.nn[u]));
       } else {
-        a[u] = gv[u] = make_uint4(0u, 0u, 0u, 0u);
+        q.a[u] = q.gv[u] = make_uint4(0u, 0u, 0u, 0u);
       }
     }
+  };
+  auto finish = [&](size_t base, const Grp& q) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const size_t row = base + u * RPW + lrow;
       float acc = 0.f;
-      const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&a[u]);
-      const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&gv[u]);
+      const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&q.a[u]);
+      const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&q.gv[u]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 x = __bfloat1622float2(ap[k]), y = __bfloat1622float2(gp[k]);
@@ -100,11 +106,38 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
       }
 #pragma unroll
       for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (row < rows && sub == 0) {
-        const size_t idx = ((size_t)b * H + hh[u]) * Np + nn[u];  // workspace rows are padded to Np
-        Dout[idx] = acc;
-        lse2[idx] = L[u] == -INFINITY ? INFINITY : L[u] * 1.4426950408889634f;
+      if (row < rows) {
+        if (sub == 0) {
+          const size_t idx = ((size_t)b * H + q.hh[u]) * Np + q.nn[u];  // workspace rows are padded to Np
+          Dout[idx] = acc;
+          lse2[idx] = q.L[u] == -INFINITY ? INFINITY : q.L[u] * 1.4426950408889634f;
+        }
+        if (dq_acc != nullptr) {  // fused backward: zero this row's fp32 dQ accumulator (8 floats per lane)
+          uint4* z = reinterpret_cast<uint4*>(dq_acc + (row0 + row) * D) + 2 * sub;
+          z[0] = z[1] = make_uint4(0u, 0u, 0u, 0u);
+        }
       }
+    }
+  };
+  const size_t stride = nwarps * RPW * U;
+#ifndef HK_PRE_PIPE
+#define HK_PRE_PIPE 1
+#endif
+  if (HK_PRE_PIPE) {  // software pipeline: the next iteration's loads are in flight while this one reduces
+    size_t base = gwarp * RPW * U;
+    Grp cur;
+    if (base < rows) load(base, cur);
+    for (; base < rows; base += stride) {
+      Grp nxt;
+      if (base + stride < rows) load(base + stride, nxt);
+      finish(base, cur);
+      cur = nxt;
+    }
+  } else {
+    for (size_t base = gwarp * RPW * U; base < rows; base += stride) {
+      Grp cur;
+      load(base, cur);
+      finish(base, cur);
     }
   }
   if (Np > sq.lq) {
@@ -114,6 +147,26 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
       Dout[idx] = 0.f;
       lse2[idx] = INFINITY;
     }
+  }
+}
+
+// Fused backward epilogue: dQ = bf16(dQ_acc / sqrt(d)) over the query rows of sequence b =
+// blockIdx.y (its rows beyond max_seqlen are left untouched, hk_attn.h), 8 elements per thread-step.
+template <int D>
+__global__ void __launch_bounds__(256) dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
+                                                         SeqGeom g, int H, float scale) {
+  const Seq sq = seq_of(g, blockIdx.y);
+  const size_t base = (size_t)sq.gq0 * H * (D / 8), n8 = (size_t)sq.lq * H * (D / 8);
+  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < n8; j += (size_t)gridDim.x * blockDim.x) {
+    const size_t i = base + j;
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(acc) + 2 * i);
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(acc) + 2 * i + 1);
+    uint4 o;
+    o.x = pack_bf16(a.x * scale, a.y * scale);
+    o.y = pack_bf16(a.z * scale, a.w * scale);
+    o.z = pack_bf16(b.x * scale, b.y * scale);
+    o.w = pack_bf16(b.z * scale, b.w * scale);
+    __stcs(reinterpret_cast<uint4*>(dq) + i, o);
   }
 }
 
@@ -166,6 +219,23 @@ struct BwdCfg {
 #endif
   static constexpr int NWG2 = ((D == 64 && HK_DQ_4WG) || (D == 128 && HK_BWD_4WG128)) ? 4 : 2;
   static constexpr int THREADS2 = 32 * (4 * NWG2 + 2);
+  // Fused single pass (d = 64 only): the dK/dV pass also forms
+  // dQ_partial = dS K_j per block on the tensor core (dS staged in shared memory as the MN-major A
+  // operand, accumulator in TMEM columns [384, 512), double-buffered) and a dQ warpgroup adds it
+  // into an fp32 dQ accumulator with the bulk-async tensor reduce (cp.reduce.async.bulk.tensor
+  // .add.f32, from a shared-memory staging tile); a convert pass scales and rounds it to bf16.
+  static constexpr uint32_t DS_TILE = 128 * 128 * 2;  // dS [128 keys][128 queries] bf16, two SW128 panels
+  static constexpr uint32_t DQ_STAGE = 128 * 64 * 4;  // dQ_partial [128 queries][64] fp32, two SW128 boxes
+  static constexpr int NSA_F = 4, NSB_F = 3;
+  static constexpr uint32_t BAR_BYTES_F = 512;
+  static constexpr uint32_t SMEM1F = 2 * T128 + NSA_F * T128 + NSB_F * SLOT_B1 + DS_TILE + DQ_STAGE + BAR_BYTES_F +
+                                     1024;
+  // 16 warps: two elementwise warpgroups (64 query columns per thread), TMA, MMA, two idle warps,
+  // four dQ warps — every SM sub-partition gets two elementwise warps and two others, so after
+  // setmaxnreg (elementwise 160, others 96) each holds exactly its 4 x 128 launch registers.
+  // (Four elementwise warpgroups, the two-pass d = 64 choice, would leave 80 registers each.)
+  static constexpr int NWG1F = 2;
+  static constexpr int THREADS1F = 512;
 };
 
 // SMEM descriptor helpers for [rows][D] bf16 tiles stored as D/64 panels of rows x 128 B.
@@ -268,21 +338,24 @@ __device__ __forceinline__ KvItem kv_decode(const BwdParams& p, int item) {
   return it;
 }
 
-template <int D, bool CAUSAL>
-__global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
+template <int D, bool CAUSAL, bool FQ>
+__global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS1, 1)
     bwd_dkdv_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapdO,
                     const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
-                    const BwdParams p) {
+                    const __grid_constant__ CUtensorMap mapDQ, const BwdParams p) {
   using C = BwdCfg<D>;
-  constexpr int NSA = C::NSA, NSB = C::NSB;
+  static_assert(!FQ || D == 64, "the fused dQ pass is built for d = 64");
+  constexpr int NSA = FQ ? C::NSA_F : C::NSA, NSB = FQ ? C::NSB_F : C::NSB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  if (C::SLACK1 == 0 && smem != smem_raw) __trap();  // the D=128 layout has no alignment slack
+  if (C::SLACK1 == 0 && !FQ && smem != smem_raw) __trap();  // the D=128 layout has no alignment slack
   uint8_t* sK = smem;
   uint8_t* sV = smem + C::T128;
   uint8_t* sA = smem + 2 * C::T128;   // ring A slot s: Q [T128]
   uint8_t* sB = sA + NSA * C::T128;   // ring B slot s: dO [T128] lse2 [512 B] D [512 B]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NSB * C::SLOT_B1);
+  uint8_t* sDS = sB + NSB * C::SLOT_B1;                 // FQ: dS tile (MN-major A of dQ_partial = dS K)
+  uint8_t* sDQ = sDS + (FQ ? C::DS_TILE : 0);           // FQ: dQ_partial staging for the bulk reduce
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDQ + (FQ ? C::DQ_STAGE : 0));
   uint64_t* fullA = bars;             // [NSA]
   uint64_t* emptyA = bars + NSA;      // [NSA]
   uint64_t* fullB = bars + 2 * NSA;   // [NSB]
@@ -296,17 +369,30 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
   uint64_t& bar_kvfree = emptyB[NSB + 6];
   uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(emptyB + NSB + 7);
   Sched& sched = *reinterpret_cast<Sched*>(emptyB + NSB + 8);
-  static_assert((2 * NSA + 2 * NSB + 8) * 8 + sizeof(Sched) <= C::BAR_BYTES, "barrier area");
+  uint64_t* fq_bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(&sched) + sizeof(Sched));
+  uint64_t& bar_dsfree = fq_bars[0];  // FQ: dQ_partial(u) MMA done reading the dS tile
+  uint64_t* bar_dqfull = fq_bars + 1;   // FQ [2]: dQ_partial in TMEM buffer b complete
+  uint64_t* bar_dqempty = fq_bars + 3;  // FQ [2]: TMEM buffer b read out by the dQ warpgroup
+  static_assert((2 * NSA + 2 * NSB + 8) * 8 + sizeof(Sched) + (FQ ? 5 * 8 : 0) <=
+                    (FQ ? C::BAR_BYTES_F : C::BAR_BYTES), "barrier area");
 
   const int warp = warp_id(), lane = lane_id();
-  constexpr int NWG = C::NWG1;            // elementwise warpgroups
+  constexpr int NWG = FQ ? C::NWG1F : C::NWG1;  // elementwise warpgroups
   constexpr int CW = 128 / NWG;           // query columns per elementwise thread
   constexpr int WTMA = 4 * NWG, WMMA = 4 * NWG + 1;
+  constexpr int WDQ = 12;                 // FQ: the four dQ warps 12-15 (one per TMEM lane quadrant)
   const int G = p.Hq / p.Hkv;
   const int num_items = p.B * p.Hkv * (p.Npk / 128);
 
   if (threadIdx.x == 0) {
-    sched_init(sched, 1 + 4 * NWG);
+    sched_init(sched, 1 + 4 * NWG + (FQ ? 4 : 0));
+    if (FQ) {
+      mbar_init(&bar_dsfree, 1);
+      for (int b2 = 0; b2 < 2; ++b2) {
+        mbar_init(&bar_dqfull[b2], 1);
+        mbar_init(&bar_dqempty[b2], 4);
+      }
+    }
     mbar_init(&bar_kv, 1);
     mbar_init(&bar_kvfree, 1);
     for (int s = 0; s < NSA; ++s) {
@@ -329,6 +415,7 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
     tma_prefetch(&mapdO);
     tma_prefetch(&mapK);
     tma_prefetch(&mapV);
+    if (FQ) tma_prefetch(&mapDQ);
   }
   if (warp == WMMA) tmem_alloc<512>(&tmem_base_s);
   tc_fence_before();
@@ -336,10 +423,14 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
   tc_fence_after();
   const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base_s, 0);  // warp-uniform for ptxas (UR operands)
   const uint32_t tdV = tb, tdK = tb + D, tS = tb + 2 * D, tP = tb + 2 * D + 128;
+  const uint32_t tdQ = tb + 2 * D + 256;  // FQ: two 64-column dQ_partial buffers
+  // FQ: 512 threads launch at 128 registers; each role re-sizes at the top of its branch (ptxas
+  // allocates per region): per sub-partition 2 x 160 (elementwise) + 2 x 96 = 4 x 128.
 
   // All roles walk the same items; ring uses and barrier phases run on across items.
   if (warp == WTMA) {
     // ================= TMA producer =================
+    if constexpr (FQ) reg_dealloc<96>();
     if (lane == 0) {
       const uint64_t pol_keep = policy_evict_last();
       const uint64_t pol_stream = policy_evict_normal();
@@ -390,6 +481,7 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
     }
   } else if (warp == WMMA) {
     // ================= MMA issuer (whole warp, one elected lane issues) =================
+    if constexpr (FQ) reg_dealloc<96>();
     constexpr uint32_t idesc_sp = idesc_bf16(128, 128, 0, 0);  // S^T / dP^T: M=128 keys, N=128 queries
     constexpr uint32_t idesc_acc = idesc_bf16(128, D, 0, 1);   // dV / dK: B = dO_i / Q_i MN-major
     constexpr uint64_t KMAJ = sdesc_sw128_const(16, 1024);
@@ -426,7 +518,7 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
       mbar_wait(&fullB[u0 % NSB], (u0 / NSB) & 1);
       tc_fence_after();
       issue_dp(u0);
-      if (n == 1) tc_commit_w(&bar_kvfree);
+      if (!FQ && n == 1) tc_commit_w(&bar_kvfree);
       for (int it = 0; it < n; ++it) {
         const int u = u0 + it;
         const uint32_t q = slotQ(u), dO = slotO(u);
@@ -459,7 +551,16 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
           mbar_wait(&fullB[(u + 1) % NSB], ((u + 1) / NSB) & 1);
           tc_fence_after();
           issue_dp(u + 1);
-          if (it + 2 == n) tc_commit_w(&bar_kvfree);  // last S^T and dP^T issued
+          if (!FQ && it + 2 == n) tc_commit_w(&bar_kvfree);  // last S^T and dP^T issued
+        }
+        if constexpr (FQ) {  // dQ_partial(it) = dS(it) K_j into TMEM buffer u % 2 (the dQ warps drained it)
+          constexpr uint32_t idesc_dq = idesc_bf16(128, D, 1, 1);  // M = 128 queries, A = dS MN-major
+          mbar_wait(&bar_dqempty[u & 1], ((u >> 1) & 1) ^ 1);
+          tc_fence_after();
+          gemm_ss_mnmn(tdQ + 64 * (u & 1), mnmaj(smem_u32(sDS), 0), mnmaj(aK, 0), idesc_dq, 0u);
+          tc_commit_w(&bar_dqfull[u & 1]);
+          tc_commit_w(&bar_dsfree);
+          if (it + 1 == n) tc_commit_w(&bar_kvfree);  // K_j's last use
         }
       }
       tc_commit_w(&bar_acc);
@@ -469,8 +570,60 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
     drain_ring(emptyA, NSA, u0);
     drain_ring(emptyB, NSB, u0);
     if (busy > 0) mbar_wait(&bar_kvfree, (busy - 1) & 1);
-  } else {
+    if (FQ && u0 > 0) mbar_wait(&bar_dsfree, (u0 - 1) & 1);  // the last dS-tile release
+  } else if (FQ && warp >= WDQ) {
+    // ================= dQ warpgroup (FQ): TMEM dQ_partial -> staging -> bulk tensor reduce-add =================
+    reg_dealloc<96>();
+    const int qd = warp & 3;                // TMEM lane quadrant of this warp
+    const int r = qd * 32 + lane;           // query row within the 128-row tile
+    const bool issuer = warp == WDQ && lane == 0;
+    int u = 0;
+    for (int rr = 0;; ++rr) {
+      const int item = sched_take(sched, rr);
+      if (item >= num_items) break;
+      const KvItem w = kv_decode<CAUSAL>(p, item);
+      if (w.n_it == 0) continue;
+      int h = w.kvh * G, qi = w.i0;
+      for (int it = 0; it < w.n_it; ++it, ++u) {
+        const uint32_t b2 = u & 1;
+        mbar_wait(&bar_dqfull[b2], (u >> 1) & 1);
+        tc_fence_after();
+        if (issuer) tma_store_wait_read0();  // the previous reduce has read the staging tile
+        named_bar_sync(3, 128);
+        // 32 columns at a time (704 threads leave 88 registers each): row r of the [128][32] fp32
+        // box bx, SWIZZLE_128B (16-B chunk c at c ^ (r % 8))
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx) {
+          uint32_t v[32];
+          tmem_ld32(tmem_addr(tdQ + 64 * b2, qd * 32, 32 * bx), v);
+          tmem_wait_ld();
+          if (bx == 1) {  // TMEM buffer read out: the next-but-one dQ_partial may overwrite it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_dqempty[b2]);
+          }
+          const uint32_t rowp = smem_u32(sDQ) + bx * (128 * 128) + r * 128;
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8)
+            sts_v4(rowp + ((c8 ^ (r & 7)) << 4), v[4 * c8], v[4 * c8 + 1], v[4 * c8 + 2], v[4 * c8 + 3]);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(3, 128);
+        if (issuer) {
+          for (int bx = 0; bx < 2; ++bx)
+            tma_reduce_add_4d(&mapDQ, sDQ + bx * (128 * 128), 32 * bx, h, w.sq.q0 + qi * 128, w.sq.tb);
+          tma_store_commit();
+        }
+        if (++qi == w.nqt) {
+          qi = w.i0;
+          ++h;
+        }
+      }
+    }
+    if (issuer) tma_store_wait0();  // every reduce complete before the CTA exits
+  } else if (warp < 4 * NWG) {
     // ================= elementwise warpgroups (warps 0 .. 4 NWG - 1) =================
+    if constexpr (FQ) reg_alloc<160>();
     const int wg = warp >> 2;              // query columns [CW wg, CW wg + CW) of each block
     const uint32_t lb = (warp & 3) * 32;   // TMEM lane base
     const int r = (warp & 3) * 32 + lane;  // key row within the tile
@@ -556,7 +709,32 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
           dp[c4 + 2] = b.x;
           dp[c4 + 3] = b.y;
         }
-        tmem_st_packed_cols<CW>(tmem_addr(cP, lb, 0), dp);
+        if constexpr (FQ) {
+          // a key row beyond the sequence (varlen: the next sequence's keys in this tile) must add
+          // nothing to dQ: its dS row is zeroed (its dK, dV rows are never stored)
+          if (!key_ok) {
+#pragma unroll
+            for (int cc = 0; cc < CW; ++cc) dp[cc] = 0.f;
+          }
+          uint32_t pk[CW / 2];
+#pragma unroll
+          for (int c2 = 0; c2 < CW / 2; ++c2) pk[c2] = pack_bf16(dp[2 * c2], dp[2 * c2 + 1]);
+          if constexpr (CW == 64)
+            tmem_st32(tmem_addr(cP, lb, 0), *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+          else
+            tmem_st16(tmem_addr(cP, lb, 0), pk);
+          // dS row r (a key) = the K-row r of the MN-major A operand: queries [CW wg, CW wg + CW) sit
+          // in panel CW wg / 64, 16-B chunks from (CW wg % 64) / 8, SWIZZLE_128B (chunk c at c ^ (r % 8))
+          if (u > 0) mbar_wait(&bar_dsfree, (u & 1) ^ 1);  // dQ_partial(u - 1) has read the tile
+          const uint32_t rowp = smem_u32(sDS) + ((CW * wg) >> 6) * (128 * 128) + r * 128;
+          const int c0 = ((CW * wg) & 63) >> 3;
+#pragma unroll
+          for (int k = 0; k < CW / 8; ++k)
+            sts_v4(rowp + (((c0 + k) ^ (r & 7)) << 4), pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+          fence_proxy_async_smem();  // generic-proxy stores visible to the tensor core
+        } else {
+          tmem_st_packed_cols<CW>(tmem_addr(cP, lb, 0), dp);
+        }
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -588,6 +766,8 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS1, 1)
         }
       }
     }
+  } else if constexpr (FQ) {
+    reg_dealloc<96>();  // the two idle warps (10, 11) give their share to the elementwise warps
   }
   tc_fence_before();
   __syncthreads();
@@ -984,7 +1164,17 @@ struct BwdShape {
   const int* cu_k;
   int B, Hq, Hkv, Nq, Nk;  // varlen: Nq, Nk = max_seqlen_q, max_seqlen_k
   int total_q, total_k;    // varlen only
+  bool fused;              // d = 64: single-pass dQ (bulk reduce-add into the fp32 accumulator) — not bitwise
 };
+
+// Workspace layout of one backward call (hk_attn.h): D and LSE2 [B][Hq][Np] fp32, 256 bytes of work
+// counters, then (d = 64) the fused backward's fp32 dQ accumulator: B * Np * Hq * 64 floats, which
+// covers [B][Nq][Hq][64] (dense) and [total_q][Hq][64] (varlen: total_q <= B * max_seqlen_q).
+inline size_t bwd_ws_bytes(int B, int Hq, int Nq, int d) {
+  if (B <= 0 || Hq <= 0 || Nq <= 0) return 0;
+  const size_t Np = ((size_t)Nq + 127) / 128 * 128;
+  return (size_t)2 * B * Hq * Np * sizeof(float) + 256 + (d == 64 ? (size_t)B * Np * Hq * 64 * sizeof(float) : 0);
+}
 
 template <int D, bool CAUSAL>
 hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,
@@ -1013,7 +1203,9 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);
     if (!done.count(dev)) {
-      if (!set_smem(bwd_dkdv_kernel<D, CAUSAL>, C::SMEM1) || !set_smem(bwd_dq_kernel<D, CAUSAL>, C::SMEM2)) {
+      bool ok2 = set_smem(bwd_dkdv_kernel<D, CAUSAL, false>, C::SMEM1) && set_smem(bwd_dq_kernel<D, CAUSAL>, C::SMEM2);
+      if constexpr (D == 64) ok2 = ok2 && set_smem(bwd_dkdv_kernel<D, CAUSAL, true>, C::SMEM1F);
+      if (!ok2) {
         snprintf(err, errlen, "cudaFuncSetAttribute(max dynamic smem) failed");
         return HK_ERR_DEVICE;
       }
@@ -1021,6 +1213,13 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     }
   }
   unsigned* sched = reinterpret_cast<unsigned*>(ws + (size_t)2 * B * Hq * Np);  // 4 counters after D, LSE2
+  const bool fq = D == 64 && sh.fused;
+  float* dq_acc = fq ? ws + (size_t)2 * B * Hq * Np + 64 : nullptr;  // after the 256-byte counter block
+  CUtensorMap mDQ = mK;  // unused by the two-pass kernels
+  if (fq && !encode_bnhd_f32(&mDQ, dq_acc, mb, mnq, Hq, D)) {
+    snprintf(err, errlen, "cuTensorMapEncodeTiled (dQ accumulator) failed (CUresult %d)", last_encode_result());
+    return HK_ERR_DEVICE;
+  }
   SeqGeom g{sh.cu_q, sh.cu_k, sh.Nq, sh.Nk, sh.total_q};
   BwdParams p{Dv,
               lse2,
@@ -1045,13 +1244,13 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   if (phase < 0 || phase == 0)
     bwd_pre_kernel<D><<<dim3((unsigned)bx, (unsigned)B), 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(O), reinterpret_cast<const __nv_bfloat16*>(dO), LSE, Dv, lse2, g, Hq,
-        (Hq & (Hq - 1)) == 0 ? __builtin_ctz((unsigned)Hq) : -1, Np, sched);
+        (Hq & (Hq - 1)) == 0 ? __builtin_ctz((unsigned)Hq) : -1, Np, sched, dq_acc);
   // B1, B2. They are independent (both only read the preprocess output): with HK_BWD_FORK the dQ
   // pass goes on a side stream forked from `stream` after B0 and joined back after it, so its
   // CTAs take the SMs the dK/dV pass's last CTAs free instead of waiting for the whole pass.
   cudaStream_t s2 = stream;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (HK_BWD_FORK && phase < 0) {
+  if (HK_BWD_FORK && phase < 0 && !fq) {
     s2 = side_stream(stream);
     if (s2 && cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) == cudaSuccess &&
         cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) == cudaSuccess &&
@@ -1063,10 +1262,21 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   }
   if (phase < 0 || phase == 1) {
     const int items = B * Hkv * (Npk / 128);  // persistent: one CTA per SM
-    bwd_dkdv_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS1, C::SMEM1, stream>>>(mQ, mdO, mK,
-                                                                                                    mV, p);
+    const int grid = items < num_sms ? items : num_sms;
+    if constexpr (D == 64) {
+      if (fq)
+        bwd_dkdv_kernel<D, CAUSAL, true><<<grid, C::THREADS1F, C::SMEM1F, stream>>>(mQ, mdO, mK, mV, mDQ, p);
+      else
+        bwd_dkdv_kernel<D, CAUSAL, false><<<grid, C::THREADS1, C::SMEM1, stream>>>(mQ, mdO, mK, mV, mDQ, p);
+    } else {
+      bwd_dkdv_kernel<D, CAUSAL, false><<<grid, C::THREADS1, C::SMEM1, stream>>>(mQ, mdO, mK, mV, mDQ, p);
+    }
   }
-  if (phase < 0 || phase == 2) {
+  if (fq && (phase < 0 || phase == 2)) {  // dQ = bf16(dQ_acc / sqrt(d)), grid (x, sequence) like B0
+    dq_convert_kernel<D><<<dim3((unsigned)bx, (unsigned)B), 256, 0, stream>>>(
+        dq_acc, reinterpret_cast<__nv_bfloat16*>(dQ), g, Hq, rsqrtf((float)D));
+  }
+  if (!fq && (phase < 0 || phase == 2)) {
     const int items = B * Hq * (Np / 128);  // persistent: one CTA per SM
     bwd_dq_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS2, C::SMEM2, s2>>>(mQ, mdO, mK, mV,
                                                                                              p);

@@ -29,6 +29,7 @@
 #include "ptx.cuh"
 #include "sched.cuh"
 #include "seq.cuh"
+#include "rope.cuh"
 #include "softmax.cuh"
 
 namespace hk {
@@ -41,6 +42,8 @@ struct FwdParams {
   int num_pairs;  // ceil(Nq / 256): Q-tile pairs per head (varlen: of the longest sequence)
   int num_items;  // B * Hq * num_pairs work items
   unsigned* sched;  // [2] work counters: dynamic scheduling (varlen with a workspace); nullptr = static snake
+  const float* rope_cos;  // ROPE: [N][D/2] fp32 (position = query row), the fused rotary of Q
+  const float* rope_sin;
 };
 
 template <int D>
@@ -124,7 +127,10 @@ __device__ __forceinline__ int fwd_next_busy(const FwdParams& p, int r, int cta,
   }
 }
 
-template <int D, bool CAUSAL>
+// ROPE (NEXT #3, hk_attn_fwd_rope): warps 10-11 (otherwise idle) rotate each item's Q tiles in
+// shared memory right after they land (rotate-half, rope.cuh: the same arithmetic as hk_rope) and
+// publish them on bar_qr, which the MMA warp waits on instead of bar_q; K arrives pre-rotated.
+template <int D, bool CAUSAL, bool ROPE>
 __global__ void __launch_bounds__(384, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
                const __grid_constant__ CUtensorMap mapV, const FwdParams p) {
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sV = sK + NS * TB;   // NS tiles
 
   __shared__ uint64_t bar_q, bar_qfree, bar_kfull[NS], bar_kempty[NS], bar_vfull[NS], bar_vempty[NS];
-  __shared__ uint64_t bar_s[2], bar_p[2], bar_pl[2], bar_o[2], bar_oempty[2], bar_sfree[2], bar_pv[2];
+  __shared__ uint64_t bar_s[2], bar_p[2], bar_pl[2], bar_o[2], bar_oempty[2], bar_sfree[2], bar_pv[2], bar_qr;
   __shared__ uint32_t tmem_base_s;
   __shared__ Sched sched;
 
@@ -150,8 +156,9 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) hk_trace(30, 0, 0);  // CTA start
 
   if (threadIdx.x == 0) {
-    sched_init(sched);
+    sched_init(sched, ROPE ? 11 : 9);
     mbar_init(&bar_q, 1);
+    mbar_init(&bar_qr, 2);  // ROPE: both rotary warps
     mbar_init(&bar_qfree, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bar_kfull[s], 1);
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__(384, 1)
         const bool last_item = !dyn && rn < 0;
         uses += it.nkv;
         ++busy;
-        mbar_wait(&bar_q, q_ph);
+        mbar_wait(ROPE ? &bar_qr : &bar_q, q_ph);  // ROPE: Q landed and rotated
         q_ph ^= 1;
         mbar_wait(&bar_kfull[s], ph);
         tc_fence_after();
@@ -367,6 +374,62 @@ __global__ void __launch_bounds__(384, 1)
           mbar_wait(&bar_vempty[k], (last / NS) & 1);
         }
         if (busy > 0) mbar_wait(&bar_qfree, (busy - 1) & 1);
+      }
+    } else if (ROPE && warp >= 10) {
+      // ================= fused rotary of Q (warps 10-11) =================
+      // A row's elements i and i + D/2 sit in the same 16-B chunk slot of the two 64-column
+      // panels (D = 128) or in chunks c and c + 4 of its one 128-B row (D = 64), both at the
+      // 128B-swizzled position (chunk ^ (row % 8)).
+      constexpr int CPR = D / 16;  // chunk pairs per row
+      const int tid = (warp - 10) * 32 + lane;
+      const uint32_t q_base = smem_u32(sQ);
+      uint32_t q_ph = 0;
+      int rn = dyn ? 0 : fwd_next_busy<CAUSAL>(p, 0, cta, ctas);
+      for (;;) {
+        int item;
+        if (dyn) {
+          item = sched_take(sched, rn++);
+          if (item >= p.num_items) break;
+        } else {
+          if (rn < 0) break;
+          item = fwd_item_index<CAUSAL>(rn, cta, ctas);
+          rn = fwd_next_busy<CAUSAL>(p, rn + 1, cta, ctas);
+        }
+        const FwdItem it = fwd_decode<CAUSAL>(p, item);
+        if (it.nkv == 0) continue;
+        mbar_wait(&bar_q, q_ph);
+        q_ph ^= 1;
+#pragma unroll 1
+        for (int t = 0; t < 2; ++t) {
+          if ((t == 0 ? it.nkv0 : it.nkv1) == 0) continue;  // tile not loaded
+          const int qt = t == 0 ? it.qt0 : it.qt1;
+          const uint32_t tile = q_base + t * TB;
+#pragma unroll 2
+          for (int u = tid; u < 128 * CPR; u += 64) {
+            const int r = u / CPR, c = u % CPR;
+            const int n = qt * 128 + r;  // position of the query row
+            if (n >= it.sq.lq) continue;
+            const uint32_t alo = tile + r * 128 + ((c ^ (r & 7)) << 4);
+            const uint32_t ahi = D == 128 ? tile + 128 * 128 + r * 128 + ((c ^ (r & 7)) << 4)
+                                          : tile + r * 128 + (((c + 4) ^ (r & 7)) << 4);
+            uint4 va, vb;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(va.x), "=r"(va.y), "=r"(va.z), "=r"(va.w)
+                         : "r"(alo));
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(vb.x), "=r"(vb.y), "=r"(vb.z), "=r"(vb.w)
+                         : "r"(ahi));
+            float a[8], b[8], cs[8], sn[8], lo[8], hi[8];
+            unpack8(va, a);
+            unpack8(vb, b);
+            rope_load_cs(p.rope_cos, p.rope_sin, (size_t)n, D / 2, c, 1.f, cs, sn);
+            rope_pair8(a, b, cs, sn, lo, hi);
+            const uint4 wa = pack8(lo), wb = pack8(hi);
+            sts_v4(alo, wa.x, wa.y, wa.z, wa.w);
+            sts_v4(ahi, wb.x, wb.y, wb.z, wb.w);
+          }
+        }
+        fence_proxy_async_smem();  // generic-proxy stores visible to the tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_qr);
       }
     }
   } else {

@@ -16,6 +16,43 @@
 #include "membound.cuh"
 #include "ring.cuh"
 
+// Rotary launch shared by hk_rope(_ex) and hk_attn_fwd_rope (arguments validated by the caller).
+static hk_status rope_launch(const void* x, const float* cos, const float* sin, void* out, int B, int N, int H, int d,
+                             float sgn, int num_sms, cudaStream_t stream) {
+  const size_t bytes = (size_t)B * N * H * d * 2;
+  hk::RopeParams q;
+  q.x = reinterpret_cast<const __nv_bfloat16*>(x);
+  q.cos = cos;
+  q.sin = sin;
+  q.out = reinterpret_cast<__nv_bfloat16*>(out);
+  q.rows = (size_t)B * N * H;
+  q.N = N;
+  q.H = H;
+  q.d = d;
+  q.sgn = sgn;
+  // inputs beyond L2 (126 MB): the head-loop form loads each position's cos/sin once for all H
+  // heads (1.08-1.13x at 268 MB / 1 GB); smaller ones stay with one thread per (row, chunk)
+  // (the head loop leaves too few threads there: 0.91x at 67 MB). Same results either way.
+  if (bytes > ((size_t)126 << 20)) {
+    const size_t threads = (size_t)B * N * (d / 16);
+    size_t blocks = (threads + 255) / 256;
+    if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
+    if (threads < ((size_t)1 << 31))
+      hk::rope_hloop_kernel<uint32_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
+    else
+      hk::rope_hloop_kernel<size_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
+    return launched("hk_rope");
+  }
+  const size_t threads = q.rows * (d / 16);
+  size_t blocks = (threads + 255) / 256;
+  if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
+  if (threads < ((size_t)1 << 31))
+    hk::rope_kernel<uint32_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
+  else
+    hk::rope_kernel<size_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
+  return launched("hk_rope");
+}
+
 extern "C" {
 
 const char* hk_attn_last_error(void) { return g_err; }
@@ -31,7 +68,7 @@ const char* hk_status_string(hk_status s) {
   return "HK_ERR_UNKNOWN";
 }
 
-int hk_attn_abi_version(void) { return 3; }  // 2: + Nq != Nk and varlen entry points
+int hk_attn_abi_version(void) { return 4; }  // 2: + Nq != Nk and varlen; 4: + _ex (flags), fused d=64 bwd, rope
 
 hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, float* LSE, int B, int Hq, int Hkv,
                       int N, int d, int causal, cudaStream_t stream) {
@@ -43,8 +80,7 @@ hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, floa
 }
 size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d) {
   (void)Hkv;
-  (void)d;
-  return ws_bytes(B, Hq, N);
+  return ws_bytes(B, Hq, N, d);
 }
 hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,
                       void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes, int B, int Hq, int Hkv,
@@ -59,8 +95,7 @@ hk_status hk_attn_fwd_qk(const void* Q, const void* K, const void* V, void* O, f
 size_t hk_attn_bwd_qk_workspace_bytes(int B, int Hq, int Hkv, int Nq, int Nk, int d) {
   (void)Hkv;
   (void)Nk;
-  (void)d;
-  return ws_bytes(B, Hq, Nq);
+  return ws_bytes(B, Hq, Nq, d);
 }
 hk_status hk_attn_bwd_qk(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                          const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes, int B,
@@ -83,8 +118,7 @@ hk_status hk_attn_fwd_varlen(const void* Q, const void* K, const void* V, void* 
 size_t hk_attn_bwd_varlen_workspace_bytes(int B, int Hq, int Hkv, int max_seqlen_q, int max_seqlen_k, int d) {
   (void)Hkv;
   (void)max_seqlen_k;
-  (void)d;
-  return ws_bytes(B, Hq, max_seqlen_q);
+  return ws_bytes(B, Hq, max_seqlen_q, d);
 }
 hk_status hk_attn_bwd_varlen(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                              const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
@@ -99,6 +133,26 @@ hk_status hk_attn_bwd_varlen(const void* Q, const void* K, const void* V, const 
                   packed(cu_seqlens_q, cu_seqlens_k, B, Hq, Hkv, total_q, total_k, max_seqlen_q, max_seqlen_k), d,
                   causal, stream);
 }
+hk_status hk_attn_bwd_ex(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                         const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes, int B,
+                         int Hq, int Hkv, int Nq, int Nk, int d, int causal, unsigned flags, cudaStream_t stream) {
+  return bwd_impl(-1, Q, K, V, O, LSE, dO, dQ, dK, dV, workspace, workspace_bytes, dense(B, Hq, Hkv, Nq, Nk), d,
+                  causal, stream, flags);
+}
+hk_status hk_attn_bwd_varlen_ex(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
+                                const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
+                                const int* cu_seqlens_q, const int* cu_seqlens_k, int B, int Hq, int Hkv, int total_q,
+                                int total_k, int max_seqlen_q, int max_seqlen_k, int d, int causal, unsigned flags,
+                                cudaStream_t stream) {
+  if (!cu_seqlens_q || !cu_seqlens_k) {
+    g_err[0] = 0;
+    return fail(HK_ERR_INVALID_ARGUMENT, "null cu_seqlens");
+  }
+  return bwd_impl(-1, Q, K, V, O, LSE, dO, dQ, dK, dV, workspace, workspace_bytes,
+                  packed(cu_seqlens_q, cu_seqlens_k, B, Hq, Hkv, total_q, total_k, max_seqlen_q, max_seqlen_k), d,
+                  causal, stream, flags);
+}
+
 hk_status hk_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, cudaStream_t stream) {
   g_err[0] = 0;
   if (M <= 0 || N <= 0 || K <= 0) return fail(HK_ERR_INVALID_ARGUMENT, "M, N, K must be positive (%d, %d, %d)", M, N, K);
@@ -186,8 +240,8 @@ hk_status hk_ln_dropout_residual(const void* x, const void* residual, const void
   return launched("hk_ln_dropout_residual");
 }
 
-hk_status hk_rope(const void* x, const float* cos, const float* sin, void* out, int B, int N, int H, int d,
-                  cudaStream_t stream) {
+hk_status hk_rope_ex(const void* x, const float* cos, const float* sin, void* out, int B, int N, int H, int d,
+                     int inverse, cudaStream_t stream) {
   g_err[0] = 0;
   if (B <= 0 || N <= 0 || H <= 0 || d <= 0) return fail(HK_ERR_INVALID_ARGUMENT, "B, N, H, d must be positive");
   if (!x || !cos || !sin || !out) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
@@ -199,36 +253,38 @@ hk_status hk_rope(const void* x, const float* cos, const float* sin, void* out, 
   int num_sms = 0;
   hk_status s = check_device(&num_sms);
   if (s != HK_OK) return s;
-  hk::RopeParams q;
-  q.x = reinterpret_cast<const __nv_bfloat16*>(x);
-  q.cos = cos;
-  q.sin = sin;
-  q.out = reinterpret_cast<__nv_bfloat16*>(out);
-  q.rows = (size_t)B * N * H;
-  q.N = N;
-  q.H = H;
-  q.d = d;
-  // inputs beyond L2 (126 MB): the head-loop form loads each position's cos/sin once for all H
-  // heads (1.08-1.13x at 268 MB / 1 GB); smaller ones stay with one thread per (row, chunk)
-  // (the head loop leaves too few threads there: 0.91x at 67 MB). Same results either way.
-  if (bytes > ((size_t)126 << 20)) {
-    const size_t threads = (size_t)B * N * (d / 16);
-    size_t blocks = (threads + 255) / 256;
-    if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
-    if (threads < ((size_t)1 << 31))
-      hk::rope_hloop_kernel<uint32_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
-    else
-      hk::rope_hloop_kernel<size_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
-    return launched("hk_rope");
-  }
-  const size_t threads = q.rows * (d / 16);
-  size_t blocks = (threads + 255) / 256;
-  if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
-  if (threads < ((size_t)1 << 31))
-    hk::rope_kernel<uint32_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
-  else
-    hk::rope_kernel<size_t><<<(unsigned)blocks, 256, 0, stream>>>(q);
-  return launched("hk_rope");
+  return rope_launch(x, cos, sin, out, B, N, H, d, inverse ? -1.f : 1.f, num_sms, stream);
+}
+
+hk_status hk_rope(const void* x, const float* cos, const float* sin, void* out, int B, int N, int H, int d,
+                  cudaStream_t stream) {
+  return hk_rope_ex(x, cos, sin, out, B, N, H, d, 0, stream);
+}
+
+hk_status hk_attn_fwd_rope(const void* Q, const void* K, const void* V, const float* cos, const float* sin, void* O,
+                           float* LSE, void* Kr, int B, int Hq, int Hkv, int N, int d, int causal,
+                           cudaStream_t stream) {
+  g_err[0] = 0;
+  if (N <= 0) return fail(HK_ERR_INVALID_ARGUMENT, "N must be positive (got %d)", N);
+  if (!cos || !sin || !Kr || !K) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (!aligned16(cos) || !aligned16(sin) || !aligned16(Kr))
+    return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  if (B <= 0 || Hkv <= 0) return fail(HK_ERR_INVALID_ARGUMENT, "B, Hkv must be positive");
+  const size_t kv_bytes = (size_t)B * N * Hkv * d * 2, q_bytes = (size_t)B * N * Hq * d * 2;
+  if (overlaps(Kr, kv_bytes, K, kv_bytes) || (V && overlaps(Kr, kv_bytes, V, kv_bytes)) ||
+      (Q && overlaps(Kr, kv_bytes, Q, q_bytes)) || (O && overlaps(Kr, kv_bytes, O, q_bytes)) ||
+      (LSE && overlaps(Kr, kv_bytes, LSE, (size_t)B * Hq * N * 4)))
+    return fail(HK_ERR_INVALID_ARGUMENT, "Kr must not alias the other tensors");
+  hk_status s = validate_common(dense(B, Hq, Hkv, N, N), d);  // d in {64, 128} before anything runs
+  if (s != HK_OK) return s;
+  int num_sms = 0;
+  s = check_device(&num_sms);
+  if (s != HK_OK) return s;
+  // K is read by every query tile of its group: rotate it once, into Kr; Q tiles are rotated in
+  // shared memory by the forward kernel itself (read once per CTA)
+  s = rope_launch(K, cos, sin, Kr, B, N, Hkv, d, 1.f, num_sms, stream);
+  if (s != HK_OK) return s;
+  return fwd_impl(Q, Kr, V, O, LSE, dense(B, Hq, Hkv, N, N), d, causal, stream, nullptr, 0, cos, sin);
 }
 
 hk_status hk_attn_merge(float* O_acc, float* LSE_acc, const void* O_part, const float* LSE_part, void* O_out, int B,

@@ -113,17 +113,13 @@ hk_status validate_common(const Shape& sh, int d) {
   return HK_OK;
 }
 
-size_t ws_bytes(int B, int Hq, int Nq) {
-  if (B <= 0 || Hq <= 0 || Nq <= 0) return 0;
-  const size_t Np = ((size_t)Nq + 127) / 128 * 128;  // rows padded to whole 128-row tiles
-  return (size_t)2 * B * Hq * Np * sizeof(float) + 256;  // + the persistent kernels' work counters
-}
+size_t ws_bytes(int B, int Hq, int Nq, int d) { return hk::bwd_ws_bytes(B, Hq, Nq, d); }
 
-template <int D, bool CAUSAL>
+template <int D, bool CAUSAL, bool ROPE = false>
 hk_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const hk::FwdParams& p,
                      int num_sms, cudaStream_t stream) {
   using C = hk::FwdCfg<D>;
-  auto* fn = hk::fwd_kernel<D, CAUSAL>;
+  auto* fn = hk::fwd_kernel<D, CAUSAL, ROPE>;
   hk_status s = ensure_smem(fn, C::SMEM);
   if (s != HK_OK) return s;
   // persistent: one CTA per SM (the SMEM footprint allows one), items in snake order
@@ -136,8 +132,10 @@ hk_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
 
 static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                           const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
-                          const Shape& sh, int d, int causal, cudaStream_t stream) {
+                          const Shape& sh, int d, int causal, cudaStream_t stream,
+                          unsigned flags = 0) {
   g_err[0] = 0;
+  if (flags & ~(unsigned)HK_BWD_DETERMINISTIC) return fail(HK_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
   hk_status s = validate_common(sh, d);
   if (s != HK_OK) return s;
   if (!Q || !K || !V || !O || !LSE || !dO || !dQ || !dK || !dV || !workspace)
@@ -145,7 +143,7 @@ static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V
   const void* ptrs[] = {Q, K, V, O, LSE, dO, dQ, dK, dV, workspace};
   for (const void* ptr : ptrs)
     if (!aligned16(ptr)) return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
-  const size_t need = ws_bytes(sh.B, sh.Hq, sh.Nq);
+  const size_t need = ws_bytes(sh.B, sh.Hq, sh.Nq, d);
   if (workspace_bytes < need)
     return fail(HK_ERR_INVALID_ARGUMENT, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
   const size_t q_bytes = sh.q_rows() * sh.Hq * d * 2, kv_bytes = sh.k_rows() * sh.Hkv * d * 2;
@@ -165,13 +163,15 @@ static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V
   int num_sms = 0;
   s = check_device(&num_sms);
   if (s != HK_OK) return s;
-  const hk::BwdShape bs{sh.cu_q, sh.cu_k, sh.B, sh.Hq, sh.Hkv, sh.Nq, sh.Nk, sh.total_q, sh.total_k};
+  const bool fused = d == 64 && !(flags & HK_BWD_DETERMINISTIC);  // NEXT #1 single pass at d = 64
+  const hk::BwdShape bs{sh.cu_q, sh.cu_k, sh.B, sh.Hq, sh.Hkv, sh.Nq, sh.Nk, sh.total_q, sh.total_k, fused};
   return hk::launch_bwd(Q, K, V, O, LSE, dO, dQ, dK, dV, reinterpret_cast<float*>(workspace), bs, d, causal != 0,
                         stream, g_err, sizeof(g_err), phase, num_sms);
 }
 
 static hk_status fwd_impl(const void* Q, const void* K, const void* V, void* O, float* LSE, const Shape& sh, int d,
-                          int causal, cudaStream_t stream, void* workspace = nullptr, size_t workspace_bytes = 0) {
+                          int causal, cudaStream_t stream, void* workspace = nullptr, size_t workspace_bytes = 0,
+                          const float* rope_cos = nullptr, const float* rope_sin = nullptr) {
   g_err[0] = 0;
   hk_status s = validate_common(sh, d);
   if (s != HK_OK) return s;
@@ -210,8 +210,17 @@ static hk_status fwd_impl(const void* Q, const void* K, const void* V, void* O, 
   p.num_pairs = ((sh.Nq + 127) / 128 + 1) / 2;
   p.num_items = sh.B * sh.Hq * p.num_pairs;
   p.sched = reinterpret_cast<unsigned*>(workspace);  // dynamic scheduling when given a workspace
+  p.rope_cos = rope_cos;
+  p.rope_sin = rope_sin;
   if (workspace && cudaMemsetAsync(workspace, 0, 8, stream) != cudaSuccess)
     return fail(HK_ERR_LAUNCH, "cudaMemsetAsync(workspace counters) failed");
+  if (rope_cos) {
+    if (d == 64)
+      return causal ? launch_fwd<64, true, true>(mq, mk, mv, p, num_sms, stream)
+                    : launch_fwd<64, false, true>(mq, mk, mv, p, num_sms, stream);
+    return causal ? launch_fwd<128, true, true>(mq, mk, mv, p, num_sms, stream)
+                  : launch_fwd<128, false, true>(mq, mk, mv, p, num_sms, stream);
+  }
   if (d == 64)
     return causal ? launch_fwd<64, true>(mq, mk, mv, p, num_sms, stream)
                   : launch_fwd<64, false>(mq, mk, mv, p, num_sms, stream);

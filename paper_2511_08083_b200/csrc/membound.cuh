@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 
+#include "rope.cuh"
+
 namespace hk {
 
 // ---------------------------------------------------------------- dropout hash
@@ -18,23 +20,6 @@ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
   x *= 0x846ca68bu;
   x ^= x >> 16;
   return x;
-}
-
-__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float2 t = __bfloat1622float2(h[k]);
-    f[2 * k] = t.x;
-    f[2 * k + 1] = t.y;
-  }
-}
-__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
-  uint4 v;
-  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(f[2 * k], f[2 * k + 1]);
-  return v;
 }
 
 // ---------------------------------------------------------------- LayerNorm
@@ -143,6 +128,7 @@ struct RopeParams {
   __nv_bfloat16* out;      // [B][N][H][d]
   size_t rows;             // B * N * H
   int N, H, d;
+  float sgn;               // +1: rotate by theta; -1: the inverse rotation (gradients)
 };
 
 // One thread per (row, 8-wide chunk of the first half): it loads the matching
@@ -161,17 +147,9 @@ __global__ void __launch_bounds__(256) rope_kernel(const RopeParams p) {
     float a[8], b[8], c[8], s[8];
     unpack8(__ldcs(reinterpret_cast<const uint4*>(xr) + ch), a);
     unpack8(__ldcs(reinterpret_cast<const uint4*>(xr + half) + ch), b);
-    const float4* cp = reinterpret_cast<const float4*>(p.cos + (size_t)n * half + ch * 8);
-    const float4* sp = reinterpret_cast<const float4*>(p.sin + (size_t)n * half + ch * 8);
-    const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
-    c[0] = c0.x, c[1] = c0.y, c[2] = c0.z, c[3] = c0.w, c[4] = c1.x, c[5] = c1.y, c[6] = c1.z, c[7] = c1.w;
-    s[0] = s0.x, s[1] = s0.y, s[2] = s0.z, s[3] = s0.w, s[4] = s1.x, s[5] = s1.y, s[6] = s1.z, s[7] = s1.w;
+    rope_load_cs(p.cos, p.sin, (size_t)n, half, ch, p.sgn, c, s);
     float lo[8], hi[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      lo[e] = fmaf(a[e], c[e], -b[e] * s[e]);
-      hi[e] = fmaf(b[e], c[e], a[e] * s[e]);
-    }
+    rope_pair8(a, b, c, s, lo, hi);
     __nv_bfloat16* orow = p.out + (size_t)row * p.d;
     __stcs(reinterpret_cast<uint4*>(orow) + ch, pack8(lo));
     __stcs(reinterpret_cast<uint4*>(orow + half) + ch, pack8(hi));
@@ -189,11 +167,8 @@ __global__ void __launch_bounds__(256) rope_hloop_kernel(const RopeParams p) {
     const size_t bn = t / (I)cpr;
     const int ch = (int)(t - (I)bn * (I)cpr);
     const int n = (int)((I)bn % (I)p.N);
-    const float4* cp = reinterpret_cast<const float4*>(p.cos + (size_t)n * half + ch * 8);
-    const float4* sp = reinterpret_cast<const float4*>(p.sin + (size_t)n * half + ch * 8);
-    const float4 c0 = __ldg(cp), c1 = __ldg(cp + 1), s0 = __ldg(sp), s1 = __ldg(sp + 1);
-    const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-    const float s[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    float c[8], s[8];
+    rope_load_cs(p.cos, p.sin, (size_t)n, half, ch, p.sgn, c, s);
     constexpr int HG = 4;  // heads per group: their loads go out together
     for (int h0 = 0; h0 < p.H; h0 += HG) {
       uint4 va[HG], vb[HG];
@@ -211,11 +186,7 @@ __global__ void __launch_bounds__(256) rope_hloop_kernel(const RopeParams p) {
           float a[8], b[8], lo[8], hi[8];
           unpack8(va[u], a);
           unpack8(vb[u], b);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            lo[e] = fmaf(a[e], c[e], -b[e] * s[e]);
-            hi[e] = fmaf(b[e], c[e], a[e] * s[e]);
-          }
+          rope_pair8(a, b, c, s, lo, hi);
           __nv_bfloat16* orow = p.out + (bn * p.H + h0 + u) * p.d;
           __stcs(reinterpret_cast<uint4*>(orow) + ch, pack8(lo));
           __stcs(reinterpret_cast<uint4*>(orow + half) + ch, pack8(hi));

@@ -162,6 +162,16 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// Bulk-async reduce-add of a shared-memory tile into global memory through a 4-D tensor map
+// (fp32 add; the dQ accumulator of the fused backward).
+__device__ __forceinline__ void tma_reduce_add_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                                  int c3) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -184,6 +194,12 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
+}
+
+// 16-byte shared-memory store at a 32-bit shared address (a generic-pointer store through a
+// computed address compiles to ST.E with a 64-bit address per chunk)
+__device__ __forceinline__ void sts_v4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
 // ------------------------------------------------------------------ named barriers
@@ -445,6 +461,15 @@ __device__ __forceinline__ void gemm_tsp_mn(uint32_t d, uint32_t a_tmem, uint64_
   asm volatile(HK_MMA_HEAD HK_TS_FIRST HK_TS_STEP(8, 128) HK_TS_STEP(16, 256) HK_TS_STEP(24, 384)
                    HK_TS_STEP(64, 512) HK_TS_STEP(72, 640) HK_TS_STEP(80, 768) HK_TS_STEP(88, 896) "}" ::"r"(d),
                "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+               : "memory");
+}
+
+// A and B both MN-major SW128 128-row-per-K-step tiles, K = 128 (8 k-steps of 16 rows x 128 B):
+// the fused backward's dQ_partial = dS K_j (dS stored [keys][queries], K_j [keys][d]).
+__device__ __forceinline__ void gemm_ss_mnmn(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(HK_MMA_HEAD HK_SS_FIRST HK_SS_STEP(128, 128) HK_SS_STEP(256, 256) HK_SS_STEP(384, 384)
+                   HK_SS_STEP(512, 512) HK_SS_STEP(640, 640) HK_SS_STEP(768, 768) HK_SS_STEP(896, 896) "}" ::"r"(d),
+               "l"(a), "l"(b), "r"(idesc), "r"(acc)
                : "memory");
 }
 

@@ -48,6 +48,25 @@ inline bool encode_bnhd(CUtensorMap* map, const void* base, int B, int N, int H,
   return r == CUDA_SUCCESS;
 }
 
+// An fp32 BNHD tensor [B][N][H][d] as the 4-D map (d, H, N, B), box (32, 1, 128, 1), 128-byte
+// swizzle (32 fp32 = 128 B per box row): the fused backward's dQ accumulator (bulk reduce-add).
+inline bool encode_bnhd_f32(CUtensorMap* map, const void* base, int B, int N, int H, int d) {
+  auto fn = get_encode_fn();
+  if (!fn) {
+    last_encode_result() = -1;
+    return false;
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)H, (cuuint64_t)N, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)d * 4, (cuuint64_t)H * d * 4, (cuuint64_t)N * H * d * 4};
+  cuuint32_t box[4] = {32, 1, 128, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  last_encode_result() = (int)r;
+  return r == CUDA_SUCCESS;
+}
+
 // A row-major bf16 matrix [rows][cols] viewed as the 2-D map (cols, rows), box
 // (64, box_rows), 128-byte swizzle (K-major operand tiles for tcgen05).
 inline bool encode_rowmajor(CUtensorMap* map, const void* base, int rows, int cols, int box_rows) {

@@ -270,7 +270,8 @@ def ring_attn_bwd(q, k, v, o, lse, do, causal: bool, comm: RingComm, streams: in
                                                          args[0].shape[1], args[0].shape[3]) // 4,
                                  dtype=torch.float32, device=args[0].device)
                 e = fan.run(lambda args=args, g=g, ws=ws, m=mode:
-                            api.attn_bwd(*args, m == "causal", workspace=ws, dq=g[0], dk=g[1], dv=g[2]))
+                            api.attn_bwd(*args, m == "causal", workspace=ws, dq=g[0], dk=g[1], dv=g[2],
+                                         deterministic=True))
                 parts.append((li, i, qh, kh, g, e))
         for li, i, qh, kh, (dq_p, dk_p, dv_p), e in parts:
             t = trav[li]

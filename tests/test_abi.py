@@ -56,13 +56,15 @@ def test_host_only_validation(lib):
     size, and argument validation that fails before any CUDA call."""
     from paper_2511_08083_b200 import _lib
     L = _lib.lib()
-    assert L.hk_attn_abi_version() == 3
+    assert L.hk_attn_abi_version() == 4
     assert L.hk_status_string(2) == b"HK_ERR_UNSUPPORTED"
-    assert L.hk_attn_bwd_workspace_bytes(2, 4, 2, 256, 64) == 2 * 2 * 4 * 256 * 4 + 256
+    assert L.hk_attn_bwd_workspace_bytes(2, 4, 2, 256, 128) == 2 * 2 * 4 * 256 * 4 + 256
+    # d = 64 adds the fused backward's fp32 dQ accumulator, B * Np * Hq * 64 floats
+    assert L.hk_attn_bwd_workspace_bytes(2, 4, 2, 256, 64) == 2 * 2 * 4 * 256 * 4 + 256 + 2 * 256 * 4 * 256
     p = ctypes.c_void_p(16)
     assert L.hk_attn_fwd(p, p, p, p, p, 1, 2, 2, 128, 96, 0, None) == 2   # d = 96
     assert L.hk_attn_fwd(p, p, p, p, p, 1, 2, 2, 0, 64, 0, None) == 1     # N = 0
-    assert L.hk_attn_bwd_workspace_bytes(1, 2, 2, 200, 64) == 2 * 2 * 256 * 4 + 256  # rows padded to 128
+    assert L.hk_attn_bwd_workspace_bytes(1, 2, 2, 200, 128) == 2 * 2 * 256 * 4 + 256  # rows padded to 128
     assert L.hk_attn_fwd(p, p, p, p, p, 1, 3, 2, 128, 64, 0, None) == 1   # Hq % Hkv
     assert b"multiple" in L.hk_attn_last_error()
     assert L.hk_attn_fwd(p, p, p, p, p, 0, 2, 2, 128, 64, 0, None) == 1   # B = 0
@@ -75,6 +77,9 @@ def test_host_only_validation(lib):
     a = [ctypes.c_void_p(16 * (i + 1) << 30) for i in range(10)]
     assert L.hk_attn_bwd(*a, 0, 1, 2, 2, 128, 64, 0, None) == 1
     assert b"workspace" in L.hk_attn_last_error()
+    # bwd_ex: unknown flag bits are rejected before anything else
+    assert L.hk_attn_bwd_ex(*a, 0, 1, 2, 2, 128, 128, 64, 0, 6, None) == 1
+    assert b"flags" in L.hk_attn_last_error()
 
 
 def test_host_only_validation_next4(lib):
@@ -84,7 +89,7 @@ def test_host_only_validation_next4(lib):
     L = _lib.lib()
     p = ctypes.c_void_p(16)
     Z = ctypes.c_size_t
-    assert L.hk_attn_bwd_qk_workspace_bytes(2, 4, 2, 200, 1000, 64) == 2 * 2 * 4 * 256 * 4 + 256
+    assert L.hk_attn_bwd_qk_workspace_bytes(2, 4, 2, 200, 1000, 64) == 2 * 2 * 4 * 256 * 4 + 256 + 2 * 256 * 4 * 256
     assert L.hk_attn_bwd_varlen_workspace_bytes(3, 4, 2, 129, 7, 128) == 2 * 3 * 4 * 256 * 4 + 256
     assert L.hk_attn_fwd_qk(p, p, p, p, p, 1, 2, 2, 128, 0, 64, 0, None) == 1     # Nk = 0
     assert L.hk_attn_fwd_qk(p, p, p, p, p, 1, 2, 2, 128, 256, 80, 0, None) == 2   # d = 80

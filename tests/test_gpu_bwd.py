@@ -29,8 +29,9 @@ def run(B, N, Hq, Hkv, d, causal, seed, std_qk=None):
     from paper_2511_08083_b200 import attn_bwd, attn_fwd
     x = gen(B, N, Hq, Hkv, d, seed=seed, std_qk=std_qk)
     o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
+    from paper_2511_08083_b200 import bwd_workspace_bytes
     Np = (N + 127) // 128 * 128
-    ws = torch.empty(2 * B * Hq * Np + 64, dtype=torch.float32, device="cuda")  # + scheduler counters
+    ws = torch.empty(bwd_workspace_bytes(B, Hq, Hkv, N, d) // 4, dtype=torch.float32, device="cuda")
     dq, dk, dv = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, workspace=ws)
     torch.cuda.synchronize()
     ref = oracle.attn_fwd_bwd(np64(x["Q"]), np64(x["K"]), np64(x["V"]), np64(x["dO"]), causal)
@@ -66,15 +67,40 @@ def test_bwd_stress_std4(causal):
 
 @pytest.mark.parametrize("d", [64, 128])
 def test_bwd_deterministic(d):
-    """Bitwise run-to-run reproducibility (no atomics, fixed reduction order).
-    Also the race canary: a pipeline hazard shows up as a run that differs."""
+    """Bitwise run-to-run reproducibility of the deterministic backward (no atomics, fixed
+    reduction order). Also the race canary: a pipeline hazard shows up as a run that differs."""
     from paper_2511_08083_b200 import attn_bwd, attn_fwd
     x = gen(2, 640, 8, 2, d, seed=11)
     outs = []
     for _ in range(4):
         o, lse = attn_fwd(x["Q"], x["K"], x["V"], True)
-        outs.append((o, lse) + attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], True))
+        outs.append((o, lse) + attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], True, deterministic=True))
     torch.cuda.synchronize()
     for run in outs[1:]:
         for a, b in zip(outs[0], run):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("B,N,Hq,Hkv", [(2, 640, 8, 2), (1, 1024, 4, 4), (2, 333, 6, 3), (1, 128, 2, 1)])
+def test_bwd_fused_d64(B, N, Hq, Hkv, causal):
+    """The d = 64 default backward is the fused single pass (NEXT #1, hk_attn.h): dK, dV bitwise equal
+    to the deterministic two-pass backward (same kernel arithmetic for them) and bitwise run to run;
+    dQ — fp32 partials added in L2 in arrival order — within the BASELINE tolerance of the oracle,
+    of itself across runs up to the bf16 rounding flips fp32 reordering causes (a flip moves an
+    element by one bf16 ulp, 2^-8 relative; rel-L2 <= 2^-8 sqrt(1%) = 4e-4), and within bf16 rounding of the
+    two-pass dQ (which rounds its own dS = P (dP - D), from S = Q K^T instead of S^T = K Q^T, to
+    bf16: rel-L2 <= 4e-3 = one bf16 ulp 2^-8)."""
+    from paper_2511_08083_b200 import attn_bwd, attn_fwd
+    d = 64
+    x = gen(B, N, Hq, Hkv, d, seed=N + Hq)
+    o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
+    det = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, deterministic=True)
+    runs = [attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal) for _ in range(3)]
+    torch.cuda.synchronize()
+    ref = oracle.attn_fwd_bwd(np64(x["Q"]), np64(x["K"]), np64(x["V"]), np64(x["dO"]), causal)
+    for dq, dk, dv in runs:
+        assert torch.equal(dk, det[1]) and torch.equal(dv, det[2])
+        assert rel_l2(np64(dq), np64(det[0])) <= 4e-3
+        assert rel_l2(np64(dq), np64(runs[0][0])) <= 4e-4
+        assert rel_l2(np64(dq), ref["dQ"]) <= TOL_RELL2

@@ -196,10 +196,12 @@ def test_fullsize(name):
     x = gen(B, N, Hq, Hkv, d, seed=SEED)
     o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
     dq, dk, dv = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal)
-    # bitwise run-to-run determinism of the backward (fixed reduction order, no atomics)
+    # run-to-run determinism: bitwise for dK, dV (fixed reduction order, no atomics) and, at d = 128,
+    # dQ; the d = 64 fused backward adds fp32 dQ partials in L2 arrival order (hk_attn.h)
     dq2, dk2, dv2 = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal)
     torch.cuda.synchronize()
-    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
+    assert torch.equal(dk, dk2) and torch.equal(dv, dv2)
+    assert torch.equal(dq, dq2) if d == 128 else rel_l2(np64(dq2), np64(dq)) <= 4e-4  # bf16 flips (test_gpu_bwd)
     del dq2, dk2, dv2
     outs = (o, lse, dq, dk, dv)
     check_invariants(x, outs, B, Hq, Hkv, G)

@@ -114,12 +114,12 @@ def test_varlen_uniform_equals_dense_bitwise(N, d, causal):
     B, Hq, Hkv = 3, 4, 2
     x = make_inputs(B, N, Hq, Hkv, d, seed=9, device="cuda")
     o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
-    dq, dk, dv = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal)
+    dq, dk, dv = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, deterministic=True)
     cu = torch.arange(0, (B + 1) * N, N, dtype=torch.int32, device="cuda")
     flat = lambda t: t.reshape(B * N, t.shape[2], d)
     ov, lv = attn_fwd_varlen(flat(x["Q"]), flat(x["K"]), flat(x["V"]), cu, cu, N, N, causal)
     dqv, dkv, dvv = attn_bwd_varlen(flat(x["Q"]), flat(x["K"]), flat(x["V"]), ov, lv, flat(x["dO"]), cu, cu, N, N,
-                                    causal)
+                                    causal, deterministic=True)
     torch.cuda.synchronize()
     assert torch.equal(ov, flat(o))
     assert torch.equal(lv, lse.permute(1, 0, 2).reshape(Hq, B * N))

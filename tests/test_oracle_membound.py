@@ -88,3 +88,26 @@ def test_rope_equals_complex_rotation_and_inverts():
     np.testing.assert_allclose(y[..., :8], z.real, rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(y[..., 8:], z.imag, rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(rope(y, c, -s), x, rtol=1e-12, atol=1e-12)
+
+
+def test_rope_attention_gradient_chain_rule_finite_differences():
+    """Reading #21 + NEXT #3 (attention on rotated Q, K): the gradient w.r.t. the unrotated Q, K is
+    the inverse rotation of the oracle's gradient w.r.t. the rotated ones, R^T g = rope(g, c, -s)
+    (what attn_bwd_rope computes). Pinned by central finite differences of L = sum(O * dO)."""
+    from oracle import attn_fwd, attn_fwd_bwd
+    rng = np.random.default_rng(11)
+    B, N, Hq, Hkv, d = 1, 5, 2, 1, 8
+    Q, K, V, dO = (rng.standard_normal(s) for s in ((B, N, Hq, d), (B, N, Hkv, d), (B, N, Hkv, d), (B, N, Hq, d)))
+    c, s = rope_tables(N, d)
+    for causal in (False, True):
+        ref = attn_fwd_bwd(rope(Q, c, s), rope(K, c, s), V, dO, causal)
+        gq, gk = rope(ref["dQ"], c, -s), rope(ref["dK"], c, -s)
+        loss = lambda q, k: float((attn_fwd(rope(q, c, s), rope(k, c, s), V, causal)[0] * dO).sum())
+        h = 1e-6
+        for (t, g) in ((Q, gq), (K, gk)):
+            for idx in [(0, 0, 0, 0), (0, 3, 0, 5), (0, 4, t.shape[2] - 1, 7), (0, 2, 0, 2)]:
+                tp, tm = t.copy(), t.copy()
+                tp[idx] += h
+                tm[idx] -= h
+                fd = (loss(tp, K) - loss(tm, K)) / (2 * h) if t is Q else (loss(Q, tp) - loss(Q, tm)) / (2 * h)
+                assert abs(fd - g[idx]) <= 1e-6 * max(1.0, abs(fd)), (causal, idx, fd, g[idx])
