@@ -137,6 +137,13 @@ hk_status hk_attn_bwd_varlen(const void* Q, const void* K, const void* V, const 
  * backward (bitwise reproducible dQ, the d = 128 path) at d = 64; at d = 128 flags change nothing.
  * hk_attn_bwd* without _ex use flags = 0. Unknown flag bits: HK_ERR_INVALID_ARGUMENT. */
 #define HK_BWD_DETERMINISTIC 1u
+/* HK_BWD_ACCUMULATE_F32: dQ, dK, dV point to fp32 tensors of the same shapes, and the call ADDS
+ * its (scaled, unrounded) results into them instead of writing bf16 — for callers that sum the
+ * gradients of several calls (context-parallel ring attention: one call per visible chunk pair)
+ * without rounding each part to bf16. Rows no query / key sees add nothing. Each output row is
+ * owned by one CTA (no atomics); concurrent calls adding into the same accumulator must be
+ * stream-ordered. */
+#define HK_BWD_ACCUMULATE_F32 2u
 hk_status hk_attn_bwd_ex(const void* Q, const void* K, const void* V, const void* O, const float* LSE,
                          const void* dO, void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes,
                          int B, int Hq, int Hkv, int Nq, int Nk, int d, int causal, unsigned flags,

@@ -82,14 +82,16 @@ def bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk=None) -> int:
 
 
 HK_BWD_DETERMINISTIC = 1  # include/hk_attn.h
+HK_BWD_ACCUMULATE_F32 = 2
 
 
 def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None, dk=None, dv=None,
-             deterministic: bool = False):
+             deterministic: bool = False, accumulate: bool = False):
     """dQ, dK, dV of L = sum(O * dO) for O = attention(q, k, v).
     Returns (dq, dk, dv) bf16, plus the workspace holds D = rowsum(dO*O) then LSE*log2e.
     d = 64 runs the fused single-pass backward unless `deterministic` (hk_attn.h: dQ is then
-    reproducible only up to fp32 reordering; dK, dV stay bitwise)."""
+    reproducible only up to fp32 reordering; dK, dV stay bitwise). accumulate: dq, dk, dv are
+    caller-supplied fp32 tensors the results are ADDED into (HK_BWD_ACCUMULATE_F32)."""
     for n, t in (("q", q), ("k", k), ("v", v), ("o", o), ("do", do)):
         _check_tensor(n, t)
     _check_tensor("lse", lse, torch.float32)
@@ -97,18 +99,21 @@ def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None,
     _expect_shape("o", o, q.shape)
     _expect_shape("do", do, q.shape)
     _expect_shape("lse", lse, (B, Hq, N))
+    if accumulate and (dq is None or dk is None or dv is None):
+        raise ValueError("accumulate=True needs the fp32 dq, dk, dv accumulators")
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
     for n, t, ref in (("dq", dq, q), ("dk", dk, k), ("dv", dv, v)):
-        _check_tensor(n, t)
+        _check_tensor(n, t, torch.float32 if accumulate else torch.bfloat16)
         _expect_shape(n, t, ref.shape)
     nbytes = bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk)
     ws = torch.empty(nbytes // 4, dtype=torch.float32, device=q.device) if workspace is None else workspace
     _check_workspace(ws, nbytes)
     check(lib().hk_attn_bwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
                                _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), B, Hq, Hkv, N, Nk, d,
-                               int(bool(causal)), HK_BWD_DETERMINISTIC if deterministic else 0, _stream()))
+                               int(bool(causal)), (HK_BWD_DETERMINISTIC if deterministic else 0) |
+                               (HK_BWD_ACCUMULATE_F32 if accumulate else 0), _stream()))
     return dq, dk, dv
 
 

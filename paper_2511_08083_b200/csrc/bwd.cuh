@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
   };
   const size_t stride = nwarps * RPW * U;
 #ifndef HK_PRE_PIPE
-#define HK_PRE_PIPE 1
+#define HK_PRE_PIPE 0  // measured 0.92-1.00x (profiles/ab_pre_pipe_r2j.jsonl): off
 #endif
   if (HK_PRE_PIPE) {  // software pipeline: the next iteration's loads are in flight while this one reduces
     size_t base = gwarp * RPW * U;
@@ -150,17 +150,35 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
   }
 }
 
+// fp32 accumulate mode: dst[0..8) += scale * o[0..8) (one CTA owns each output row: no atomics)
+__device__ __forceinline__ void add8_f32(float* dst, const uint32_t* o, float scale) {
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  float4 a = d4[0], b = d4[1];
+  a.x += __uint_as_float(o[0]) * scale, a.y += __uint_as_float(o[1]) * scale;
+  a.z += __uint_as_float(o[2]) * scale, a.w += __uint_as_float(o[3]) * scale;
+  b.x += __uint_as_float(o[4]) * scale, b.y += __uint_as_float(o[5]) * scale;
+  b.z += __uint_as_float(o[6]) * scale, b.w += __uint_as_float(o[7]) * scale;
+  d4[0] = a;
+  d4[1] = b;
+}
+
 // Fused backward epilogue: dQ = bf16(dQ_acc / sqrt(d)) over the query rows of sequence b =
 // blockIdx.y (its rows beyond max_seqlen are left untouched, hk_attn.h), 8 elements per thread-step.
 template <int D>
 __global__ void __launch_bounds__(256) dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
-                                                         SeqGeom g, int H, float scale) {
+                                                         SeqGeom g, int H, float scale, bool acc32) {
   const Seq sq = seq_of(g, blockIdx.y);
   const size_t base = (size_t)sq.gq0 * H * (D / 8), n8 = (size_t)sq.lq * H * (D / 8);
   for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < n8; j += (size_t)gridDim.x * blockDim.x) {
     const size_t i = base + j;
     const float4 a = __ldcs(reinterpret_cast<const float4*>(acc) + 2 * i);
     const float4 b = __ldcs(reinterpret_cast<const float4*>(acc) + 2 * i + 1);
+    if (acc32) {  // fp32 accumulate mode: dq is the caller's fp32 accumulator
+      const uint32_t o[8] = {__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(a.z), __float_as_uint(a.w),
+                             __float_as_uint(b.x), __float_as_uint(b.y), __float_as_uint(b.z), __float_as_uint(b.w)};
+      add8_f32(reinterpret_cast<float*>(dq) + 8 * i, o, scale);
+      continue;
+    }
     uint4 o;
     o.x = pack_bf16(a.x * scale, a.y * scale);
     o.y = pack_bf16(a.z * scale, a.w * scale);
@@ -179,7 +197,9 @@ struct BwdParams {
   unsigned* sched;    // [4] work counters in the workspace: dK/dV draw, done; dQ draw, done
   SeqGeom g;          // dense / varlen geometry (seq.cuh)
   int B, Hq, Hkv, Np, Npk;  // Npk = Nk (varlen: max_seqlen_k) rounded up to 128
+  bool acc32;         // HK_BWD_ACCUMULATE_F32: dq / dk / dv are fp32 accumulators the results add into
 };
+
 
 // 128 x 128 tiles throughout: tcgen05.mma with N=64 paces at 48 cycles per
 // K=16 step instead of 32 (measured, scripts/rates.py), N=128 at full rate.
@@ -643,8 +663,8 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
       const bool key_ok = key < w.sq.lk;  // key rows of a ragged last tile beyond the sequence are not stored
       __nv_bfloat16* out =
           (is_dk ? p.dk : p.dv) + ((size_t)(w.sq.gk0 + (key_ok ? key : 0)) * p.Hkv + w.kvh) * D + ecol0;
-      if (w.n_it == 0) {  // no query sees these keys: dK = dV = 0
-        if (key_ok) {
+      if (w.n_it == 0) {  // no query sees these keys: dK = dV = 0 (accumulate mode: nothing to add)
+        if (key_ok && !p.acc32) {
 #pragma unroll
           for (int k = 0; k < ECOLS / 8; ++k) reinterpret_cast<uint4*>(out)[k] = make_uint4(0u, 0u, 0u, 0u);
         }
@@ -754,6 +774,15 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
         uint32_t o[32];
         tmem_ld32(tmem_addr(tacc, lb, c0), o);
         tmem_wait_ld();
+        if (p.acc32) {  // fp32 accumulate mode: add into the caller's fp32 dK / dV
+          float* outf = reinterpret_cast<float*>(is_dk ? p.dk : p.dv) +
+                        ((size_t)(w.sq.gk0 + (key_ok ? key : 0)) * p.Hkv + w.kvh) * D + ecol0 + c0;
+          if (key_ok) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) add8_f32(outf + 8 * k, o + 8 * k, scale);
+          }
+          continue;
+        }
         uint4 o4[4];
         uint32_t* op = reinterpret_cast<uint32_t*>(o4);
 #pragma unroll
@@ -1025,8 +1054,8 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS2, 1)
       const int q = w.iq * 128 + r;
       const bool q_ok = q < w.sq.lq;  // query rows of a ragged last tile beyond the sequence are not stored
       __nv_bfloat16* out = p.dq + ((size_t)(w.sq.gq0 + (q_ok ? q : 0)) * p.Hq + w.h) * D + wg * QC;
-      if (w.n_it == 0) {  // no key visible to these rows: dQ = 0
-        if (q_ok) {
+      if (w.n_it == 0) {  // no key visible to these rows: dQ = 0 (accumulate mode: nothing to add)
+        if (q_ok && !p.acc32) {
 #pragma unroll
           for (int k = 0; k < QC / 8; ++k) reinterpret_cast<uint4*>(out)[k] = make_uint4(0u, 0u, 0u, 0u);
         }
@@ -1104,6 +1133,14 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS2, 1)
       item = sched_take(sched, rr);  // look ahead: is there a next item?
       if (busy(item)) copy_in();
       const float scale = rsqrtf((float)D);
+      if (p.acc32) {  // fp32 accumulate mode: add into the caller's fp32 dQ
+        float* outf = reinterpret_cast<float*>(p.dq) + ((size_t)(w.sq.gq0 + (q_ok ? q : 0)) * p.Hq + w.h) * D + wg * QC;
+        if (q_ok) {
+#pragma unroll
+          for (int c0 = 0; c0 < QC; c0 += 8) add8_f32(outf + c0, o + c0, scale);
+        }
+        continue;
+      }
 #pragma unroll
       for (int c0 = 0; c0 < QC; c0 += 8) {
         uint4 o4;
@@ -1165,6 +1202,7 @@ struct BwdShape {
   int B, Hq, Hkv, Nq, Nk;  // varlen: Nq, Nk = max_seqlen_q, max_seqlen_k
   int total_q, total_k;    // varlen only
   bool fused;              // d = 64: single-pass dQ (bulk reduce-add into the fp32 accumulator) — not bitwise
+  bool acc32;              // HK_BWD_ACCUMULATE_F32: dQ, dK, dV are fp32 accumulators
 };
 
 // Workspace layout of one backward call (hk_attn.h): D and LSE2 [B][Hq][Np] fp32, 256 bytes of work
@@ -1232,7 +1270,8 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
               Hq,
               Hkv,
               Np,
-              Npk};
+              Npk,
+              sh.acc32};
   // B0: grid (x, b), x sized for the longest sequence and capped at ~16 blocks per SM overall
   const size_t rows = (size_t)sh.Nq * Hq;
   const size_t warps_needed = (rows + (32 / (D / 8)) - 1) / (32 / (D / 8));
@@ -1274,7 +1313,7 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   }
   if (fq && (phase < 0 || phase == 2)) {  // dQ = bf16(dQ_acc / sqrt(d)), grid (x, sequence) like B0
     dq_convert_kernel<D><<<dim3((unsigned)bx, (unsigned)B), 256, 0, stream>>>(
-        dq_acc, reinterpret_cast<__nv_bfloat16*>(dQ), g, Hq, rsqrtf((float)D));
+        dq_acc, reinterpret_cast<__nv_bfloat16*>(dQ), g, Hq, rsqrtf((float)D), sh.acc32);
   }
   if (!fq && (phase < 0 || phase == 2)) {
     const int items = B * Hq * (Np / 128);  // persistent: one CTA per SM

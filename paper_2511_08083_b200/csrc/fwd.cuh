@@ -127,9 +127,10 @@ __device__ __forceinline__ int fwd_next_busy(const FwdParams& p, int r, int cta,
   }
 }
 
-// ROPE (NEXT #3, hk_attn_fwd_rope): warps 10-11 (otherwise idle) rotate each item's Q tiles in
-// shared memory right after they land (rotate-half, rope.cuh: the same arithmetic as hk_rope) and
-// publish them on bar_qr, which the MMA warp waits on instead of bar_q; K arrives pre-rotated.
+// ROPE (NEXT #3, hk_attn_fwd_rope): each softmax warpgroup rotates its own Q tile in shared
+// memory at the start of an item, one row per thread (rotate-half, rope.cuh: the same arithmetic
+// as hk_rope), and publishes it on bar_qr[t], which the MMA warp waits on before S_t = Q_t K^T;
+// K arrives pre-rotated (hk_rope into Kr).
 template <int D, bool CAUSAL, bool ROPE>
 __global__ void __launch_bounds__(384, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sV = sK + NS * TB;   // NS tiles
 
   __shared__ uint64_t bar_q, bar_qfree, bar_kfull[NS], bar_kempty[NS], bar_vfull[NS], bar_vempty[NS];
-  __shared__ uint64_t bar_s[2], bar_p[2], bar_pl[2], bar_o[2], bar_oempty[2], bar_sfree[2], bar_pv[2], bar_qr;
+  __shared__ uint64_t bar_s[2], bar_p[2], bar_pl[2], bar_o[2], bar_oempty[2], bar_sfree[2], bar_pv[2], bar_qr[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ Sched sched;
 
@@ -156,9 +157,10 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) hk_trace(30, 0, 0);  // CTA start
 
   if (threadIdx.x == 0) {
-    sched_init(sched, ROPE ? 11 : 9);
+    sched_init(sched);
     mbar_init(&bar_q, 1);
-    mbar_init(&bar_qr, 2);  // ROPE: both rotary warps
+    mbar_init(&bar_qr[0], 4);  // ROPE: the tile's warpgroup rotated it
+    mbar_init(&bar_qr[1], 4);
     mbar_init(&bar_qfree, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bar_kfull[s], 1);
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(384, 1)
       };
 
       int s = 0;
-      uint32_t ph = 0, q_ph = 0;
+      uint32_t ph = 0, q_ph = 0, qr_ph[2] = {0, 0};
       uint32_t p_ph[2] = {0, 0}, oe_ph[2] = {0, 0};  // bar_pl and bar_p complete in lockstep
       bool o_used[2] = {false, false};  // O_t holds an earlier item's accumulator (wait for its epilogue)
       uint32_t sf_ph[2] = {0, 0};        // split P: bar_sfree phases
@@ -289,12 +291,20 @@ __global__ void __launch_bounds__(384, 1)
         const bool last_item = !dyn && rn < 0;
         uses += it.nkv;
         ++busy;
-        mbar_wait(ROPE ? &bar_qr : &bar_q, q_ph);  // ROPE: Q landed and rotated
+        if (!ROPE) mbar_wait(&bar_q, q_ph);
         q_ph ^= 1;
         mbar_wait(&bar_kfull[s], ph);
         tc_fence_after();
-        if (it.nkv0 > 0) issue_s(0, s);
-        if (it.nkv1 > 0) issue_s(1, s);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if ((t == 0 ? it.nkv0 : it.nkv1) == 0) continue;
+          if (ROPE) {  // Q tile t landed and rotated by its warpgroup
+            mbar_wait(&bar_qr[t], qr_ph[t]);
+            qr_ph[t] ^= 1;
+            tc_fence_after();
+          }
+          issue_s(t, s);
+        }
         tc_commit_w(&bar_kempty[s]);
         if (it.nkv == 1 && !last_item) tc_commit_w(&bar_qfree);
         for (int j = 0; j < it.nkv; ++j) {
@@ -375,62 +385,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         if (busy > 0) mbar_wait(&bar_qfree, (busy - 1) & 1);
       }
-    } else if (ROPE && warp >= 10) {
-      // ================= fused rotary of Q (warps 10-11) =================
-      // A row's elements i and i + D/2 sit in the same 16-B chunk slot of the two 64-column
-      // panels (D = 128) or in chunks c and c + 4 of its one 128-B row (D = 64), both at the
-      // 128B-swizzled position (chunk ^ (row % 8)).
-      constexpr int CPR = D / 16;  // chunk pairs per row
-      const int tid = (warp - 10) * 32 + lane;
-      const uint32_t q_base = smem_u32(sQ);
-      uint32_t q_ph = 0;
-      int rn = dyn ? 0 : fwd_next_busy<CAUSAL>(p, 0, cta, ctas);
-      for (;;) {
-        int item;
-        if (dyn) {
-          item = sched_take(sched, rn++);
-          if (item >= p.num_items) break;
-        } else {
-          if (rn < 0) break;
-          item = fwd_item_index<CAUSAL>(rn, cta, ctas);
-          rn = fwd_next_busy<CAUSAL>(p, rn + 1, cta, ctas);
-        }
-        const FwdItem it = fwd_decode<CAUSAL>(p, item);
-        if (it.nkv == 0) continue;
-        mbar_wait(&bar_q, q_ph);
-        q_ph ^= 1;
-#pragma unroll 1
-        for (int t = 0; t < 2; ++t) {
-          if ((t == 0 ? it.nkv0 : it.nkv1) == 0) continue;  // tile not loaded
-          const int qt = t == 0 ? it.qt0 : it.qt1;
-          const uint32_t tile = q_base + t * TB;
-#pragma unroll 2
-          for (int u = tid; u < 128 * CPR; u += 64) {
-            const int r = u / CPR, c = u % CPR;
-            const int n = qt * 128 + r;  // position of the query row
-            if (n >= it.sq.lq) continue;
-            const uint32_t alo = tile + r * 128 + ((c ^ (r & 7)) << 4);
-            const uint32_t ahi = D == 128 ? tile + 128 * 128 + r * 128 + ((c ^ (r & 7)) << 4)
-                                          : tile + r * 128 + (((c + 4) ^ (r & 7)) << 4);
-            uint4 va, vb;
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(va.x), "=r"(va.y), "=r"(va.z), "=r"(va.w)
-                         : "r"(alo));
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(vb.x), "=r"(vb.y), "=r"(vb.z), "=r"(vb.w)
-                         : "r"(ahi));
-            float a[8], b[8], cs[8], sn[8], lo[8], hi[8];
-            unpack8(va, a);
-            unpack8(vb, b);
-            rope_load_cs(p.rope_cos, p.rope_sin, (size_t)n, D / 2, c, 1.f, cs, sn);
-            rope_pair8(a, b, cs, sn, lo, hi);
-            const uint4 wa = pack8(lo), wb = pack8(hi);
-            sts_v4(alo, wa.x, wa.y, wa.z, wa.w);
-            sts_v4(ahi, wb.x, wb.y, wb.z, wb.w);
-          }
-        }
-        fence_proxy_async_smem();  // generic-proxy stores visible to the tensor core
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_qr);
-      }
+
     }
   } else {
     // ================= softmax warpgroups =================
@@ -443,11 +398,50 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_base = (warp & 3) * 32;
     const int r = (warp & 3) * 32 + lane;  // row within the Q tile == TMEM lane
     const float c = 1.4426950408889634f / sqrtf((float)D);  // (1/sqrt d) log2 e
-    uint32_t s_ph = 0, o_ph = 0;
+    uint32_t s_ph = 0, o_ph = 0, q_ph = 0;
     int step = 0;  // running KV-step count (trace index only)
     // turn-taking (C::ALT): tile 0 waits on barrier 1 and releases barrier 2, tile 1 the reverse;
     // tile 1 opens the first turn. Only steps both tiles have take turns (the counts agree).
     if (C::ALT && t == 1) named_bar_arrive(1, 256);
+    // ROPE: wait for an item's Q tiles and rotate this warpgroup's tile, one row per thread
+    auto wait_rotate = [&](const FwdItem& x) {
+      mbar_wait(&bar_q, q_ph);  // every busy item loads Q once: keep this warpgroup's phase in step
+      q_ph ^= 1;
+      if ((t == 0 ? x.nkv0 : x.nkv1) == 0) return;  // tile not loaded: the MMA warp does not wait for it
+      const int rowx = (t == 0 ? x.qt0 : x.qt1) * 128 + r;  // position of the query row
+      if (rowx < x.sq.lq) {
+        constexpr int CP = D / 16;  // chunk pairs per row
+        float cs[CP][8], sn[CP][8];  // every cos / sin load of the row in flight at once
+#pragma unroll
+        for (int c = 0; c < CP; ++c) rope_load_cs(p.rope_cos, p.rope_sin, (size_t)rowx, D / 2, c, 1.f, cs[c], sn[c]);
+        const uint32_t tile = smem_u32(sQ) + t * TB + r * 128;
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+          // a row's elements i and i + D/2: the same chunk slot of the two panels (D = 128) or
+          // chunks c and c + 4 of its 128-B row (D = 64), both at the 128B-swizzled position
+          const uint32_t alo = tile + ((c ^ (r & 7)) << 4);
+          const uint32_t ahi = D == 128 ? alo + 128 * 128 : tile + (((c + 4) ^ (r & 7)) << 4);
+          uint4 va, vb;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(va.x), "=r"(va.y), "=r"(va.z), "=r"(va.w)
+                       : "r"(alo));
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(vb.x), "=r"(vb.y), "=r"(vb.z), "=r"(vb.w)
+                       : "r"(ahi));
+          float a[8], b[8], lo[8], hi[8];
+          unpack8(va, a);
+          unpack8(vb, b);
+          rope_pair8(a, b, cs[c], sn[c], lo, hi);
+          const uint4 wa = pack8(lo), wb = pack8(hi);
+          sts_v4(alo, wa.x, wa.y, wa.z, wa.w);
+          sts_v4(ahi, wb.x, wb.y, wb.z, wb.w);
+        }
+      }
+      fence_proxy_async_smem();  // generic-proxy stores visible to the tensor core
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_qr[t]);
+    };
+    // (Rotating the next item's Q before this item's epilogue, while the last P V runs, measured
+    // 0.83x of the plain forward at C3 against 0.91x for rotating at the item start: the wait for
+    // the next Q tile then delays the epilogue and the O release the next P V needs.)
     for (int rr = 0;; ++rr) {
       const int item = dyn ? sched_take(sched, rr) : fwd_item_index<CAUSAL>(rr, cta, ctas);
       if (item >= p.num_items) break;
@@ -456,6 +450,7 @@ __global__ void __launch_bounds__(384, 1)
       const int qt = t == 0 ? it.qt0 : it.qt1;
       const int row = qt * 128 + r;
       const bool row_ok = row < it.sq.lq;  // rows of a ragged last tile beyond the sequence are not stored
+      if (ROPE && it.nkv > 0) wait_rotate(it);
       if (nk == 0) {  // no row of this tile sees a key: O = 0, LSE = -inf (reading #22)
         if (row_ok) {
           uint4* dst = reinterpret_cast<uint4*>(p.o + ((size_t)(it.sq.gq0 + row) * p.Hq + it.h) * D);

@@ -135,7 +135,9 @@ static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V
                           const Shape& sh, int d, int causal, cudaStream_t stream,
                           unsigned flags = 0) {
   g_err[0] = 0;
-  if (flags & ~(unsigned)HK_BWD_DETERMINISTIC) return fail(HK_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  if (flags & ~(unsigned)(HK_BWD_DETERMINISTIC | HK_BWD_ACCUMULATE_F32))
+    return fail(HK_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  const bool acc32 = (flags & HK_BWD_ACCUMULATE_F32) != 0;
   hk_status s = validate_common(sh, d);
   if (s != HK_OK) return s;
   if (!Q || !K || !V || !O || !LSE || !dO || !dQ || !dK || !dV || !workspace)
@@ -151,7 +153,8 @@ static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V
   const void* ins[] = {Q, K, V, O, LSE, dO};
   const size_t in_sz[] = {q_bytes, kv_bytes, kv_bytes, q_bytes, lse_bytes, q_bytes};
   void* outs[] = {dQ, dK, dV, workspace};
-  const size_t out_sz[] = {q_bytes, kv_bytes, kv_bytes, workspace_bytes};
+  const size_t osc = acc32 ? 2 : 1;  // fp32 accumulators are twice the bf16 outputs
+  const size_t out_sz[] = {q_bytes * osc, kv_bytes * osc, kv_bytes * osc, workspace_bytes};
   for (int i = 0; i < 4; ++i) {
     for (int k = 0; k < 6; ++k)
       if (overlaps(outs[i], out_sz[i], ins[k], in_sz[k]))
@@ -164,7 +167,7 @@ static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V
   s = check_device(&num_sms);
   if (s != HK_OK) return s;
   const bool fused = d == 64 && !(flags & HK_BWD_DETERMINISTIC);  // NEXT #1 single pass at d = 64
-  const hk::BwdShape bs{sh.cu_q, sh.cu_k, sh.B, sh.Hq, sh.Hkv, sh.Nq, sh.Nk, sh.total_q, sh.total_k, fused};
+  const hk::BwdShape bs{sh.cu_q, sh.cu_k, sh.B, sh.Hq, sh.Hkv, sh.Nq, sh.Nk, sh.total_q, sh.total_k, fused, acc32};
   return hk::launch_bwd(Q, K, V, O, LSE, dO, dQ, dK, dV, reinterpret_cast<float*>(workspace), bs, d, causal != 0,
                         stream, g_err, sizeof(g_err), phase, num_sms);
 }

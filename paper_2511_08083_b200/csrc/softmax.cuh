@@ -30,9 +30,18 @@ __device__ __forceinline__ void softmax_chunk32(const float* s, float c, float m
       const float2 sc = make_float2(fmaxf(s[2 * k], smin), fmaxf(s[2 * k + 1], smin));
       const float2 j = fma2(sc, c2, bias2);
       const float2 f = fma2(sc, c2, sub2(bias2, j));
-      float2 q = fma2(make_float2(0.05508885905f, 0.05508885905f), f, make_float2(0.242604658f, 0.242604658f));
-      q = fma2(q, f, make_float2(0.6932762861f, 0.6932762861f));
-      q = fma2(q, f, make_float2(0.999928891658f, 0.999928891658f));
+#ifndef HK_FWD_POLY2
+#define HK_FWD_POLY2 1  // 1.01-1.03x (profiles/ab_fwd_poly2_r2l.jsonl); reading #27
+#endif
+      float2 q;
+      if (HK_FWD_POLY2) {  // degree 2 (max relative error 1.7e-3, below bf16's half ulp 2^-9)
+        q = fma2(make_float2(0.23842824f, 0.23842824f), f, make_float2(0.70344784f, 0.70344784f));
+        q = fma2(q, f, make_float2(1.00044318f, 1.00044318f));
+      } else {
+        q = fma2(make_float2(0.05508885905f, 0.05508885905f), f, make_float2(0.242604658f, 0.242604658f));
+        q = fma2(q, f, make_float2(0.6932762861f, 0.6932762861f));
+        q = fma2(q, f, make_float2(0.999928891658f, 0.999928891658f));
+      }
       e = make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(j.x) << 23)),
                       __int_as_float(__float_as_int(q.y) + (__float_as_int(j.y) << 23)));
     } else {
@@ -139,6 +148,9 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
   // alt_arrive, 256 threads = both warpgroups): each runs with the SM's MUFU and FMA pipes to
   // itself, in the order the MMA warp consumes P (tile 0, then tile 1).
   if (alt_wait >= 0) named_bar_sync(alt_wait, 256);
+#ifndef HK_FWD_STLATE
+#define HK_FWD_STLATE 1  // 1.003-1.027x (profiles/ab_fwd_stlate_r2l.jsonl)
+#endif
 #pragma unroll
   for (int c0 = 0; c0 < 128; c0 += 32) {
     uint32_t pk[16];
@@ -146,9 +158,18 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
       softmax_chunk32<false, EMU_OF_8>(s + c0, c, m_use == -INFINITY ? 0.f : m_use, smin, pk, acc);
     else
       softmax_chunk32<true, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);
+    // HK_FWD_STLATE: publish the first half of P after the third chunk's exponentials, so the
+    // wait for the first two chunks' TMEM stores hides behind that work
+    const int pub = HK_FWD_STLATE ? 64 : 32;
+    if (HK_FWD_STLATE && bar_lo != nullptr && c0 == pub) {
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(bar_lo);
+    }
     tmem_st16(tmem_addr(tP, lane_base, c0 / 2), pk);
-    if (bar_lo != nullptr && c0 == 32) {  // P of keys [0, 64) (and the O rescale) in TMEM:
-      tmem_wait_st();                     // the first half of P V may start
+    if (!HK_FWD_STLATE && bar_lo != nullptr && c0 == pub) {  // P of keys [0, 64) (and the O rescale) in
+      tmem_wait_st();                                         // TMEM: the first half of P V may start
       tc_fence_before();
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(bar_lo);

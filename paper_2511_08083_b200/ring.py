@@ -11,8 +11,9 @@ each key chunk kc it holds:
 with the CUDA kernels of include/hk_attn.h, folding each partial (O, LSE) into an
 fp32 accumulator with hk_attn_merge (include/hk_ring.h). The backward rotates K,
 V and fp32 dK/dV accumulators; with the final O and LSE every hk_attn_bwd call
-returns its key set's exact share of dQ, dK, dV (hk_accum_bf16 sums them), and
-one more rotation brings dK/dV home.
+returns its key set's exact share of dQ, dK, dV, added straight into the fp32
+accumulators (HK_BWD_ACCUMULATE_F32; with streams > 1, bf16 partials summed by
+hk_accum_bf16), and one more rotation brings dK/dV home.
 
 Every arithmetic step runs in libhkattn.so; this module only schedules calls and
 moves tensors. The exchange is behind `RingComm`: `DistRing` (one rank per
@@ -265,15 +266,30 @@ def ring_attn_bwd(q, k, v, o, lse, do, causal: bool, comm: RingComm, streams: in
                 if ps != s:
                     continue
                 args = (q[li][qh], t[kh], t[2 + kh], o[li][qh], lse[li][qh], do[li][qh])
-                g = [torch.empty_like(args[0]), torch.empty_like(args[1]), torch.empty_like(args[2])]
                 ws = torch.empty(api.bwd_workspace_bytes(args[0].shape[0], args[0].shape[2], args[1].shape[2],
                                                          args[0].shape[1], args[0].shape[3]) // 4,
                                  dtype=torch.float32, device=args[0].device)
+                if streams == 1:
+                    # one stream: the call adds its share straight into the fp32 accumulators
+                    # (HK_BWD_ACCUMULATE_F32) — no bf16 rounding of the per-step partials
+                    if dq_seen[li][qh] == 0:
+                        dq_acc[li][qh].zero_()
+                    dq_seen[li][qh] += 1
+                    api.attn_bwd(*args, mode == "causal", workspace=ws, dq=dq_acc[li][qh], dk=t[4 + kh],
+                                 dv=t[6 + kh], deterministic=True, accumulate=True)
+                    if i == dq_last[li][qh]:
+                        _accum(dq_acc[li][qh], None, dq[li][qh])
+                    continue
+                g = [torch.empty_like(args[0]), torch.empty_like(args[1]), torch.empty_like(args[2])]
                 e = fan.run(lambda args=args, g=g, ws=ws, m=mode:
                             api.attn_bwd(*args, m == "causal", workspace=ws, dq=g[0], dk=g[1], dv=g[2],
                                          deterministic=True))
-                parts.append((li, i, qh, kh, g, e))
-        for li, i, qh, kh, (dq_p, dk_p, dv_p), e in parts:
+                # the workspace (and the partials) stay referenced until the join: freed earlier, the
+                # caching allocator would hand the block to the next call while this one still runs
+                parts.append((li, i, qh, kh, g, e, ws))
+        # streams > 1: calls sharing an accumulator would race, so each writes bf16 partials that are
+        # summed here in fp32 (hk_accum_bf16)
+        for li, i, qh, kh, (dq_p, dk_p, dv_p), e, _ws in parts:
             t = trav[li]
             fan.join(e)
             last = i == dq_last[li][qh]

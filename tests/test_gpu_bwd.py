@@ -104,3 +104,29 @@ def test_bwd_fused_d64(B, N, Hq, Hkv, causal):
         assert rel_l2(np64(dq), np64(det[0])) <= 4e-3
         assert rel_l2(np64(dq), np64(runs[0][0])) <= 4e-4
         assert rel_l2(np64(dq), ref["dQ"]) <= TOL_RELL2
+
+
+@pytest.mark.parametrize("det", [True, False])
+@pytest.mark.parametrize("d,causal", [(128, True), (64, False), (64, True)])
+def test_bwd_accumulate_f32(d, causal, det):
+    """HK_BWD_ACCUMULATE_F32 adds the (scaled, unrounded) gradients into caller fp32 tensors: two
+    calls on the same inputs from a start value A give A + 2 g, with g within fp32 rounding of the
+    bf16 call's result (which rounds g once) and within the BASELINE tolerance of the oracle."""
+    from paper_2511_08083_b200 import attn_bwd, attn_fwd
+    B, N, Hq, Hkv = 2, 333, 4, 2
+    x = gen(B, N, Hq, Hkv, d, seed=40 + d)
+    o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
+    bf = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, deterministic=True)
+    start = [torch.full(t.shape, 0.5, dtype=torch.float32, device="cuda") for t in bf]
+    acc = [t.clone() for t in start]
+    for _ in range(2):
+        attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, dq=acc[0], dk=acc[1], dv=acc[2],
+                 deterministic=det, accumulate=True)
+    torch.cuda.synchronize()
+    ref = oracle.attn_fwd_bwd(np64(x["Q"]), np64(x["K"]), np64(x["V"]), np64(x["dO"]), causal)
+    for name, a, s0, b in zip(("dQ", "dK", "dV"), acc, start, bf):
+        g = (np64(a) - np64(s0)) / 2
+        assert rel_l2(g, np64(b)) <= 4e-3, name          # bf16 rounding of the bf16 call
+        assert rel_l2(g, ref[name]) <= TOL_RELL2, name
+    with pytest.raises(ValueError):
+        attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, accumulate=True)

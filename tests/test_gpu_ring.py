@@ -72,6 +72,7 @@ CASES = [
     (4, 2, 2048, 4, 1, 64),
     (3, 1, 1536, 8, 2, 128),   # c = 256
     (2, 2, 640, 2, 2, 64),     # c = 160: ragged 128-row tiles inside every chunk
+    (8, 1, 2048, 4, 2, 128),   # P = 8: 16 chunks of 128 rows, 8 steps of fp32 accumulation
 ]
 
 
@@ -88,13 +89,17 @@ def test_ring_loopback_matches_whole_sequence(case, causal):
     o = [f[0] for f in fw]
     lse = [f[1] for f in fw]
     bw = ring.ring_attn_bwd(sh["Q"], sh["K"], sh["V"], o, lse, sh["dO"], causal, comm)
-    # the same schedule with each step's calls on 3 side streams: bitwise the same results
+    # the same schedule with each step's calls on 3 side streams: the forward bitwise the same; the
+    # backward there sums bf16-rounded per-call partials (calls sharing an fp32 accumulator would
+    # race), so it agrees with the one-stream fp32-accumulating backward to bf16 rounding
     fw3 = ring.ring_attn_fwd(sh["Q"], sh["K"], sh["V"], causal, comm, streams=3)
     bw3 = ring.ring_attn_bwd(sh["Q"], sh["K"], sh["V"], o, lse, sh["dO"], causal, comm, streams=3)
     torch.cuda.synchronize()
     for r in range(P):
         assert all(torch.equal(a, b) for a, b in zip(fw[r][0] + fw[r][1], fw3[r][0] + fw3[r][1]))
-        assert all(torch.equal(a, b) for x, y in zip(bw[r], bw3[r]) for a, b in zip(x, y))
+        for g1, g3 in zip(bw[r], bw3[r]):
+            for a, b in zip(g1, g3):
+                assert rel_l2(np64(b), np64(a)) <= 4e-3
     O = ring.zigzag_unshard(o)
     LSE = ring.zigzag_unshard([(a.transpose(1, 2), b.transpose(1, 2)) for a, b in lse]).transpose(1, 2)
     dQ, dK, dV = (ring.zigzag_unshard([b[i] for b in bw]) for i in range(3))
