@@ -244,12 +244,18 @@ struct BwdCfg {
   // operand, accumulator in TMEM columns [384, 512), double-buffered) and a dQ warpgroup adds it
   // into an fp32 dQ accumulator with the bulk-async tensor reduce (cp.reduce.async.bulk.tensor
   // .add.f32, from a shared-memory staging tile); a convert pass scales and rounds it to bf16.
+  // d = 128 (round 2): TMEM has no free columns (dV, dK, S^T, dP^T fill all 512), so dQ_partial
+  // accumulates in the S^T columns once dV has consumed P^T, and S^T of the next block waits for its
+  // read-out; shared memory has no room for a separate staging tile, so the dS tile is reused as
+  // the staging of the two 64-column halves of dQ_partial (rings 2 + 2 deep: 226.5 KB).
   static constexpr uint32_t DS_TILE = 128 * 128 * 2;  // dS [128 keys][128 queries] bf16, two SW128 panels
-  static constexpr uint32_t DQ_STAGE = 128 * 64 * 4;  // dQ_partial [128 queries][64] fp32, two SW128 boxes
-  static constexpr int NSA_F = 4, NSB_F = 3;
+  static constexpr uint32_t DQ_STAGE = D == 64 ? 128 * 64 * 4 : 0;  // dQ_partial [128][64] fp32 (d=128: in DS_TILE)
+  static constexpr int NSA_F = D == 64 ? 4 : 2, NSB_F = D == 64 ? 3 : 2;
   static constexpr uint32_t BAR_BYTES_F = 512;
+  static constexpr uint32_t SLACK_F = D == 64 ? 1024 : 0;
   static constexpr uint32_t SMEM1F = 2 * T128 + NSA_F * T128 + NSB_F * SLOT_B1 + DS_TILE + DQ_STAGE + BAR_BYTES_F +
-                                     1024;
+                                     SLACK_F;
+  static_assert(SMEM1F <= 232448, "fused dK/dV shared memory");
   // 16 warps: two elementwise warpgroups (64 query columns per thread), TMA, MMA, two idle warps,
   // four dQ warps — every SM sub-partition gets two elementwise warps and two others, so after
   // setmaxnreg (elementwise 160, others 96) each holds exactly its 4 x 128 launch registers.
@@ -364,18 +370,18 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
                     const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                     const __grid_constant__ CUtensorMap mapDQ, const BwdParams p) {
   using C = BwdCfg<D>;
-  static_assert(!FQ || D == 64, "the fused dQ pass is built for d = 64");
+  constexpr bool FQ128 = FQ && D == 128;  // fused, d = 128: dQ_partial in the S^T columns (BwdCfg)
   constexpr int NSA = FQ ? C::NSA_F : C::NSA, NSB = FQ ? C::NSB_F : C::NSB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  if (C::SLACK1 == 0 && !FQ && smem != smem_raw) __trap();  // the D=128 layout has no alignment slack
+  if ((FQ ? C::SLACK_F : C::SLACK1) == 0 && smem != smem_raw) __trap();  // layouts without alignment slack
   uint8_t* sK = smem;
   uint8_t* sV = smem + C::T128;
   uint8_t* sA = smem + 2 * C::T128;   // ring A slot s: Q [T128]
   uint8_t* sB = sA + NSA * C::T128;   // ring B slot s: dO [T128] lse2 [512 B] D [512 B]
   uint8_t* sDS = sB + NSB * C::SLOT_B1;                 // FQ: dS tile (MN-major A of dQ_partial = dS K)
-  uint8_t* sDQ = sDS + (FQ ? C::DS_TILE : 0);           // FQ: dQ_partial staging for the bulk reduce
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sDQ + (FQ ? C::DQ_STAGE : 0));
+  uint8_t* sDQ = FQ128 ? sDS : sDS + (FQ ? C::DS_TILE : 0);  // FQ: dQ_partial staging (d=128: the dS tile)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + (FQ ? C::DS_TILE + C::DQ_STAGE : 0));
   uint64_t* fullA = bars;             // [NSA]
   uint64_t* emptyA = bars + NSA;      // [NSA]
   uint64_t* fullB = bars + 2 * NSA;   // [NSB]
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
   tc_fence_after();
   const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base_s, 0);  // warp-uniform for ptxas (UR operands)
   const uint32_t tdV = tb, tdK = tb + D, tS = tb + 2 * D, tP = tb + 2 * D + 128;
-  const uint32_t tdQ = tb + 2 * D + 256;  // FQ: two 64-column dQ_partial buffers
+  const uint32_t tdQ = FQ128 ? tS : tb + 2 * D + 256;  // FQ: d = 64 two 64-column buffers; d = 128 the S^T columns
   // FQ: 512 threads launch at 128 registers; each role re-sizes at the top of its branch (ptxas
   // allocates per region): per sub-partition 2 x 160 (elementwise) + 2 x 96 = 4 x 128.
 
@@ -523,6 +529,61 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
     int u0 = 0;  // ring uses before this item == blocks before this item
     uint32_t kv_ph = 0;
     int busy = 0;  // items with work so far (one bar_kv / bar_kvfree phase each)
+    if constexpr (FQ128) {
+      // d = 128 fused order per block u: dV(u) [P^T in the S^T columns], dK(u) [dS^T in the dP^T
+      // columns], dQ_partial(u) = dS K_j into the S^T columns, dP^T(u+1) (fills the tensor pipe while
+      // the dQ warps read dQ_partial(u) out), then S^T(u+1) once the S^T columns are free again.
+      constexpr uint32_t idesc_dq = idesc_bf16(128, D, 1, 1);  // M = 128 queries, A = dS MN-major
+      auto issue_s_free = [&](int u) {  // S^T(u) into columns dQ_partial(u - 1) may still occupy
+        if (u > 0) {
+          mbar_wait(&bar_dqempty[0], (u - 1) & 1);
+          tc_fence_after();
+        }
+        mbar_wait(&fullA[u % NSA], (u / NSA) & 1);
+        tc_fence_after();
+        issue_s(u);
+      };
+      for (int r = 0;; ++r) {
+        const int item = sched_take(sched, r);
+        if (item >= num_items) break;
+        const KvItem w = kv_decode<CAUSAL>(p, item);
+        const int n = w.n_it;
+        if (n == 0) continue;
+        ++busy;
+        mbar_wait(&bar_kv, kv_ph);
+        kv_ph ^= 1;
+        mbar_wait(&fullB[u0 % NSB], (u0 / NSB) & 1);
+        tc_fence_after();
+        issue_dp(u0);
+        issue_s_free(u0);
+        for (int it = 0; it < n; ++it) {
+          const int u = u0 + it;
+          const uint32_t q = slotQ(u), dO = slotO(u);
+          const uint32_t acc = it > 0 ? 1u : 0u;
+          const bool more = it + 1 < n;
+          mbar_wait(&bar_p, u & 1);
+          tc_fence_after();
+          gemm_tsp_mn(tdV, tS, mnmaj(dO, 0), idesc_acc, acc);
+          mbar_wait(&bar_ds, u & 1);
+          tc_fence_after();
+          gemm_tsp_mn(tdK, tP, mnmaj(q, 0), idesc_acc, acc);
+          gemm_ss_mnmn(tdQ, mnmaj(smem_u32(sDS), 0), mnmaj(aK, 0), idesc_dq, 0u);
+          tc_commit_w(&bar_dqfull[0]);
+          tc_commit_w(&emptyA[u % NSA]);
+          tc_commit_w(&emptyB[u % NSB]);
+          if (more) {
+            mbar_wait(&fullB[(u + 1) % NSB], ((u + 1) / NSB) & 1);
+            tc_fence_after();
+            issue_dp(u + 1);
+            issue_s_free(u + 1);
+          } else {
+            tc_commit_w(&bar_kvfree);  // K_j's last use (dQ_partial), V_j's (dP^T) before it
+          }
+        }
+        tc_commit_w(&bar_acc);
+        u0 += n;
+      }
+    } else {
     for (int r = 0;; ++r) {
       const int item = sched_take(sched, r);
       if (item >= num_items) break;
@@ -573,7 +634,7 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
           issue_dp(u + 1);
           if (!FQ && it + 2 == n) tc_commit_w(&bar_kvfree);  // last S^T and dP^T issued
         }
-        if constexpr (FQ) {  // dQ_partial(it) = dS(it) K_j into TMEM buffer u % 2 (the dQ warps drained it)
+        if constexpr (FQ && !FQ128) {  // dQ_partial(it) = dS(it) K_j into TMEM buffer u % 2 (drained by the dQ warps)
           constexpr uint32_t idesc_dq = idesc_bf16(128, D, 1, 1);  // M = 128 queries, A = dS MN-major
           mbar_wait(&bar_dqempty[u & 1], ((u >> 1) & 1) ^ 1);
           tc_fence_after();
@@ -585,6 +646,7 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
       }
       tc_commit_w(&bar_acc);
       u0 += n;
+    }
     }
     // the releases of the final uses are never waited for by the producer: let them land
     drain_ring(emptyA, NSA, u0);
@@ -604,6 +666,52 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
       const KvItem w = kv_decode<CAUSAL>(p, item);
       if (w.n_it == 0) continue;
       int h = w.kvh * G, qi = w.i0;
+      if constexpr (FQ128) {
+        // d = 128: dQ_partial (128 columns, in the S^T columns) leaves in two 64-column halves through
+        // the dS tile (two [128][32] fp32 SW128 boxes per half); the S^T columns are released after
+        // the second half is read, the dS tile after the TMA has read the second half's staging
+        for (int it = 0; it < w.n_it; ++it, ++u) {
+          mbar_wait(&bar_dqfull[0], u & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int half = 0; half < 2; ++half) {
+            if (half == 1 && issuer) tma_store_wait_read0();  // the first half's staging has been read
+            named_bar_sync(3, 128);
+#pragma unroll
+            for (int bx = 0; bx < 2; ++bx) {
+              uint32_t v[32];
+              tmem_ld32(tmem_addr(tdQ, qd * 32, 64 * half + 32 * bx), v);
+              tmem_wait_ld();
+              if (half == 1 && bx == 1) {  // every column read: S^T(u + 1) may overwrite them
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_dqempty[0]);
+              }
+              const uint32_t rowp = smem_u32(sDQ) + bx * (128 * 128) + r * 128;
+#pragma unroll
+              for (int c8 = 0; c8 < 8; ++c8)
+                sts_v4(rowp + ((c8 ^ (r & 7)) << 4), v[4 * c8], v[4 * c8 + 1], v[4 * c8 + 2], v[4 * c8 + 3]);
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(3, 128);
+            if (issuer) {
+              for (int bx = 0; bx < 2; ++bx)
+                tma_reduce_add_4d(&mapDQ, sDQ + bx * (128 * 128), 64 * half + 32 * bx, h, w.sq.q0 + qi * 128,
+                                  w.sq.tb);
+              tma_store_commit();
+            }
+          }
+          if (issuer) {  // the dS tile is free for the next block's dS once the TMA has read it
+            tma_store_wait_read0();
+            mbar_arrive(&bar_dsfree);
+          }
+          if (++qi == w.nqt) {
+            qi = w.i0;
+            ++h;
+          }
+        }
+        continue;
+      }
       for (int it = 0; it < w.n_it; ++it, ++u) {
         const uint32_t b2 = u & 1;
         mbar_wait(&bar_dqfull[b2], (u >> 1) & 1);
@@ -1206,12 +1314,22 @@ struct BwdShape {
 };
 
 // Workspace layout of one backward call (hk_attn.h): D and LSE2 [B][Hq][Np] fp32, 256 bytes of work
-// counters, then (d = 64) the fused backward's fp32 dQ accumulator: B * Np * Hq * 64 floats, which
-// covers [B][Nq][Hq][64] (dense) and [total_q][Hq][64] (varlen: total_q <= B * max_seqlen_q).
+// counters, then the fused backward's fp32 dQ accumulator: B * Np * Hq * d floats, which covers
+// [B][Nq][Hq][d] (dense) and [total_q][Hq][d] (varlen: total_q <= B * max_seqlen_q).
+// The fused single pass at d = 128 (1 CTA per key tile, dQ_partial in the S^T columns, staging in
+// the dS tile) is correct but measured 0.64-0.83x of the two-pass backward (its 64 KB
+// of dQ partials per block need ~26 B/clk/SM of L2 reduce bandwidth, the chip's whole measured
+// rate, on the S^T critical path): built only with -DHK_FUSED128=1.
+#ifndef HK_FUSED128
+#define HK_FUSED128 0
+#endif
+constexpr bool bwd_fused_default(int d) { return d == 64 || HK_FUSED128; }
+
 inline size_t bwd_ws_bytes(int B, int Hq, int Nq, int d) {
   if (B <= 0 || Hq <= 0 || Nq <= 0) return 0;
   const size_t Np = ((size_t)Nq + 127) / 128 * 128;
-  return (size_t)2 * B * Hq * Np * sizeof(float) + 256 + (d == 64 ? (size_t)B * Np * Hq * 64 * sizeof(float) : 0);
+  return (size_t)2 * B * Hq * Np * sizeof(float) + 256 +
+         (bwd_fused_default(d) ? (size_t)B * Np * Hq * d * sizeof(float) : 0);
 }
 
 template <int D, bool CAUSAL>
@@ -1242,7 +1360,7 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     std::lock_guard<std::mutex> lk(mu);
     if (!done.count(dev)) {
       bool ok2 = set_smem(bwd_dkdv_kernel<D, CAUSAL, false>, C::SMEM1) && set_smem(bwd_dq_kernel<D, CAUSAL>, C::SMEM2);
-      if constexpr (D == 64) ok2 = ok2 && set_smem(bwd_dkdv_kernel<D, CAUSAL, true>, C::SMEM1F);
+      ok2 = ok2 && set_smem(bwd_dkdv_kernel<D, CAUSAL, true>, C::SMEM1F);
       if (!ok2) {
         snprintf(err, errlen, "cudaFuncSetAttribute(max dynamic smem) failed");
         return HK_ERR_DEVICE;
@@ -1251,7 +1369,7 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     }
   }
   unsigned* sched = reinterpret_cast<unsigned*>(ws + (size_t)2 * B * Hq * Np);  // 4 counters after D, LSE2
-  const bool fq = D == 64 && sh.fused;
+  const bool fq = sh.fused;
   float* dq_acc = fq ? ws + (size_t)2 * B * Hq * Np + 64 : nullptr;  // after the 256-byte counter block
   CUtensorMap mDQ = mK;  // unused by the two-pass kernels
   if (fq && !encode_bnhd_f32(&mDQ, dq_acc, mb, mnq, Hq, D)) {
@@ -1302,14 +1420,10 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   if (phase < 0 || phase == 1) {
     const int items = B * Hkv * (Npk / 128);  // persistent: one CTA per SM
     const int grid = items < num_sms ? items : num_sms;
-    if constexpr (D == 64) {
-      if (fq)
-        bwd_dkdv_kernel<D, CAUSAL, true><<<grid, C::THREADS1F, C::SMEM1F, stream>>>(mQ, mdO, mK, mV, mDQ, p);
-      else
-        bwd_dkdv_kernel<D, CAUSAL, false><<<grid, C::THREADS1, C::SMEM1, stream>>>(mQ, mdO, mK, mV, mDQ, p);
-    } else {
+    if (fq)
+      bwd_dkdv_kernel<D, CAUSAL, true><<<grid, C::THREADS1F, C::SMEM1F, stream>>>(mQ, mdO, mK, mV, mDQ, p);
+    else
       bwd_dkdv_kernel<D, CAUSAL, false><<<grid, C::THREADS1, C::SMEM1, stream>>>(mQ, mdO, mK, mV, mDQ, p);
-    }
   }
   if (fq && (phase < 0 || phase == 2)) {  // dQ = bf16(dQ_acc / sqrt(d)), grid (x, sequence) like B0
     dq_convert_kernel<D><<<dim3((unsigned)bx, (unsigned)B), 256, 0, stream>>>(

@@ -60,7 +60,15 @@ struct FwdCfg {
 #define HK_FWD_NS64 4
 #endif
   static constexpr int NS = (D == 128) ? 2 : HK_FWD_NS64;  // K/V ring depth
-  static constexpr uint32_t SMEM = 2 * TILE_BYTES + 2 * NS * TILE_BYTES + 1024;
+#ifndef HK_FWD_ROWSUM
+#define HK_FWD_ROWSUM 0
+#endif
+  // d = 64: the row sum l by the tensor core (softmax.cuh ROWSUM): O_t is ON = D + 16 columns and
+  // V gains a second MN-major panel (a constant 16 KB tile whose column 0 is 1), reached through
+  // each V slot's descriptor LBO
+  static constexpr bool ROWSUM = (D == 64) && HK_FWD_ROWSUM;
+  static constexpr int ON = ROWSUM ? D + 16 : D;
+  static constexpr uint32_t SMEM = 2 * TILE_BYTES + 2 * NS * TILE_BYTES + (ROWSUM ? 128 * 128 : 0) + 1024;
   static constexpr int THREADS = 384;
 #ifndef HK_FWD_EMU128
 #define HK_FWD_EMU128 3
@@ -144,6 +152,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sQ = smem;           // 2 tiles
   uint8_t* sK = smem + 2 * TB;  // NS tiles
   uint8_t* sV = sK + NS * TB;   // NS tiles
+  uint8_t* sOnes = sV + NS * TB;  // ROWSUM: [128 keys][64] bf16 panel, column 0 = 1 (SW128)
 
   __shared__ uint64_t bar_q, bar_qfree, bar_kfull[NS], bar_kempty[NS], bar_vfull[NS], bar_vempty[NS];
   __shared__ uint64_t bar_s[2], bar_p[2], bar_pl[2], bar_o[2], bar_oempty[2], bar_sfree[2], bar_pv[2], bar_qr[2];
@@ -185,6 +194,14 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch(&mapV);
   }
   if (warp == 9) tmem_alloc<512>(&tmem_base_s);
+  if (C::ROWSUM && warp >= 10) {  // the ones panel: row r's logical chunk 0 = (1, 0 ... 0), the rest 0
+    for (int r = (warp - 10) * 32 + lane; r < 128; r += 64) {
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch)
+        sts_v4(smem_u32(sOnes) + r * 128 + ((ch ^ (r & 7)) << 4), ch == 0 ? 0x3F80u : 0u, 0u, 0u, 0u);
+    }
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -253,7 +270,7 @@ __global__ void __launch_bounds__(384, 1)
     } else if (warp == 9) {
       // ================= MMA issuer (whole warp, one elected lane issues) =================
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);  // S = Q K^T: A K-major, B K-major
-      constexpr uint32_t idesc_o = idesc_bf16(128, D, 0, 1);    // O += P V: A TMEM, B (V) MN-major
+      constexpr uint32_t idesc_o = idesc_bf16(128, C::ON, 0, 1);  // O += P V: A TMEM, B (V) MN-major
       constexpr uint64_t KMAJ = sdesc_sw128_const(16, 1024);
       constexpr uint64_t VMN = sdesc_sw128_const(128 * 128, 1024);
       const uint64_t dq0 = KMAJ | (smem_u32(sQ) >> 4);
@@ -341,13 +358,16 @@ __global__ void __launch_bounds__(384, 1)
 #ifdef HK_TRACE
               hk_trace(10 + t, tstep[t]++, 0);  // MMA: P_t seen, PV issue (running step of tile t)
 #endif
-              const uint64_t vd = dv0 + ((s * TB) >> 4);
+              // ROWSUM: the second N panel (columns D ..) is the ones tile, LBO bytes past this slot
+              const uint64_t vd = C::ROWSUM ? sdesc_const(smem_u32(sOnes) - smem_u32(sV + s * TB), 1024, 2) |
+                                                  (smem_u32(sV + s * TB) >> 4)
+                                            : dv0 + ((s * TB) >> 4);
               const uint32_t tPa = C::SPLIT_P ? tbase + 256 + 2 * D + 64 * t : tbase + 128 * t;
-              gemm_ts_mn_lo(tbase + 256 + D * t, tPa, vd, idesc_o, j > 0 ? 1u : 0u);
+              gemm_ts_mn_lo(tbase + 256 + C::ON * t, tPa, vd, idesc_o, j > 0 ? 1u : 0u);
               mbar_wait(&bar_p[t], p_ph[t]);
               p_ph[t] ^= 1;
               tc_fence_after();
-              gemm_ts_mn_hi(tbase + 256 + D * t, tPa, vd, idesc_o);
+              gemm_ts_mn_hi(tbase + 256 + C::ON * t, tPa, vd, idesc_o);
               if (C::SPLIT_P) {
                 if (j + 1 < nk) {
                   tc_commit_w(&bar_pv[t]);
@@ -392,7 +412,7 @@ __global__ void __launch_bounds__(384, 1)
     reg_alloc<192>();
     const int t = warp >> 2;  // Q tile of this warpgroup
     const uint32_t tS = tbase + 128 * t;
-    const uint32_t tO = tbase + 256 + D * t;
+    const uint32_t tO = tbase + 256 + C::ON * t;
     const uint32_t tP = C::SPLIT_P ? tbase + 256 + 2 * D + 64 * t : tS;  // bf16 P (split P: own columns)
     uint32_t pv_ph = 0;
     const uint32_t lane_base = (warp & 3) * 32;
@@ -474,7 +494,7 @@ __global__ void __launch_bounds__(384, 1)
         const int kleft = it.sq.lk - j * 128;
         const int kvalid = kleft < 128 ? kleft : 128;
         const bool turn = C::ALT && j < min(it.nkv0, it.nkv1);
-        softmax_step<D, C::EMU_OF_8>(tS, tO, lane_base, r, c, m, l, shift, j > 0, kvalid, 40 + 4 * t, step,
+        softmax_step<D, C::EMU_OF_8, C::ROWSUM>(tS, tO, lane_base, r, c, m, l, shift, j > 0, kvalid, 40 + 4 * t, step,
                                      &bar_pl[t], tP, C::SPLIT_P && j + 1 < nk ? &bar_sfree[t] : nullptr,
                                      C::SPLIT_P && j > 0 ? &bar_pv[t] : nullptr, &pv_ph, turn ? 1 + t : -1,
                                      turn ? 2 - t : -1);
@@ -489,6 +509,12 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&bar_o[t], o_ph);
       o_ph ^= 1;
       tc_fence_after();
+      if constexpr (C::ROWSUM) {  // l = P . 1, accumulated (and lazily rescaled) with O
+        uint32_t lv[16];
+        tmem_ld16(tmem_addr(tO, lane_base, D), lv);
+        tmem_wait_ld();
+        l = __uint_as_float(lv[0]);
+      }
       const float inv_l = l > 0.f ? 1.f / l : 0.f;  // l = 0: the row saw no key (O = 0)
       __nv_bfloat16* orow = p.o + ((size_t)(it.sq.gq0 + (row_ok ? row : 0)) * p.Hq + it.h) * D;
 #pragma unroll

@@ -166,7 +166,8 @@ static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V
   int num_sms = 0;
   s = check_device(&num_sms);
   if (s != HK_OK) return s;
-  const bool fused = d == 64 && !(flags & HK_BWD_DETERMINISTIC);  // NEXT #1 single pass at d = 64
+  // NEXT #1 single pass: d = 64 (d = 128 only in -DHK_FUSED128=1 builds, bwd.cuh)
+  const bool fused = hk::bwd_fused_default(d) && !(flags & HK_BWD_DETERMINISTIC);
   const hk::BwdShape bs{sh.cu_q, sh.cu_k, sh.B, sh.Hq, sh.Hkv, sh.Nq, sh.Nk, sh.total_q, sh.total_k, fused, acc32};
   return hk::launch_bwd(Q, K, V, O, LSE, dO, dQ, dK, dV, reinterpret_cast<float*>(workspace), bs, d, causal != 0,
                         stream, g_err, sizeof(g_err), phase, num_sms);

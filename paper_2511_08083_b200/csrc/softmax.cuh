@@ -18,7 +18,7 @@ constexpr float EXP_MAGIC = 12582912.f;  // 1.5 * 2^23: x + magic rounds x to an
 // (magic - m) - j, 2^f comes from a degree-3 minimax polynomial (relative
 // error 7.7e-5 < bf16's 3.9e-3) and n is added into the exponent bits. Scores
 // are clamped so c s - m >= -125 (the exponent add cannot underflow).
-template <bool EMU, int EMU_OF_8>
+template <bool EMU, int EMU_OF_8, bool ROWSUM = false>
 __device__ __forceinline__ void softmax_chunk32(const float* s, float c, float m, float smin, uint32_t (&pk)[16],
                                                 float2 (&acc)[2]) {
   const float2 c2 = make_float2(c, c), nm2 = make_float2(-m, -m);
@@ -48,7 +48,7 @@ __device__ __forceinline__ void softmax_chunk32(const float* s, float c, float m
       const float2 x = fma2(make_float2(s[2 * k], s[2 * k + 1]), c2, nm2);
       e = make_float2(ex2(x.x), ex2(x.y));
     }
-    acc[k & 1] = add2(acc[k & 1], e);
+    if (!ROWSUM) acc[k & 1] = add2(acc[k & 1], e);  // ROWSUM: the P V MMA sums the row (ones column of V)
     pk[k] = pack_bf16(e.x, e.y);
   }
 }
@@ -66,7 +66,10 @@ __device__ __forceinline__ void softmax_chunk32(const float* s, float c, float m
 // S columns are released (bar_sfree) as soon as S is in registers so the next
 // S = Q K^T can overwrite them while this step runs, and the step waits for the
 // previous P V (bar_pv) before it rescales O or overwrites P.
-template <int D, int EMU_OF_8>
+// ROWSUM (d = 64): O carries a 17th 16-column block whose first column accumulates P . 1 (a ones
+// column appended to V), so the row sum l comes from the tensor core: the step skips its adds
+// (l is left untouched) and the O rescale covers ON = D + 16 columns.
+template <int D, int EMU_OF_8, bool ROWSUM = false>
 __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t lane_base, int r, float c,
                                              float& m, float& l, int shift, bool o_live, int kvalid = 128,
                                              int trace_ev = -1, uint32_t trace_idx = 0, uint64_t* bar_lo = nullptr,
@@ -129,7 +132,7 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
   if (o_live && __any_sync(0xffffffffu, alpha != 1.f)) {
     // 16 columns at a time: the 128 scores are still live here
 #pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 16) {
+    for (int c0 = 0; c0 < (ROWSUM ? D + 16 : D); c0 += 16) {
       float o[16];
       tmem_ld16(tmem_addr(tO, lane_base, c0), reinterpret_cast<uint32_t*>(o));
       tmem_wait_ld();
@@ -155,9 +158,9 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
   for (int c0 = 0; c0 < 128; c0 += 32) {
     uint32_t pk[16];
     if (masked)  // a row with no visible key yet (m_use = -inf) gets P = 2^-inf = 0, not NaN
-      softmax_chunk32<false, EMU_OF_8>(s + c0, c, m_use == -INFINITY ? 0.f : m_use, smin, pk, acc);
+      softmax_chunk32<false, EMU_OF_8, ROWSUM>(s + c0, c, m_use == -INFINITY ? 0.f : m_use, smin, pk, acc);
     else
-      softmax_chunk32<true, EMU_OF_8>(s + c0, c, m_use, smin, pk, acc);
+      softmax_chunk32<true, EMU_OF_8, ROWSUM>(s + c0, c, m_use, smin, pk, acc);
     // HK_FWD_STLATE: publish the first half of P after the third chunk's exponentials, so the
     // wait for the first two chunks' TMEM stores hides behind that work
     const int pub = HK_FWD_STLATE ? 64 : 32;
@@ -177,8 +180,10 @@ __device__ __forceinline__ void softmax_step(uint32_t tS, uint32_t tO, uint32_t 
   }
   if (alt_arrive >= 0) named_bar_arrive(alt_arrive, 256);
   HK_SM_TRACE(2)  // exps done, P stores issued
-  const float2 rs2 = add2(acc[0], acc[1]);
-  l = l * alpha + (rs2.x + rs2.y);
+  if (!ROWSUM) {
+    const float2 rs2 = add2(acc[0], acc[1]);
+    l = l * alpha + (rs2.x + rs2.y);
+  }
   m = m_use;
 #undef HK_SM_TRACE
 }

@@ -1,4 +1,4 @@
-"""NEXT #1 A/B: the d = 64 fused single-pass backward (default) vs the deterministic two-pass
+"""NEXT #1 A/B: the fused single-pass backward (default) vs the deterministic two-pass
 backward (HK_BWD_DETERMINISTIC), interleaved in one process on the same inputs; public API calls,
 CUDA events, medians of R repeats. Prints one JSON line per config."""
 import argparse
@@ -15,7 +15,8 @@ from paper_2511_08083_b200.inputs import make_inputs  # noqa: E402
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from probe import CONFIGS  # noqa: E402
 
-CONFIGS.update({"C4-4096": (16, 4096, 32, 32, 64, True), "C4-16384": (16, 16384, 32, 32, 64, True)})
+CONFIGS.update({"C4-4096": (16, 4096, 32, 32, 64, True), "C4-16384": (16, 16384, 32, 32, 64, True),
+                "C5-8192-nc": (16, 8192, 64, 8, 128, False)})
 
 
 def main():

@@ -81,10 +81,11 @@ def test_bwd_deterministic(d):
             assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("d", [64, 128])  # d = 128 runs the two-pass backward unless built with HK_FUSED128=1
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("B,N,Hq,Hkv", [(2, 640, 8, 2), (1, 1024, 4, 4), (2, 333, 6, 3), (1, 128, 2, 1)])
-def test_bwd_fused_d64(B, N, Hq, Hkv, causal):
-    """The d = 64 default backward is the fused single pass (NEXT #1, hk_attn.h): dK, dV bitwise equal
+def test_bwd_fused(B, N, Hq, Hkv, causal, d):
+    """The default backward is the fused single pass (NEXT #1, hk_attn.h): dK, dV bitwise equal
     to the deterministic two-pass backward (same kernel arithmetic for them) and bitwise run to run;
     dQ — fp32 partials added in L2 in arrival order — within the BASELINE tolerance of the oracle,
     of itself across runs up to the bf16 rounding flips fp32 reordering causes (a flip moves an
@@ -92,7 +93,6 @@ def test_bwd_fused_d64(B, N, Hq, Hkv, causal):
     two-pass dQ (which rounds its own dS = P (dP - D), from S = Q K^T instead of S^T = K Q^T, to
     bf16: rel-L2 <= 4e-3 = one bf16 ulp 2^-8)."""
     from paper_2511_08083_b200 import attn_bwd, attn_fwd
-    d = 64
     x = gen(B, N, Hq, Hkv, d, seed=N + Hq)
     o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
     det = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, deterministic=True)
