@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
 #define HK_PRE_U128 2
 #endif
 #ifndef HK_PRE_U64
-#define HK_PRE_U64 2
+#define HK_PRE_U64 4  // r2: with the fused backward's dQ-accumulator zeroing, 4 is 1.10x at C4-8192 (profiles/ab_pre_u_r2r.jsonl)
 #endif
   constexpr int U = D == 128 ? HK_PRE_U128 : HK_PRE_U64;  // measured (scripts/ab.py): 2 for both since the 32-bit (h, n) division
   // One warp iteration's rows: their O / dO vectors, LSE and (h, n).

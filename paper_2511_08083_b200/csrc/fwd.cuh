@@ -61,7 +61,7 @@ struct FwdCfg {
 #endif
   static constexpr int NS = (D == 128) ? 2 : HK_FWD_NS64;  // K/V ring depth
 #ifndef HK_FWD_ROWSUM
-#define HK_FWD_ROWSUM 0
+#define HK_FWD_ROWSUM 1  // C4 forward 1.05-1.08x (profiles/ab_fwd_rowsum_r2p.jsonl); reading #28
 #endif
   // d = 64: the row sum l by the tensor core (softmax.cuh ROWSUM): O_t is ON = D + 16 columns and
   // V gains a second MN-major panel (a constant 16 KB tile whose column 0 is 1), reached through
@@ -74,7 +74,7 @@ struct FwdCfg {
 #define HK_FWD_EMU128 3
 #endif
 #ifndef HK_FWD_EMU64
-#define HK_FWD_EMU64 3
+#define HK_FWD_EMU64 4  // with the row sum on the tensor core: 1.02x at C4-8192 (profiles/ab_fwd_emu64_r2q.jsonl)
 #endif
   static constexpr int EMU_OF_8 = (D == 128) ? HK_FWD_EMU128 : HK_FWD_EMU64;  // exps per 8 on the FMA pipe
 #ifndef HK_FWD_ALT

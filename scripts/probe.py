@@ -24,7 +24,8 @@ CONFIGS = {
     "C5-8192-nc": (16, 8192, 64, 8, 128, False),
     "C5-16384-nc": (16, 16384, 64, 8, 128, False),
     "C5-16384-c": (16, 16384, 64, 8, 128, True),
-    "C4-2048": (16, 2048, 32, 32, 64, True),
+    "C4-4096": (16, 4096, 32, 32, 64, True),
+    "C4-16384": (16, 16384, 32, 32, 64, True),
 }
 
 
