@@ -68,7 +68,15 @@ struct FwdCfg {
   // each V slot's descriptor LBO
   static constexpr bool ROWSUM = (D == 64) && HK_FWD_ROWSUM;
   static constexpr int ON = ROWSUM ? D + 16 : D;
-  static constexpr uint32_t SMEM = 2 * TILE_BYTES + 2 * NS * TILE_BYTES + (ROWSUM ? 128 * 128 : 0) + 1024;
+  // epilogue staging: one 16 KB SW128 panel [128 rows][64 columns] bf16 per Q tile; O leaves through a TMA
+  // store of whole rows instead of per-thread row stores (HK_FWD_OSTAGE)
+#ifndef HK_FWD_OSTAGE
+#define HK_FWD_OSTAGE 1
+#endif
+  static constexpr bool OSTAGE = HK_FWD_OSTAGE != 0;
+  static constexpr uint32_t STAGE_BYTES = OSTAGE ? 2 * 128 * 128 : 0;
+  static constexpr uint32_t SMEM =
+      2 * TILE_BYTES + 2 * NS * TILE_BYTES + (ROWSUM ? 128 * 128 : 0) + STAGE_BYTES + 1024;
   static constexpr int THREADS = 384;
 #ifndef HK_FWD_EMU128
 #define HK_FWD_EMU128 3
@@ -142,7 +150,8 @@ __device__ __forceinline__ int fwd_next_busy(const FwdParams& p, int r, int cta,
 template <int D, bool CAUSAL, bool ROPE>
 __global__ void __launch_bounds__(384, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
-               const __grid_constant__ CUtensorMap mapV, const FwdParams p) {
+               const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapO,
+               const FwdParams p) {
   using C = FwdCfg<D>;
   constexpr int NS = C::NS;
   constexpr uint32_t TB = C::TILE_BYTES;
@@ -153,6 +162,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sK = smem + 2 * TB;  // NS tiles
   uint8_t* sV = sK + NS * TB;   // NS tiles
   uint8_t* sOnes = sV + NS * TB;  // ROWSUM: [128 keys][64] bf16 panel, column 0 = 1 (SW128)
+  uint8_t* sStage = sOnes + (C::ROWSUM ? 128 * 128 : 0);  // OSTAGE: O staging panel of tile t at t * 16 KB
 
   __shared__ uint64_t bar_q, bar_qfree, bar_kfull[NS], bar_kempty[NS], bar_vfull[NS], bar_vempty[NS];
   __shared__ uint64_t bar_s[2], bar_p[2], bar_pl[2], bar_o[2], bar_oempty[2], bar_sfree[2], bar_pv[2], bar_qr[2];
@@ -192,6 +202,7 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch(&mapQ);
     tma_prefetch(&mapK);
     tma_prefetch(&mapV);
+    if (C::OSTAGE) tma_prefetch(&mapO);
   }
   if (warp == 9) tmem_alloc<512>(&tmem_base_s);
   if (C::ROWSUM && warp >= 10) {  // the ones panel: row r's logical chunk 0 = (1, 0 ... 0), the rest 0
@@ -214,12 +225,21 @@ __global__ void __launch_bounds__(384, 1)
     reg_dealloc<112>();
     if (warp == 8 && lane == 0) {
       // ================= TMA producer =================
-      const uint64_t pol_q = policy_evict_first();
+#ifndef HK_FWD_QPOL
+#define HK_FWD_QPOL 0
+#endif
+      const uint64_t pol_q = HK_FWD_QPOL ? policy_evict_last() : policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
       int s = 0;
       uint32_t ph = 0, qf_ph = 0;
+#ifdef HK_TRACE
+      uint32_t nq_tr = 0;
+#endif
       auto load_kv = [&](const FwdItem& it, int j) {
         mbar_wait(&bar_kempty[s], ph ^ 1);
+#ifdef HK_TRACE
+        if (j == 0) hk_trace(22, nq_tr, 0);  // producer: K_0 load issued
+#endif
         const int row = it.sq.k0 + j * 128;
         mbar_arrive_expect_tx(&bar_kfull[s], TB);
         for (int pnl = 0; pnl < C::PANELS; ++pnl)
@@ -250,12 +270,28 @@ __global__ void __launch_bounds__(384, 1)
         }
         const FwdItem it = fwd_decode<CAUSAL>(p, item);
         if (it.nkv == 0) continue;
-        load_kv(it, 0);  // K/V of the next item stream in while the previous one finishes
+#ifndef HK_FWD_QPREF
+#define HK_FWD_QPREF 0
+#endif
+        if (HK_FWD_QPREF && !dyn && r >= 0) {  // static order: warm L2 with the following item's Q tiles (first touch = HBM)
+          const FwdItem nx = fwd_decode<CAUSAL>(p, fwd_item_index<CAUSAL>(r, cta, ctas));
+          for (int pnl = 0; pnl < C::PANELS; ++pnl) {
+            if (nx.nkv0 > 0) tma_prefetch_4d(&mapQ, pnl * 64, nx.h, nx.sq.q0 + nx.qt0 * 128, nx.sq.tb);
+            if (nx.nkv1 > 0) tma_prefetch_4d(&mapQ, pnl * 64, nx.h, nx.sq.q0 + nx.qt1 * 128, nx.sq.tb);
+          }
+        }
+#ifndef HK_FWD_QFIRST
+#define HK_FWD_QFIRST 0
+#endif
+        if (!HK_FWD_QFIRST) load_kv(it, 0);  // K/V of the next item stream in while the previous one finishes
         if (!first) {    // Q buffer is free once the previous item's last S = Q K^T completed
           mbar_wait(&bar_qfree, qf_ph);
           qf_ph ^= 1;
         }
         first = false;
+#ifdef HK_TRACE
+        hk_trace(17, nq_tr++, 0);  // producer: Q load issued
+#endif
         const bool has0 = it.nkv0 > 0, has1 = it.nkv1 > 0;
         mbar_arrive_expect_tx(&bar_q, ((has0 ? 1 : 0) + (has1 ? 1 : 0)) * TB);
         for (int pnl = 0; pnl < C::PANELS; ++pnl) {
@@ -265,7 +301,7 @@ __global__ void __launch_bounds__(384, 1)
             tma_load_4d(&mapQ, &bar_q, sQ + TB + pnl * 128 * 128, pnl * 64, it.h, it.sq.q0 + it.qt1 * 128, it.sq.tb,
                         pol_q);
         }
-        for (int j = 1; j < it.nkv; ++j) load_kv(it, j);
+        for (int j = HK_FWD_QFIRST ? 0 : 1; j < it.nkv; ++j) load_kv(it, j);
       }
     } else if (warp == 9) {
       // ================= MMA issuer (whole warp, one elected lane issues) =================
@@ -308,10 +344,19 @@ __global__ void __launch_bounds__(384, 1)
         const bool last_item = !dyn && rn < 0;
         uses += it.nkv;
         ++busy;
+#ifdef HK_TRACE
+        hk_trace(12, busy - 1, 0);  // MMA: item start
+#endif
         if (!ROPE) mbar_wait(&bar_q, q_ph);
         q_ph ^= 1;
+#ifdef HK_TRACE
+        hk_trace(13, busy - 1, 0);  // MMA: Q landed
+#endif
         mbar_wait(&bar_kfull[s], ph);
         tc_fence_after();
+#ifdef HK_TRACE
+        hk_trace(24, busy - 1, 0);  // MMA: K_0 landed
+#endif
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           if ((t == 0 ? it.nkv0 : it.nkv1) == 0) continue;
@@ -321,8 +366,14 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_after();
           }
           issue_s(t, s);
+#ifdef HK_TRACE
+          hk_trace(25 + t, busy - 1, 0);  // MMA: first S_t of the item issued
+#endif
         }
         tc_commit_w(&bar_kempty[s]);
+#ifdef HK_TRACE
+        hk_trace(14, busy - 1, 0);  // MMA: first S of the item issued
+#endif
         if (it.nkv == 1 && !last_item) tc_commit_w(&bar_qfree);
         for (int j = 0; j < it.nkv; ++j) {
           const int s1 = s + 1 == NS ? 0 : s + 1;
@@ -354,6 +405,9 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_wait(&bar_oempty[t], oe_ph[t]);
                 oe_ph[t] ^= 1;
               }
+#ifdef HK_TRACE
+              if (j == 0) hk_trace(18 + t, busy - 1, 0);  // MMA: first P V of the item may issue
+#endif
               tc_fence_after();
 #ifdef HK_TRACE
               hk_trace(10 + t, tstep[t]++, 0);  // MMA: P_t seen, PV issue (running step of tile t)
@@ -385,6 +439,9 @@ __global__ void __launch_bounds__(384, 1)
               } else {
                 tc_commit_w(&bar_o[t]);
                 o_used[t] = true;
+#ifdef HK_TRACE
+                hk_trace(15 + t, busy - 1, 0);  // MMA: last P V of tile t issued
+#endif
               }
             }
           }
@@ -396,6 +453,9 @@ __global__ void __launch_bounds__(384, 1)
           s = s1;
           ph = ph1;
         }
+#ifdef HK_TRACE
+        hk_trace(20, busy - 1, 0);  // MMA: item loop done
+#endif
       }
       if (dyn) {  // let the releases nothing waits for land before the CTA exits
         for (int k = 0; k < NS && k < uses; ++k) {
@@ -509,6 +569,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&bar_o[t], o_ph);
       o_ph ^= 1;
       tc_fence_after();
+      if (threadIdx.x % 128 == 0) hk_trace(33 + t, rr, 0);  // epilogue of tile t: O complete
       if constexpr (C::ROWSUM) {  // l = P . 1, accumulated (and lazily rescaled) with O
         uint32_t lv[16];
         tmem_ld16(tmem_addr(tO, lane_base, D), lv);
@@ -516,26 +577,65 @@ __global__ void __launch_bounds__(384, 1)
         l = __uint_as_float(lv[0]);
       }
       const float inv_l = l > 0.f ? 1.f / l : 0.f;  // l = 0: the row saw no key (O = 0)
-      __nv_bfloat16* orow = p.o + ((size_t)(it.sq.gq0 + (row_ok ? row : 0)) * p.Hq + it.h) * D;
+      if (C::OSTAGE && !CAUSAL && (qt + 1) * 128 <= it.sq.lq) {
+        // non-causal, whole tile inside the sequence: all of O_t into registers (O_t free for the next
+        // item's P V at once), then 64-column panels through this tile's SW128 staging panel and a TMA
+        // store, so rows leave as full 128-B lines. (Causal: the other tile is still in its last,
+        // extra step, which this burst of TMEM reads and stores slows: the interleaved form below
+        // measured faster there, profiles/ab_fwd_ostage_r2ac.jsonl.)
+        uint32_t o[D];
 #pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 32) {
-        uint32_t o[32];
-        tmem_ld32(tmem_addr(tO, lane_base, c0), o);
+        for (int c0 = 0; c0 < D; c0 += 32)
+          tmem_ld32(tmem_addr(tO, lane_base, c0), *reinterpret_cast<uint32_t(*)[32]>(&o[c0]));
         tmem_wait_ld();
-        if (c0 + 32 == D) {  // O_t fully read: the next item's P V may overwrite it
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bar_oempty[t]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_oempty[t]);
+        if (threadIdx.x % 128 == 0) hk_trace(35 + t, rr, 0);  // O read out of TMEM
+        const uint32_t stg = smem_u32(sStage) + t * (128 * 128);
+#pragma unroll
+        for (int pnl = 0; pnl < C::PANELS; ++pnl) {
+          if (threadIdx.x % 128 == 0) tma_store_wait_read0();  // the previous store has read the panel
+          named_bar_sync(3 + t, 128);
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            const int cb = pnl * 64 + ch * 8;
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              w[k] = pack_bf16(__uint_as_float(o[cb + 2 * k]) * inv_l, __uint_as_float(o[cb + 2 * k + 1]) * inv_l);
+            sts_v4(stg + r * 128 + ((ch ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
+          }
+          fence_proxy_async_smem();  // generic-proxy stores visible to the TMA engine
+          named_bar_sync(3 + t, 128);
+          if (threadIdx.x % 128 == 0) {
+            tma_store_4d(&mapO, sStage + t * (128 * 128), pnl * 64, it.h, it.sq.q0 + qt * 128, it.sq.tb);
+            tma_store_commit();
+          }
         }
-        uint4 v[4];
-        uint32_t* vp = reinterpret_cast<uint32_t*>(v);
+      } else {
+        __nv_bfloat16* orow = p.o + ((size_t)(it.sq.gq0 + (row_ok ? row : 0)) * p.Hq + it.h) * D;
 #pragma unroll
-        for (int cc = 0; cc < 16; ++cc)
-          vp[cc] = pack_bf16(__uint_as_float(o[2 * cc]) * inv_l, __uint_as_float(o[2 * cc + 1]) * inv_l);
-        uint4* dst = reinterpret_cast<uint4*>(orow + c0);
-        if (row_ok) {
+        for (int c0 = 0; c0 < D; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem_addr(tO, lane_base, c0), o);
+          tmem_wait_ld();
+          if (c0 + 32 == D) {  // O_t fully read: the next item's P V may overwrite it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_oempty[t]);
+            if (threadIdx.x % 128 == 0) hk_trace(35 + t, rr, 0);  // O read out of TMEM
+          }
+          uint4 v[4];
+          uint32_t* vp = reinterpret_cast<uint32_t*>(v);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) dst[q] = v[q];
+          for (int cc = 0; cc < 16; ++cc)
+            vp[cc] = pack_bf16(__uint_as_float(o[2 * cc]) * inv_l, __uint_as_float(o[2 * cc + 1]) * inv_l);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+          if (row_ok) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = v[q];
+          }
         }
       }
       if (row_ok)
@@ -546,6 +646,7 @@ __global__ void __launch_bounds__(384, 1)
   }
 
   if (C::ALT && warp < 4) named_bar_sync(1, 256);  // tile 1's opening arrive (or its last turn's)
+  if (C::OSTAGE && warp < 8 && threadIdx.x % 128 == 0) tma_store_wait0();  // O stores done before exit
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc<512>(tbase);

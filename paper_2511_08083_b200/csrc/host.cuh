@@ -116,7 +116,8 @@ hk_status validate_common(const Shape& sh, int d) {
 size_t ws_bytes(int B, int Hq, int Nq, int d) { return hk::bwd_ws_bytes(B, Hq, Nq, d); }
 
 template <int D, bool CAUSAL, bool ROPE = false>
-hk_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const hk::FwdParams& p,
+hk_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
+                     const hk::FwdParams& p,
                      int num_sms, cudaStream_t stream) {
   using C = hk::FwdCfg<D>;
   auto* fn = hk::fwd_kernel<D, CAUSAL, ROPE>;
@@ -124,7 +125,7 @@ hk_status launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
   if (s != HK_OK) return s;
   // persistent: one CTA per SM (the SMEM footprint allows one), items in snake order
   dim3 grid(p.num_items < num_sms ? p.num_items : num_sms);
-  fn<<<grid, C::THREADS, C::SMEM, stream>>>(mq, mk, mv, p);
+  fn<<<grid, C::THREADS, C::SMEM, stream>>>(mq, mk, mv, mo, p);
   return launched("hk_attn_fwd");
 }
 
@@ -200,9 +201,9 @@ static hk_status fwd_impl(const void* Q, const void* K, const void* V, void* O, 
 
   const bool varlen = sh.cu_q != nullptr;
   const int mb = varlen ? 1 : sh.B, mnq = varlen ? sh.total_q : sh.Nq, mnk = varlen ? sh.total_k : sh.Nk;
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mo;
   if (!hk::encode_bnhd(&mq, Q, mb, mnq, sh.Hq, d, 128) || !hk::encode_bnhd(&mk, K, mb, mnk, sh.Hkv, d, 128) ||
-      !hk::encode_bnhd(&mv, V, mb, mnk, sh.Hkv, d, 128))
+      !hk::encode_bnhd(&mv, V, mb, mnk, sh.Hkv, d, 128) || !hk::encode_bnhd(&mo, O, mb, mnq, sh.Hq, d, 128))
     return fail(HK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (CUresult %d)", hk::last_encode_result());
   hk::FwdParams p;
   p.lse = LSE;
@@ -220,16 +221,16 @@ static hk_status fwd_impl(const void* Q, const void* K, const void* V, void* O, 
     return fail(HK_ERR_LAUNCH, "cudaMemsetAsync(workspace counters) failed");
   if (rope_cos) {
     if (d == 64)
-      return causal ? launch_fwd<64, true, true>(mq, mk, mv, p, num_sms, stream)
-                    : launch_fwd<64, false, true>(mq, mk, mv, p, num_sms, stream);
-    return causal ? launch_fwd<128, true, true>(mq, mk, mv, p, num_sms, stream)
-                  : launch_fwd<128, false, true>(mq, mk, mv, p, num_sms, stream);
+      return causal ? launch_fwd<64, true, true>(mq, mk, mv, mo, p, num_sms, stream)
+                    : launch_fwd<64, false, true>(mq, mk, mv, mo, p, num_sms, stream);
+    return causal ? launch_fwd<128, true, true>(mq, mk, mv, mo, p, num_sms, stream)
+                  : launch_fwd<128, false, true>(mq, mk, mv, mo, p, num_sms, stream);
   }
   if (d == 64)
-    return causal ? launch_fwd<64, true>(mq, mk, mv, p, num_sms, stream)
-                  : launch_fwd<64, false>(mq, mk, mv, p, num_sms, stream);
-  return causal ? launch_fwd<128, true>(mq, mk, mv, p, num_sms, stream)
-                : launch_fwd<128, false>(mq, mk, mv, p, num_sms, stream);
+    return causal ? launch_fwd<64, true>(mq, mk, mv, mo, p, num_sms, stream)
+                  : launch_fwd<64, false>(mq, mk, mv, mo, p, num_sms, stream);
+  return causal ? launch_fwd<128, true>(mq, mk, mv, mo, p, num_sms, stream)
+                : launch_fwd<128, false>(mq, mk, mv, mo, p, num_sms, stream);
 }
 
 static Shape dense(int B, int Hq, int Hkv, int Nq, int Nk) { return Shape{nullptr, nullptr, B, Hq, Hkv, Nq, Nk, 0, 0}; }

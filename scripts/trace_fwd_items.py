@@ -49,3 +49,47 @@ for cfg in sys.argv[1:]:
                            "softmax_step": round(st.median(X), 0) if X else None}
     print(json.dumps(out), flush=True)
     del x
+    # item-boundary breakdown (events: 12 MMA item start, 13 Q landed, 14 first S issued,
+    # 15+t last PV of tile t issued, 18+t first PV of tile t may issue, 17 producer Q issued,
+    # 33+t epilogue O complete, 35+t O read out, 31+t epilogue done; indices = busy item number)
+    def ev(e, a):
+        v = int(tab[e, a])
+        return v if v else None
+    nb = sum(1 for a in range(1024) if tab[12, a])
+    rows = []
+    for k in range(1, nb):
+        r = {"q_issue": ev(17, k), "mma_start": ev(12, k), "q_landed": ev(13, k), "s_issued": ev(14, k),
+             "k0_issue": ev(22, k), "k0_landed": ev(24, k), "loop_done": ev(20, k - 1),
+             "s0_issued": ev(25, k), "s1_issued": ev(26, k)}
+        for t in (0, 1):
+            r[f"lastpv{t}"] = ev(15 + t, k - 1)
+            r[f"ep_o{t}"] = ev(33 + t, k - 1)
+            r[f"ep_read{t}"] = ev(35 + t, k - 1)
+            r[f"ep_done{t}"] = ev(31 + t, k - 1)
+            r[f"pv0_{t}"] = ev(18 + t, k)
+        if all(v is not None for v in r.values()):
+            rows.append(r)
+
+    def med(f):
+        return round(st.median([f(r) for r in rows]), 0) if rows else None
+    out2 = {"config": cfg, "items": len(rows),
+            "lastpv1->mma_next_start": med(lambda r: r["mma_start"] - r["lastpv1"]),
+            "q_issue->q_landed": med(lambda r: r["q_landed"] - r["q_issue"]),
+            "mma_start->q_landed": med(lambda r: r["q_landed"] - r["mma_start"]),
+            "q_landed->s_issued": med(lambda r: r["s_issued"] - r["q_landed"]),
+            "q_issue_before_lastpv1": med(lambda r: r["lastpv1"] - r["q_issue"]),
+            "lastpv1->loop_done": med(lambda r: r["loop_done"] - r["lastpv1"]),
+            "loop_done->mma_start": med(lambda r: r["mma_start"] - r["loop_done"]),
+            "k0_issue->k0_landed": med(lambda r: r["k0_landed"] - r["k0_issue"]),
+            "k0_issue_before_q_issue": med(lambda r: r["q_issue"] - r["k0_issue"]),
+            "q_landed->k0_landed": med(lambda r: r["k0_landed"] - r["q_landed"]),
+            "k0_landed->s0_issued": med(lambda r: r["s0_issued"] - r["k0_landed"]),
+            "s0_issued->s1_issued": med(lambda r: r["s1_issued"] - r["s0_issued"]),
+            "s1_issued->s_issued": med(lambda r: r["s_issued"] - r["s1_issued"])}
+    for t in (0, 1):
+        out2[f"t{t}"] = {"lastpv->O_complete": med(lambda r: r[f"ep_o{t}"] - r[f"lastpv{t}"]),
+                         "O_complete->O_read": med(lambda r: r[f"ep_read{t}"] - r[f"ep_o{t}"]),
+                         "O_read->ep_done": med(lambda r: r[f"ep_done{t}"] - r[f"ep_read{t}"]),
+                         "lastpv->next_first_pv_ok": med(lambda r: r[f"pv0_{t}"] - r[f"lastpv{t}"]),
+                         "s_issued->first_pv_ok": med(lambda r: r[f"pv0_{t}"] - r["s_issued"])}
+    print(json.dumps(out2), flush=True)
