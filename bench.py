@@ -449,7 +449,27 @@ def time_breakdown(pb, steps, warmup, world):
     return {n: statistics.fmean(t) for n, t in per.items()}
 
 
-def kernel_table(pb, kern_ms, peaks, world):
+def smem_port_model(pb, dom, ms, sm_mhz):
+    """Second roofline of the d = 128 dK/dV pass (DESIGN.md §6 "SMEM bandwidth"): shared-memory port
+    cycles per 128x128 block = (tensor-core SS operand reads 192 KB + TMA writes of Q_i, dO_i 64 KB
+    + the LSE2/D broadcast ld.shared.v4, 8 warps x 32 x 2 wavefronts x 128 B = 64 KB-equivalent)
+    / 128 B/clk/SM, against the kernel's measured time at the sampled SM clock. A model: the port
+    width and the wavefront costs are the ones DESIGN.md §6 measured, not an ncu counter."""
+    if dom != "bwd_dkdv" or pb.d != 128 or not sm_mhz:
+        return None
+    nt = (pb.N + 127) // 128
+    blocks_per_head = nt * (nt + 1) // 2 if pb.causal else nt * nt
+    blocks = pb.B * pb.Hq * blocks_per_head
+    kb_per_block = 192 + 64 + 64
+    bytes_ = blocks * kb_per_block * 1024
+    achieved = bytes_ / (ms * 1e-3) / 1e12
+    peak = 128 * 148 * sm_mhz * 1e6 / 1e12
+    return {"bound": "smem_port", "unit": "TB/s", "achieved": round(achieved, 2), "peak": round(peak, 2),
+            "frac": round(achieved / peak, 4), "model_kb_per_block": kb_per_block, "blocks_per_launch": blocks,
+            "peak_basis": f"128 B/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (sampled median under load)"}
+
+
+def kernel_table(pb, kern_ms, peaks, world, sm_mhz=None):
     """Per-kernel algorithmic / executed rates and the roofline of the dominant kernel."""
     ff = pb.fwd_flops
     B, N, Hq, d = pb.B, pb.N, pb.Hq, pb.d
@@ -490,6 +510,9 @@ def kernel_table(pb, kern_ms, peaks, world):
             "frac_of_spec_2250": round(ach / SPEC_PEAK_TFLOPS, 4),
             "algorithmic_flops_per_launch": alg[dom], "executed_flops_per_launch": execd[dom],
             "timing": "mean launch duration from CUDA events between kernels (timed region 2)"}
+    sp = smem_port_model(pb, dom, kern_ms[dom], sm_mhz)
+    if sp is not None:
+        roof["smem_port"] = sp
     return table, roof, dom
 
 
@@ -513,14 +536,15 @@ def sub_record(name, args, peaks):
     a = argparse.Namespace(**{**vars(args), "steps": steps})
     step_ms, fwd_ms, bwd_ms, wall, clk, ms, _, kern_ms = measure(pb, a, 1, 0, with_clocks=True)
     ff = pb.fwd_flops
-    table, roof, dom = kernel_table(pb, kern_ms, peaks, 1)
+    table, roof, dom = kernel_table(pb, kern_ms, peaks, 1, (clk or {}).get("sm_mhz"))
     rec = {"workload": name, "label": pb.cfg[6], "steps": steps, "ms_per_step": round(ms, 4),
            "fwd_bwd_tflops": round(3.5 * ff / (ms * 1e-3) / 1e12, 1),
            "fwd_tflops": round(ff / (statistics.fmean(fwd_ms) * 1e-3) / 1e12, 1),
            "bwd_tflops": round(2.5 * ff / (statistics.fmean(bwd_ms) * 1e-3) / 1e12, 1),
            "pct_of_burst": round(100 * 3.5 * ff / (ms * 1e-3) / 1e12 / peaks["burst"], 2),
            "step_ms_stats": step_stats(step_ms), "kernels": table,
-           "dominant": {"kernel": dom, "frac_of_burst": roof["frac"], "achieved": roof["achieved"]},
+           "dominant": {"kernel": dom, "frac_of_burst": roof["frac"], "achieved": roof["achieved"],
+                        "smem_port": roof.get("smem_port")},
            "clocks": clk}
     del pb
     torch.cuda.empty_cache()
@@ -640,7 +664,7 @@ def main():
     flops_all = sum(gather_floats([flops_rank], world), [])
     total_flops = sum(flops_all)
     value = total_flops / (ms * 1e-3) / 1e12
-    table, roofline, dom = kernel_table(pb, kern_ms, peaks, world)
+    table, roofline, dom = kernel_table(pb, kern_ms, peaks, world, (clk or {}).get("sm_mhz"))
     fwd_all = max(r[1] for r in per_rank)
     bwd_all = max(r[2] for r in per_rank)
 

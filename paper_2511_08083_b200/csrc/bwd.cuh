@@ -290,6 +290,20 @@ __device__ __forceinline__ float2 bwd_exp2_pair(float2 x, int k) {
   return make_float2(ex2(x.x), ex2(x.y));
 }
 
+__device__ __forceinline__ float2 lds_v2(const void* p) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+// HK_DKDV_SHFL: the dK/dV elementwise warps read LSE2 / D of their query columns with one
+// conflict-free ld.shared.v2 per lane and broadcast them by shuffles, instead of 16 broadcast
+// ld.shared.v4 per phase (2 wavefronts each on a shared-memory port the pass saturates)
+#ifndef HK_DKDV_SHFL
+#define HK_DKDV_SHFL 0
+#endif
+__device__ __forceinline__ float shfl_col(float2 v, int c) {
+  return __shfl_sync(0xffffffffu, (c & 1) ? v.y : v.x, c >> 1);
+}
 __device__ __forceinline__ void lds_v4(const void* p, float& a, float& b, float& c, float& d) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(smem_u32(p)));
 }
@@ -793,10 +807,20 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
         tmem_ld_cols<CW>(tmem_addr(cS, lb, 0), v);
         tmem_wait_ld();
         const int q0 = qi * 128 + CW * wg;
+#if HK_DKDV_SHFL
+        const float2 lsp = lds_v2(vec + 4 * (CW * wg) + 8 * (lane % (CW / 2)));
+#endif
 #pragma unroll
         for (int c4 = 0; c4 < CW; c4 += 4) {
           float l0, l1, l2, l3;
+#if HK_DKDV_SHFL
+          l0 = shfl_col(lsp, c4);
+          l1 = shfl_col(lsp, c4 + 1);
+          l2 = shfl_col(lsp, c4 + 2);
+          l3 = shfl_col(lsp, c4 + 3);
+#else
           lds_v4(vec + 4 * (CW * wg + c4), l0, l1, l2, l3);
+#endif
           const float2 xa = fma2(make_float2(v[c4], v[c4 + 1]), make_float2(c, c), make_float2(-l0, -l1));
           const float2 xb = fma2(make_float2(v[c4 + 2], v[c4 + 3]), make_float2(c, c), make_float2(-l2, -l3));
           const float2 ea = bwd_exp2_pair<BWD_EMU_OF_8>(xa, c4 / 2);
@@ -824,10 +848,20 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
         float dp[CW];
         tmem_ld_cols<CW>(tmem_addr(cP, lb, 0), dp);
         tmem_wait_ld();
+#if HK_DKDV_SHFL
+        const float2 dsp = lds_v2(vec + 512 + 4 * (CW * wg) + 8 * (lane % (CW / 2)));
+#endif
 #pragma unroll
         for (int c4 = 0; c4 < CW; c4 += 4) {  // packed f32x2: half the issue slots of scalar FADD + FMUL
           float d0, d1, d2, d3;
+#if HK_DKDV_SHFL
+          d0 = shfl_col(dsp, c4);
+          d1 = shfl_col(dsp, c4 + 1);
+          d2 = shfl_col(dsp, c4 + 2);
+          d3 = shfl_col(dsp, c4 + 3);
+#else
           lds_v4(vec + 512 + 4 * (CW * wg + c4), d0, d1, d2, d3);
+#endif
           const float2 a = mul2(make_float2(v[c4], v[c4 + 1]),
                                 sub2(make_float2(dp[c4], dp[c4 + 1]), make_float2(d0, d1)));
           const float2 b = mul2(make_float2(v[c4 + 2], v[c4 + 3]),
