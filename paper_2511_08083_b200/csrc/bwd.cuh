@@ -31,6 +31,15 @@
 namespace hk {
 
 // ---------------------------------------------------------------- B0
+// 16-B vectors per lane and row: 2 at d = 128 (fewer shuffle levels and index ops per byte:
+// 1.04-1.16x, profiles/ab_pre_vpl_r2af.jsonl), 1 at d = 64 (2 measured 0.88x there)
+#ifndef HK_PRE_VPL128
+#define HK_PRE_VPL128 2
+#endif
+#ifndef HK_PRE_VPL64
+#define HK_PRE_VPL64 1
+#endif
+__host__ __device__ constexpr int pre_vpl(int d) { return d == 128 ? HK_PRE_VPL128 : HK_PRE_VPL64; }
 // Grid (x, b): one group of d/8 lanes per (n, h) row of sequence b (16-B loads),
 // rows in memory order. Workspace rows n in [lq, Np) of each (b, h) are padding:
 // LSE2 = +inf and D = 0, so padded query rows of a last tile give P = 0 and
@@ -44,7 +53,8 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
                                                       int Np, unsigned* __restrict__ sched,
                                                       float* __restrict__ dq_acc) {
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 4) sched[threadIdx.x] = 0u;
-  constexpr int LPR = D / 8;  // lanes per row
+  constexpr int VPL = pre_vpl(D);  // 16-B vectors of O (and of dO) per lane and row
+  constexpr int LPR = D / (8 * VPL);  // lanes per row
   constexpr int RPW = 32 / LPR;
   const int b = blockIdx.y;
   const Seq sq = seq_of(g, b);
@@ -65,7 +75,7 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
   constexpr int U = D == 128 ? HK_PRE_U128 : HK_PRE_U64;  // measured (scripts/ab.py): 2 for both since the 32-bit (h, n) division
   // One warp iteration's rows: their O / dO vectors, LSE and (h, n).
   struct Grp {
-    uint4 a[U], gv[U];
+    uint4 a[U][VPL], gv[U][VPL];
     float L[U];        // LSE of the row (lane sub == 0), loaded with O / dO: not a dependent round trip later
     int hh[U], nn[U];  // (h, n) of each row (rows * H < 2^31, validated)
   };
@@ -83,11 +93,15 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
         q.hh[u] = (int)(r32 - (uint32_t)q.nn[u] * (uint32_t)H);
       }
       if (row < rows) {
-        q.a[u] = __ldcs(reinterpret_cast<const uint4*>(O + (row0 + row) * D) + sub);
-        q.gv[u] = __ldcs(reinterpret_cast<const uint4*>(dO + (row0 + row) * D) + sub);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          q.a[u][v] = __ldcs(reinterpret_cast<const uint4*>(O + (row0 + row) * D) + sub * VPL + v);
+          q.gv[u][v] = __ldcs(reinterpret_cast<const uint4*>(dO + (row0 + row) * D) + sub * VPL + v);
+        }
         if (sub == 0) q.L[u] = __ldg(lse + lse_index(g, sq, b, H, q.hh[u], q.nn[u]));
       } else {
-        q.a[u] = q.gv[u] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) q.a[u][v] = q.gv[u][v] = make_uint4(0u, 0u, 0u, 0u);
       }
     }
   };
@@ -96,13 +110,16 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
     for (int u = 0; u < U; ++u) {
       const size_t row = base + u * RPW + lrow;
       float acc = 0.f;
-      const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&q.a[u]);
-      const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&q.gv[u]);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 x = __bfloat1622float2(ap[k]), y = __bfloat1622float2(gp[k]);
-        acc = fmaf(x.x, y.x, acc);
-        acc = fmaf(x.y, y.y, acc);
+      for (int v = 0; v < VPL; ++v) {
+        const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&q.a[u][v]);
+        const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&q.gv[u][v]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 x = __bfloat1622float2(ap[k]), y = __bfloat1622float2(gp[k]);
+          acc = fmaf(x.x, y.x, acc);
+          acc = fmaf(x.y, y.y, acc);
+        }
       }
 #pragma unroll
       for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -112,9 +129,10 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
           Dout[idx] = acc;
           lse2[idx] = q.L[u] == -INFINITY ? INFINITY : q.L[u] * 1.4426950408889634f;
         }
-        if (dq_acc != nullptr) {  // fused backward: zero this row's fp32 dQ accumulator (8 floats per lane)
-          uint4* z = reinterpret_cast<uint4*>(dq_acc + (row0 + row) * D) + 2 * sub;
-          z[0] = z[1] = make_uint4(0u, 0u, 0u, 0u);
+        if (dq_acc != nullptr) {  // fused backward: zero this row's fp32 dQ accumulator (8 VPL floats per lane)
+          uint4* z = reinterpret_cast<uint4*>(dq_acc + (row0 + row) * D) + 2 * VPL * sub;
+#pragma unroll
+          for (int v = 0; v < 2 * VPL; ++v) z[v] = make_uint4(0u, 0u, 0u, 0u);
         }
       }
     }
@@ -1426,7 +1444,8 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
               sh.acc32};
   // B0: grid (x, b), x sized for the longest sequence and capped at ~16 blocks per SM overall
   const size_t rows = (size_t)sh.Nq * Hq;
-  const size_t warps_needed = (rows + (32 / (D / 8)) - 1) / (32 / (D / 8));
+  constexpr int RPW0 = 32 / (D / (8 * pre_vpl(D)));  // rows per warp pass of the preprocess
+  const size_t warps_needed = (rows + RPW0 - 1) / RPW0;
   size_t bx = (warps_needed + 7) / 8;
   size_t cap = (size_t)num_sms * 16 / (size_t)B;
   if (cap < 1) cap = 1;
