@@ -319,6 +319,14 @@ __device__ __forceinline__ float2 lds_v2(const void* p) {
 #ifndef HK_DKDV_SHFL
 #define HK_DKDV_SHFL 0
 #endif
+// HK_DKDV_LDG: the same per-query vectors read with ld.global.nc.v4 (all lanes one address, an
+// L1 hit after the first warp) from the workspace, off the shared-memory port
+#ifndef HK_DKDV_LDG
+#define HK_DKDV_LDG 0
+#endif
+__device__ __forceinline__ void ldg_nc_v4(const float* p, float& a, float& b, float& c, float& d) {
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "l"(p));
+}
 __device__ __forceinline__ float shfl_col(float2 v, int c) {
   return __shfl_sync(0xffffffffu, (c & 1) ? v.y : v.x, c >> 1);
 }
@@ -812,8 +820,11 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
       }
       const int off = w.sq.lk - w.sq.lq;  // bottom-right causal alignment
       int qi = w.i0;
+      int hq = w.kvh * G;  // query head of block u (HK_DKDV_LDG)
       for (int it = 0; it < w.n_it; ++it, ++u) {
         const uint8_t* vec = sB + s * C::SLOT_B1 + C::T128;  // lse2 [128], then D [128]
+        const size_t goff = ((size_t)w.b * p.Hq + hq) * p.Np + (size_t)qi * 128 + CW * wg;  // HK_DKDV_LDG
+        (void)goff;
         const uint32_t par = u & 1;
         float v[CW];
         // ---- phase 1: P^T = exp2(c S^T - LSE2) (masked), bf16 into TMEM for dV += P^T dO
@@ -836,6 +847,8 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
           l1 = shfl_col(lsp, c4 + 1);
           l2 = shfl_col(lsp, c4 + 2);
           l3 = shfl_col(lsp, c4 + 3);
+#elif HK_DKDV_LDG
+          ldg_nc_v4(p.lse2 + goff + c4, l0, l1, l2, l3);
 #else
           lds_v4(vec + 4 * (CW * wg + c4), l0, l1, l2, l3);
 #endif
@@ -877,6 +890,8 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
           d1 = shfl_col(dsp, c4 + 1);
           d2 = shfl_col(dsp, c4 + 2);
           d3 = shfl_col(dsp, c4 + 3);
+#elif HK_DKDV_LDG
+          ldg_nc_v4(p.Dv + goff + c4, d0, d1, d2, d3);
 #else
           lds_v4(vec + 512 + 4 * (CW * wg + c4), d0, d1, d2, d3);
 #endif
@@ -920,7 +935,10 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_ds);
         if (threadIdx.x == 0) hk_trace(5, u, 0);
-        if (++qi == w.nqt) qi = w.i0;
+        if (++qi == w.nqt) {
+          qi = w.i0;
+          ++hq;
+        }
         if (++s == NSB) s = 0;
       }
       // ---- epilogue: WG0 writes dV, WG1 writes dK * (1/sqrt d)
