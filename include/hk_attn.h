@@ -154,6 +154,18 @@ hk_status hk_attn_bwd_varlen_ex(const void* Q, const void* K, const void* V, con
                                 int Hq, int Hkv, int total_q, int total_k, int max_seqlen_q, int max_seqlen_k,
                                 int d, int causal, unsigned flags, cudaStream_t stream);
 
+/* ---- SM budget for the persistent kernels (ABI 5).
+ * Every kernel of this library that runs one CTA per SM (forward, backward passes, GEMM) and the
+ * grid-stride helpers launch on at most max_ctas SMs' worth of CTAs (max_ctas <= 0: all SMs, the
+ * default). Purpose: leave SMs to a concurrent kernel on another stream — the copy kernels NCCL
+ * runs for a context-parallel ring step's K/V and dK/dV transfers (ring.py) — so
+ * that communication overlaps the attention kernels instead of queueing behind CTAs that hold
+ * every SM. A process-wide setting (atomic; read at each launch, so it applies to later calls on
+ * any thread); results do not depend on it (work order is fixed per output tile, reading #19).
+ * hk_get_max_ctas returns the current value (0 = all SMs). */
+void hk_set_max_ctas(int max_ctas);
+int hk_get_max_ctas(void);
+
 const char* hk_attn_last_error(void);
 const char* hk_status_string(hk_status s);
 int hk_attn_abi_version(void);

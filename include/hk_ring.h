@@ -37,6 +37,11 @@ hk_status hk_attn_merge(float* O_acc, float* LSE_acc, const void* O_part, const 
  * x may be NULL (treated as 0) when out != NULL and init == 0: out = bf16(acc). */
 hk_status hk_accum_bf16(float* acc, const void* x, void* out, size_t n, int init, cudaStream_t stream);
 
+/* acc += x over n fp32 elements (n % 4 == 0, 16-B aligned, no overlap; ABI 5): the ring backward
+ * adds the dK/dV accumulator received from the previous rank to this rank's own contributions for
+ * the same key chunk, which were formed while that accumulator was in flight. */
+hk_status hk_accum_f32(float* acc, const float* x, size_t n, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

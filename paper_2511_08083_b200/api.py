@@ -198,6 +198,44 @@ def attn_bwd_varlen(q, k, v, o, lse, do, cu_seqlens_q, cu_seqlens_k, max_seqlen_
     return dq, dk, dv
 
 
+def set_max_ctas(n: int) -> None:
+    """SM budget of the persistent kernels (hk_set_max_ctas): at most n CTAs per launch, n <= 0 =
+    all SMs. Process-wide; results do not depend on it."""
+    lib().hk_set_max_ctas(int(n))
+
+
+def get_max_ctas() -> int:
+    return int(lib().hk_get_max_ctas())
+
+
+class sm_budget:
+    """Context manager: persistent kernels leave `reserve` SMs free (for NCCL's copy kernels on
+    another stream) inside the block; the previous budget is restored on exit."""
+
+    def __init__(self, reserve: int):
+        self.reserve = int(reserve)
+
+    def __enter__(self):
+        self.prev = get_max_ctas()
+        if self.reserve > 0:
+            sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            set_max_ctas(max(sms - self.reserve, 2))
+        return self
+
+    def __exit__(self, *exc):
+        set_max_ctas(self.prev)
+        return False
+
+
+def accum_f32(acc, x):
+    """acc += x for fp32 CUDA tensors of equal shape (hk_accum_f32, include/hk_ring.h)."""
+    for name, t in (("acc", acc), ("x", x)):
+        _check_tensor(name, t, torch.float32)
+    _expect_shape("x", x, tuple(acc.shape))
+    check(lib().hk_accum_f32(_ptr(acc), _ptr(x), ctypes.c_size_t(acc.numel()), _stream()))
+    return acc
+
+
 def gemm(a, b, out=None):
     """C = a @ b.T (bf16 in, fp32 accumulate, bf16 out) on the tcgen05 CTA-pair
     GEMM (include/hk_gemm.h). a [M, K], b [N, K] bf16 CUDA, contiguous;

@@ -68,7 +68,10 @@ const char* hk_status_string(hk_status s) {
   return "HK_ERR_UNKNOWN";
 }
 
-int hk_attn_abi_version(void) { return 4; }  // 2: + Nq != Nk and varlen; 4: + _ex (flags), fused d=64 bwd, rope
+int hk_attn_abi_version(void) { return 5; }  // 2: + Nq != Nk and varlen; 4: + _ex (flags), fused d=64 bwd, rope;
+                                              // 5: + hk_set_max_ctas / hk_get_max_ctas, hk_accum_f32
+void hk_set_max_ctas(int max_ctas) { g_max_ctas.store(max_ctas > 0 ? max_ctas : 0); }
+int hk_get_max_ctas(void) { return g_max_ctas.load(); }
 
 hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, float* LSE, int B, int Hq, int Hkv,
                       int N, int d, int causal, cudaStream_t stream) {
@@ -332,5 +335,19 @@ hk_status hk_accum_bf16(float* acc, const void* x, void* out, size_t n, int init
   hk::accum_bf16_kernel<<<(unsigned)blocks, 256, 0, stream>>>(acc, reinterpret_cast<const __nv_bfloat16*>(x),
                                                                reinterpret_cast<__nv_bfloat16*>(out), n8, init != 0);
   return launched("hk_accum_bf16");
+}
+hk_status hk_accum_f32(float* acc, const float* x, size_t n, cudaStream_t stream) {
+  g_err[0] = 0;
+  if (n == 0 || n % 4) return fail(HK_ERR_INVALID_ARGUMENT, "n must be a positive multiple of 4");
+  if (!acc || !x) return fail(HK_ERR_INVALID_ARGUMENT, "null pointer argument");
+  if (!aligned16(acc) || !aligned16(x)) return fail(HK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  if (overlaps(acc, n * 4, x, n * 4)) return fail(HK_ERR_INVALID_ARGUMENT, "buffers must not overlap");
+  int num_sms = 0;
+  hk_status s = check_device(&num_sms);
+  if (s != HK_OK) return s;
+  size_t blocks = (n / 4 + 255) / 256;
+  if (blocks > (size_t)num_sms * 16) blocks = (size_t)num_sms * 16;
+  hk::accum_f32_kernel<<<(unsigned)blocks, 256, 0, stream>>>(acc, x, n / 4);
+  return launched("hk_accum_f32");
 }
 }  // extern "C"

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -41,6 +42,9 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   return x < y + nb && y < x + na;
 }
 
+// hk_set_max_ctas: SM budget of the persistent kernels (0 = all SMs)
+std::atomic<int> g_max_ctas{0};
+
 hk_status check_device(int* num_sms) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(HK_ERR_DEVICE, "cudaGetDevice failed");
@@ -53,7 +57,11 @@ hk_status check_device(int* num_sms) {
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
   if (major != 10 || minor != 0)
     return fail(HK_ERR_DEVICE, "device %d is sm_%d%d; libhkattn is built for sm_100a only", dev, major, minor);
-  if (num_sms) cudaDeviceGetAttribute(num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (num_sms) {
+    cudaDeviceGetAttribute(num_sms, cudaDevAttrMultiProcessorCount, dev);
+    const int cap = g_max_ctas.load();
+    if (cap > 0 && cap < *num_sms) *num_sms = cap < 2 ? 2 : cap;  // the GEMM needs one CTA pair
+  }
   return HK_OK;
 }
 

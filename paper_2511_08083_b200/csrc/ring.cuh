@@ -87,6 +87,20 @@ __global__ void __launch_bounds__(256) attn_merge_kernel(const MergeParams p) {
   }
 }
 
+// acc += x, fp32, 4 per thread-iteration (16-B loads).
+__global__ void __launch_bounds__(256) accum_f32_kernel(float* __restrict__ acc, const float* __restrict__ x,
+                                                        size_t n4) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    float4 a = reinterpret_cast<const float4*>(acc)[i];
+    const float4 b = reinterpret_cast<const float4*>(x)[i];
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+    reinterpret_cast<float4*>(acc)[i] = a;
+  }
+}
+
 // acc / out over n elements, 8 per thread-iteration (16-B bf16 loads).
 __global__ void __launch_bounds__(256) accum_bf16_kernel(float* __restrict__ acc, const __nv_bfloat16* __restrict__ x,
                                                          __nv_bfloat16* __restrict__ out, size_t n8, int init) {

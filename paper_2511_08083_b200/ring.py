@@ -191,11 +191,27 @@ class _Fanout:
 
 
 # ---------------------------------------------------------------- forward / backward
-def ring_attn_fwd(q, k, v, causal: bool, comm: RingComm, streams: int = 1):
+# SMs the persistent kernels leave free during a ring step when the exchange runs NCCL copy kernels
+# on the same GPU (api.sm_budget): with every SM held by a one-CTA-per-SM kernel the transfer of the
+# next step's K/V (and the dK/dV accumulators) cannot start until the step's kernels drain
+RESERVE_SMS_NCCL = 8
+
+
+def _reserve(comm: RingComm) -> int:
+    return RESERVE_SMS_NCCL if isinstance(comm, DistRing) and not comm.staged else 0
+
+
+def ring_attn_fwd(q, k, v, causal: bool, comm: RingComm, streams: int = 1, reserve_sms: int | None = None):
     """q, k, v: per local rank, (A, B) chunk pairs of [B, c, H, d] bf16 CUDA tensors
     (zigzag_shard). Returns per local rank ((oA, oB), (lseA, lseB)): O bf16
     [B, c, Hq, d], LSE fp32 [B, Hq, c] of the attention over the whole sequence.
-    streams > 1: a step's attention calls run concurrently on that many side streams."""
+    streams > 1: a step's attention calls run concurrently on that many side streams.
+    reserve_sms: SMs the persistent kernels leave free for the K/V transfer (default: _reserve)."""
+    with api.sm_budget(_reserve(comm) if reserve_sms is None else reserve_sms):
+        return _ring_attn_fwd(q, k, v, causal, comm, streams)
+
+
+def _ring_attn_fwd(q, k, v, causal, comm, streams):
     P = comm.world
     fan = _Fanout(streams)
     plans = [plan(P, r, causal) for r in comm.ranks]
@@ -234,10 +250,12 @@ def ring_attn_fwd(q, k, v, causal: bool, comm: RingComm, streams: int = 1):
     return [((st["o"][0], st["o"][1]), (st["lse"][0], st["lse"][1])) for st in out]
 
 
-def ring_attn_bwd(q, k, v, o, lse, do, causal: bool, comm: RingComm, streams: int = 1):
+def ring_attn_bwd(q, k, v, o, lse, do, causal: bool, comm: RingComm, streams: int = 1,
+                  reserve_sms: int | None = None):
     """Backward of ring_attn_fwd. All arguments per local rank as (A, B) chunk pairs
     (o, lse from ring_attn_fwd). Returns per local rank ((dqA, dqB), (dkA, dkB), (dvA, dvB)).
-    streams > 1: a step's backward calls run concurrently on that many side streams."""
+    streams > 1: a step's backward calls run concurrently on that many side streams.
+    reserve_sms: SMs the persistent kernels leave free for the transfers (default: _reserve)."""
     P = comm.world
     fan = _Fanout(streams)
     plans = [plan(P, r, causal) for r in comm.ranks]
@@ -247,66 +265,72 @@ def ring_attn_bwd(q, k, v, o, lse, do, causal: bool, comm: RingComm, streams: in
     dq = [[torch.empty_like(q[li][h]) for h in (0, 1)] for li in range(n_local)]
     dq_seen = [[0, 0] for _ in range(n_local)]
     dq_last = [{qh: max(i for i, p in enumerate(plans[li]) if p[1] == qh) for qh in (0, 1)} for li in range(n_local)]
-    # travelling state: K, V chunks and fp32 dK, dV accumulators (zero-initialised: a chunk's first
-    # contribution may come at any step on any rank)
-    trav = [[k[li][0], k[li][1], v[li][0], v[li][1]] +
-            [torch.zeros(k[li][h].shape, dtype=torch.float32, device=k[li][h].device) for h in (0, 1)] +
-            [torch.zeros(v[li][h].shape, dtype=torch.float32, device=v[li][h].device) for h in (0, 1)]
-            for li in range(n_local)]
-    for s in range(P):
-        # K, V of the next step travel while this step computes; the dK, dV
-        # accumulators follow once this step's contributions are in (after the last
-        # step that rotation brings every chunk's dK, dV back to its owner)
-        h_kv = comm.start([t[:4] for t in trav]) if s + 1 < P else None
-        fan.begin()
-        parts = []
-        for li in range(n_local):
-            t = trav[li]
-            for i, (ps, qh, kh, mode) in enumerate(plans[li]):
-                if ps != s:
-                    continue
-                args = (q[li][qh], t[kh], t[2 + kh], o[li][qh], lse[li][qh], do[li][qh])
-                ws = torch.empty(api.bwd_workspace_bytes(args[0].shape[0], args[0].shape[2], args[1].shape[2],
-                                                         args[0].shape[1], args[0].shape[3]) // 4,
-                                 dtype=torch.float32, device=args[0].device)
-                if streams == 1:
-                    # one stream: the call adds its share straight into the fp32 accumulators
-                    # (HK_BWD_ACCUMULATE_F32) — no bf16 rounding of the per-step partials
-                    if dq_seen[li][qh] == 0:
-                        dq_acc[li][qh].zero_()
-                    dq_seen[li][qh] += 1
-                    api.attn_bwd(*args, mode == "causal", workspace=ws, dq=dq_acc[li][qh], dk=t[4 + kh],
-                                 dv=t[6 + kh], deterministic=True, accumulate=True)
-                    if i == dq_last[li][qh]:
-                        _accum(dq_acc[li][qh], None, dq[li][qh])
-                    continue
-                g = [torch.empty_like(args[0]), torch.empty_like(args[1]), torch.empty_like(args[2])]
-                e = fan.run(lambda args=args, g=g, ws=ws, m=mode:
-                            api.attn_bwd(*args, m == "causal", workspace=ws, dq=g[0], dk=g[1], dv=g[2],
-                                         deterministic=True))
-                # the workspace (and the partials) stay referenced until the join: freed earlier, the
-                # caching allocator would hand the block to the next call while this one still runs
-                parts.append((li, i, qh, kh, g, e, ws))
-        # streams > 1: calls sharing an accumulator would race, so each writes bf16 partials that are
-        # summed here in fp32 (hk_accum_bf16)
-        for li, i, qh, kh, (dq_p, dk_p, dv_p), e, _ws in parts:
-            t = trav[li]
-            fan.join(e)
-            last = i == dq_last[li][qh]
-            _accum(dq_acc[li][qh], dq_p, dq[li][qh] if last else None, dq_seen[li][qh] == 0)
-            dq_seen[li][qh] += 1
-            _accum(t[4 + kh], dk_p)
-            _accum(t[6 + kh], dv_p)
-        acc = comm.finish(comm.start([t[4:] for t in trav]))
-        kv = comm.finish(h_kv) if h_kv is not None else [[None] * 4 for _ in range(n_local)]
-        trav = [kv[li] + acc[li] for li in range(n_local)]
+    # K, V travel one step ahead of the compute; the fp32 dK, dV accumulators travel one step
+    # behind it: at step s each rank forms its contributions to the chunks it now holds in fresh
+    # zeroed buffers while the accumulators of the same chunks (sent by the previous rank at the end
+    # of step s - 1) are in flight, then adds the arrivals in (hk_accum_f32) and sends the sums on.
+    # After the last step that send brings every chunk's dK, dV home (src = r + 1 at step P - 1).
+    kv = [[k[li][0], k[li][1], v[li][0], v[li][1]] for li in range(n_local)]
+    h_acc = None
+    with api.sm_budget(_reserve(comm) if reserve_sms is None else reserve_sms):
+        for s in range(P):
+            h_kv = comm.start(kv) if s + 1 < P else None
+            own = [[torch.zeros(kv[li][i].shape, dtype=torch.float32, device=kv[li][i].device) for i in range(4)]
+                   for li in range(n_local)]
+            fan.begin()
+            parts = []
+            for li in range(n_local):
+                t = kv[li]
+                for i, (ps, qh, kh, mode) in enumerate(plans[li]):
+                    if ps != s:
+                        continue
+                    args = (q[li][qh], t[kh], t[2 + kh], o[li][qh], lse[li][qh], do[li][qh])
+                    ws = torch.empty(api.bwd_workspace_bytes(args[0].shape[0], args[0].shape[2], args[1].shape[2],
+                                                             args[0].shape[1], args[0].shape[3]) // 4,
+                                     dtype=torch.float32, device=args[0].device)
+                    if streams == 1:
+                        # one stream: the call adds its share straight into the fp32 accumulators
+                        # (HK_BWD_ACCUMULATE_F32) — no bf16 rounding of the per-step partials
+                        if dq_seen[li][qh] == 0:
+                            dq_acc[li][qh].zero_()
+                        dq_seen[li][qh] += 1
+                        api.attn_bwd(*args, mode == "causal", workspace=ws, dq=dq_acc[li][qh], dk=own[li][kh],
+                                     dv=own[li][2 + kh], deterministic=True, accumulate=True)
+                        if i == dq_last[li][qh]:
+                            _accum(dq_acc[li][qh], None, dq[li][qh])
+                        continue
+                    g = [torch.empty_like(args[0]), torch.empty_like(args[1]), torch.empty_like(args[2])]
+                    e = fan.run(lambda args=args, g=g, ws=ws, m=mode:
+                                api.attn_bwd(*args, m == "causal", workspace=ws, dq=g[0], dk=g[1], dv=g[2],
+                                             deterministic=True))
+                    # the workspace (and the partials) stay referenced until the join: freed earlier, the
+                    # caching allocator would hand the block to the next call while this one still runs
+                    parts.append((li, i, qh, kh, g, e, ws))
+            # streams > 1: calls sharing an accumulator would race, so each writes bf16 partials that are
+            # summed here in fp32 (hk_accum_bf16)
+            for li, i, qh, kh, (dq_p, dk_p, dv_p), e, _ws in parts:
+                fan.join(e)
+                last = i == dq_last[li][qh]
+                _accum(dq_acc[li][qh], dq_p, dq[li][qh] if last else None, dq_seen[li][qh] == 0)
+                dq_seen[li][qh] += 1
+                _accum(own[li][kh], dk_p)
+                _accum(own[li][2 + kh], dv_p)
+            if h_acc is not None:  # the previous ranks' sums for the chunks this rank holds now
+                inc = comm.finish(h_acc)
+                for li in range(n_local):
+                    for i in range(4):
+                        api.accum_f32(own[li][i], inc[li][i])
+            h_acc = comm.start(own)
+            if h_kv is not None:
+                kv = comm.finish(h_kv)
+        home = comm.finish(h_acc)
     res = []
     for li in range(n_local):
-        t = trav[li]
+        t = home[li]
         dk = [torch.empty_like(k[li][h]) for h in (0, 1)]
         dv = [torch.empty_like(v[li][h]) for h in (0, 1)]
         for h in (0, 1):
-            _accum(t[4 + h], None, dk[h])
-            _accum(t[6 + h], None, dv[h])
+            _accum(t[h], None, dk[h])
+            _accum(t[2 + h], None, dv[h])
         res.append(((dq[li][0], dq[li][1]), (dk[0], dk[1]), (dv[0], dv[1])))
     return res

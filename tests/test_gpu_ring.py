@@ -66,6 +66,41 @@ def test_accum_kernel():
     assert torch.equal(out, acc.to(torch.bfloat16))
 
 
+def test_accum_f32_kernel():
+    from paper_2511_08083_b200 import api
+    g = torch.Generator(device="cuda").manual_seed(1)
+    a = torch.randn(3, 1000, generator=g, device="cuda")
+    b = torch.randn(3, 1000, generator=g, device="cuda")
+    want = a + b
+    api.accum_f32(a, b)
+    torch.cuda.synchronize()
+    assert torch.equal(a, want)  # one fp32 addition per element: the same rounding
+    with pytest.raises(ValueError):
+        api.accum_f32(a, b[:, :8])
+
+
+def test_sm_budget_results_unchanged():
+    """hk_set_max_ctas: the persistent kernels on 16 or 37 SMs (several items per CTA, another
+    snake / counter order) give bitwise the results of the full-SM launch (reading #19)."""
+    from paper_2511_08083_b200 import api
+    from paper_2511_08083_b200.inputs import make_inputs
+    for d, causal in ((128, True), (64, False)):
+        x = make_inputs(2, 1000, 8, 2, d, seed=3, device="cuda")
+        runs = []
+        for reserve in (0, 148 - 37, 148 - 16):
+            with api.sm_budget(reserve):
+                assert api.get_max_ctas() == (0 if reserve == 0 else max(torch.cuda.get_device_properties(0)
+                                                                         .multi_processor_count - reserve, 2))
+                o, lse = api.attn_fwd(x["Q"], x["K"], x["V"], causal)
+                g = api.attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, deterministic=True)
+                c = api.gemm(x["Q"].reshape(-1, d)[:512].contiguous(), x["K"].reshape(-1, d)[:256].contiguous())
+            assert api.get_max_ctas() == 0
+            torch.cuda.synchronize()
+            runs.append((o, lse) + tuple(g) + (c,))
+        for other in runs[1:]:
+            assert all(torch.equal(a, b) for a, b in zip(runs[0], other))
+
+
 CASES = [
     # P, B, N, Hq, Hkv, d
     (2, 1, 1024, 4, 2, 128),
@@ -94,7 +129,13 @@ def test_ring_loopback_matches_whole_sequence(case, causal):
     # race), so it agrees with the one-stream fp32-accumulating backward to bf16 rounding
     fw3 = ring.ring_attn_fwd(sh["Q"], sh["K"], sh["V"], causal, comm, streams=3)
     bw3 = ring.ring_attn_bwd(sh["Q"], sh["K"], sh["V"], o, lse, sh["dO"], causal, comm, streams=3)
+    # SMs left free for the transfers (the NCCL setting): bitwise the same results
+    fwr = ring.ring_attn_fwd(sh["Q"], sh["K"], sh["V"], causal, comm, reserve_sms=20)
+    bwr = ring.ring_attn_bwd(sh["Q"], sh["K"], sh["V"], o, lse, sh["dO"], causal, comm, reserve_sms=20)
     torch.cuda.synchronize()
+    for r in range(P):
+        assert all(torch.equal(a, b) for a, b in zip(fw[r][0] + fw[r][1], fwr[r][0] + fwr[r][1]))
+        assert all(torch.equal(a, b) for g1, g2 in zip(bw[r], bwr[r]) for a, b in zip(g1, g2))
     for r in range(P):
         assert all(torch.equal(a, b) for a, b in zip(fw[r][0] + fw[r][1], fw3[r][0] + fw3[r][1]))
         for g1, g3 in zip(bw[r], bw3[r]):
