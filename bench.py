@@ -449,26 +449,6 @@ def time_breakdown(pb, steps, warmup, world):
     return {n: statistics.fmean(t) for n, t in per.items()}
 
 
-def smem_port_model(pb, dom, ms, sm_mhz):
-    """Second roofline of the d = 128 dK/dV pass (DESIGN.md §6 "SMEM bandwidth"): shared-memory port
-    cycles per 128x128 block = (tensor-core SS operand reads 192 KB + TMA writes of Q_i, dO_i 64 KB
-    + the LSE2/D broadcast ld.shared.v4, 8 warps x 32 x 2 wavefronts x 128 B = 64 KB-equivalent)
-    / 128 B/clk/SM, against the kernel's measured time at the sampled SM clock. A model: the port
-    width and the wavefront costs are the ones DESIGN.md §6 measured, not an ncu counter."""
-    if dom != "bwd_dkdv" or pb.d != 128 or not sm_mhz:
-        return None
-    nt = (pb.N + 127) // 128
-    blocks_per_head = nt * (nt + 1) // 2 if pb.causal else nt * nt
-    blocks = pb.B * pb.Hq * blocks_per_head
-    kb_per_block = 192 + 64 + 64
-    bytes_ = blocks * kb_per_block * 1024
-    achieved = bytes_ / (ms * 1e-3) / 1e12
-    peak = 128 * 148 * sm_mhz * 1e6 / 1e12
-    return {"bound": "smem_port", "unit": "TB/s", "achieved": round(achieved, 2), "peak": round(peak, 2),
-            "frac": round(achieved / peak, 4), "model_kb_per_block": kb_per_block, "blocks_per_launch": blocks,
-            "peak_basis": f"128 B/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (sampled median under load)"}
-
-
 def kernel_table(pb, kern_ms, peaks, world, sm_mhz=None):
     """Per-kernel algorithmic / executed rates and the roofline of the dominant kernel."""
     ff = pb.fwd_flops
@@ -510,9 +490,6 @@ def kernel_table(pb, kern_ms, peaks, world, sm_mhz=None):
             "frac_of_spec_2250": round(ach / SPEC_PEAK_TFLOPS, 4),
             "algorithmic_flops_per_launch": alg[dom], "executed_flops_per_launch": execd[dom],
             "timing": "mean launch duration from CUDA events between kernels (timed region 2)"}
-    sp = smem_port_model(pb, dom, kern_ms[dom], sm_mhz)
-    if sp is not None:
-        roof["smem_port"] = sp
     return table, roof, dom
 
 
@@ -543,8 +520,7 @@ def sub_record(name, args, peaks):
            "bwd_tflops": round(2.5 * ff / (statistics.fmean(bwd_ms) * 1e-3) / 1e12, 1),
            "pct_of_burst": round(100 * 3.5 * ff / (ms * 1e-3) / 1e12 / peaks["burst"], 2),
            "step_ms_stats": step_stats(step_ms), "kernels": table,
-           "dominant": {"kernel": dom, "frac_of_burst": roof["frac"], "achieved": roof["achieved"],
-                        "smem_port": roof.get("smem_port")},
+           "dominant": {"kernel": dom, "frac_of_burst": roof["frac"], "achieved": roof["achieved"]},
            "clocks": clk}
     del pb
     torch.cuda.empty_cache()

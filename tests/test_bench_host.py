@@ -34,18 +34,3 @@ def test_kernel_table_labels_dq_executed_vs_algorithmic():
     assert abs(roof["achieved"] - 1000.0) < 1e-6 and abs(roof["frac"] - 0.625) < 1e-9
     assert table["bwd_dq"]["tflops_executed"] == 1000.0 and abs(table["bwd_dq"]["tflops_algorithmic"] - 333.3) < 0.1
     assert table["fwd"]["tflops_executed"] == table["fwd"]["tflops_algorithmic"] == 1000.0
-
-
-def test_smem_port_model_counts_blocks_and_bytes():
-    # causal C3-like: 64 key tiles -> 64*65/2 = 2080 blocks per head; 320 KB per block
-    pb = types.SimpleNamespace(B=16, N=8192, Hq=32, d=128, causal=True)
-    sp = bench.smem_port_model(pb, "bwd_dkdv", 10.0, 1500.0)
-    assert sp["blocks_per_launch"] == 16 * 32 * 2080
-    bytes_ = 16 * 32 * 2080 * 320 * 1024
-    assert abs(sp["achieved"] - round(bytes_ / 1e-2 / 1e12, 2)) < 1e-9
-    assert abs(sp["peak"] - 128 * 148 * 1.5e9 / 1e12) < 1e-2
-    # only the d = 128 dK/dV pass has the model; no clock, no model
-    assert bench.smem_port_model(pb, "fwd", 10.0, 1500.0) is None
-    assert bench.smem_port_model(pb, "bwd_dkdv", 10.0, None) is None
-    nc = types.SimpleNamespace(B=1, N=256, Hq=1, d=128, causal=False)
-    assert bench.smem_port_model(nc, "bwd_dkdv", 1.0, 1000.0)["blocks_per_launch"] == 4
