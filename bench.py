@@ -318,7 +318,7 @@ class Problem:
     def __init__(self, name, rank, world, scaling, seed):
         import torch
 
-        from paper_2511_08083_b200 import bwd_workspace_bytes
+        from paper_2511_08083_b200.api import bwd_workspace_bytes, default_bwd_workspace_bytes
         from paper_2511_08083_b200.inputs import make_inputs
         from paper_2511_08083_b200.shard import strong_shard, weak_shard
         self.name = name
@@ -342,8 +342,12 @@ class Problem:
         self.o = torch.empty_like(self.q)
         self.lse = torch.empty((self.B, self.Hq, N), dtype=torch.float32, device="cuda")
         self.dq, self.dk, self.dv = torch.empty_like(self.q), torch.empty_like(self.k), torch.empty_like(self.v)
-        self.ws = torch.empty(bwd_workspace_bytes(self.B, self.Hq, self.Hkv, N, d) // 4, dtype=torch.float32,
-                              device="cuda")
+        # the workspace the public attn_bwd allocates itself: the stored-dS backward where it applies and
+        # fits the budget (d = 128 dense), else the plain one
+        nb = default_bwd_workspace_bytes(self.B, self.Hq, self.Hkv, N, d, None, causal)
+        self.ds = nb > bwd_workspace_bytes(self.B, self.Hq, self.Hkv, N, d)
+        self.ds_bytes = nb - bwd_workspace_bytes(self.B, self.Hq, self.Hkv, N, d) if self.ds else 0
+        self.ws = torch.empty((nb + 3) // 4, dtype=torch.float32, device="cuda")
         self.fwd_flops = fwd_flops(self.B, N, self.Hq, d, causal)  # this rank's share
         in_bytes = sum(t.numel() * t.element_size() for t in (self.q, self.k, self.v, self.do))
         self.l2_note = "inputs larger than L2 (126 MB)" if in_bytes > 126e6 else "L2 flushed between steps"
@@ -444,7 +448,8 @@ def time_breakdown(pb, steps, warmup, world):
     barrier(world)
     # d = 64: hk_attn_bwd's default is the fused single pass (NEXT #1): phase 1 = dK/dV + dQ partials
     # (bulk reduce-add), phase 2 = the dQ convert pass
-    names = ("fwd", "bwd_pre", "bwd_dkdv_dq", "dq_convert") if pb.d == 64 else ("fwd", "bwd_pre", "bwd_dkdv", "bwd_dq")
+    names = ("fwd", "bwd_pre", "bwd_dkdv_dq", "dq_convert") if pb.d == 64 else \
+        ("fwd", "bwd_pre", "bwd_dkdv_ds", "bwd_dq_ds") if pb.ds else ("fwd", "bwd_pre", "bwd_dkdv", "bwd_dq")
     per = {n: [e[i].elapsed_time(e[i + 1]) for e in ev] for i, n in enumerate(names)}
     return {n: statistics.fmean(t) for n, t in per.items()}
 
@@ -456,9 +461,11 @@ def kernel_table(pb, kern_ms, peaks, world, sm_mhz=None):
     # FLOPs per launch: executed = the tensor-core work the kernel issues; algorithmic = the share
     # of the method's 5 backward GEMMs (reading #14) it contributes.
     execd = {"fwd": ff, "bwd_dkdv": 2.0 * ff, "bwd_dq": 1.5 * ff,     # dkdv: S^T dP^T dV dK; dq: S dP dQ
-             "bwd_dkdv_dq": 2.5 * ff}                                  # fused (d = 64): all 5 GEMMs once
+             "bwd_dkdv_dq": 2.5 * ff,                                  # fused (d = 64): all 5 GEMMs once
+             "bwd_dkdv_ds": 2.0 * ff, "bwd_dq_ds": 0.5 * ff}          # stored dS: dQ = dS K only
     alg = {"fwd": ff, "bwd_dkdv": 2.0 * ff, "bwd_dq": 0.5 * ff,       # dq: only dQ = dS K is not a recompute
-           "bwd_dkdv_dq": 2.5 * ff}
+           "bwd_dkdv_dq": 2.5 * ff, "bwd_dkdv_ds": 2.0 * ff, "bwd_dq_ds": 0.5 * ff}
+    ds_bytes = getattr(pb, "ds_bytes", 0)  # stored dS: written by bwd_dkdv_ds, read by bwd_dq_ds
     pre_bytes = B * Hq * N * (4 * d + 4 + 4 + 4)  # read O, dO (bf16), LSE; write D, LSE2
     if d == 64:
         pre_bytes += B * Hq * N * d * 4          # + zero the fp32 dQ accumulator (fused backward)
@@ -475,6 +482,11 @@ def kernel_table(pb, kern_ms, peaks, world, sm_mhz=None):
             rec.update(tflops_executed=round(execd[n] / (ms * 1e-3) / 1e12, 1),
                        tflops_algorithmic=round(alg[n] / (ms * 1e-3) / 1e12, 1),
                        frac_of_burst_executed=round(execd[n] / (ms * 1e-3) / 1e12 / peaks["burst"], 4))
+            if n in ("bwd_dkdv_ds", "bwd_dq_ds") and ds_bytes:
+                # the dS round trip through HBM: written by the dK/dV pass, read (+ dQ written) by the dQ pass
+                nb = ds_bytes + (B * Hq * N * d * 2 if n == "bwd_dq_ds" else 0)
+                gbs = nb / (ms * 1e-3) / 1e9
+                rec.update(hbm_gbs=round(gbs, 1), frac_of_hbm=round(gbs / peaks["hbm_gbs"], 4), hbm_bytes=nb)
         table[n] = rec
     dom = max((n for n in kern_ms if n not in ("bwd_pre", "dq_convert")), key=lambda n: kern_ms[n])
     ach = alg[dom] / (kern_ms[dom] * 1e-3) / 1e12
@@ -700,7 +712,8 @@ def run_e2e(args, pb, world):
     dO and D2H of O, LSE, dQ, dK, dV, pipelined on three streams over batch chunks."""
     import torch
 
-    from paper_2511_08083_b200 import attn_bwd, attn_fwd, bwd_workspace_bytes
+    from paper_2511_08083_b200 import attn_bwd, attn_fwd
+    from paper_2511_08083_b200.api import default_bwd_workspace_bytes
     B, N, Hq, Hkv, d, causal = pb.B, pb.N, pb.Hq, pb.Hkv, pb.d, pb.causal
     x = pb.x
     chunk = 2 if B % 2 == 0 else 1
@@ -716,7 +729,8 @@ def run_e2e(args, pb, world):
              "dK": torch.empty(dk.shape, dtype=dk.dtype, pin_memory=True),
              "dV": torch.empty(dv.shape, dtype=dv.dtype, pin_memory=True)}
     dev_out = {"O": o, "LSE": lse, "dQ": dq, "dK": dk, "dV": dv}
-    ws = torch.empty(bwd_workspace_bytes(chunk, Hq, Hkv, N, d) // 4, dtype=torch.float32, device="cuda")
+    ws = torch.empty((default_bwd_workspace_bytes(chunk, Hq, Hkv, N, d, None, causal) + 3) // 4, dtype=torch.float32,
+                     device="cuda")
     s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     done_cmp = [torch.cuda.Event() for _ in range(nchunks)]
     done_out = [torch.cuda.Event() for _ in range(nchunks)]

@@ -154,6 +154,18 @@ hk_status hk_attn_bwd_varlen_ex(const void* Q, const void* K, const void* V, con
                                 int Hq, int Hkv, int total_q, int total_k, int max_seqlen_q, int max_seqlen_k,
                                 int d, int causal, unsigned flags, cudaStream_t stream);
 
+/* ---- Stored-dS backward (ABI 6; d = 128, dense calls: hk_attn_bwd, _qk, _ex).
+ * A workspace of at least hk_attn_bwd_ds_workspace_bytes(...) bytes (> the plain size exactly when the
+ * path applies) selects it: the dK/dV pass also writes every visited 128 x 128 block's bf16 dS^T
+ * into the workspace (after the plain part, 1024-byte aligned), and the dQ pass is then ONE GEMM per
+ * block, dQ = (1/sqrt d) dS K, reading those tiles back, instead of re-computing S and dP (three
+ * GEMMs). The extra workspace is B * Hq * blocks * 32 KB, blocks = T(T+1)/2 (causal, Nq == Nk) or
+ * Tq * Tk, T = ceil(N / 128): 35 GB for B = 16, Hq = 32, N = 8192 causal. Results: dK, dV bitwise the
+ * two-pass ones; dQ is formed from the dK/dV pass's bf16 dS (computed from S^T = K Q^T) and differs
+ * from the two-pass dQ by that rounding (reading #29); bitwise reproducible run to run.
+ * Returns the plain workspace size where the path does not apply (d = 64, varlen is separate API). */
+size_t hk_attn_bwd_ds_workspace_bytes(int B, int Hq, int Hkv, int Nq, int Nk, int d, int causal);
+
 /* ---- SM budget for the persistent kernels (ABI 5).
  * Every kernel of this library that runs one CTA per SM (forward, backward passes, GEMM) and the
  * grid-stride helpers launch on at most max_ctas SMs' worth of CTAs (max_ctas <= 0: all SMs, the

@@ -43,6 +43,7 @@ SIGNATURES = {
     "hk_attn_merge": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P]),
     "hk_accum_bf16": (_I, [_P, _P, _P, _Z, _I, _P]),
     "hk_accum_f32": (_I, [_P, _P, _Z, _P]),
+    "hk_attn_bwd_ds_workspace_bytes": (_Z, [_I, _I, _I, _I, _I, _I, _I]),
     "hk_set_max_ctas": (None, [_I]),
     "hk_get_max_ctas": (_I, []),
     "hk_attn_last_error": (ctypes.c_char_p, []),

@@ -81,6 +81,32 @@ def bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk=None) -> int:
     return int(lib().hk_attn_bwd_qk_workspace_bytes(B, Hq, Hkv, N, Nk, d))
 
 
+def bwd_ds_workspace_bytes(B, Hq, Hkv, N, d, Nk=None, causal=False) -> int:
+    """Workspace size that selects the stored-dS backward (hk_attn_bwd_ds_workspace_bytes; equal to
+    bwd_workspace_bytes where that path does not apply)."""
+    return int(lib().hk_attn_bwd_ds_workspace_bytes(B, Hq, Hkv, N, N if Nk is None else Nk, d, int(bool(causal))))
+
+
+# Largest stored-dS workspace attn_bwd allocates on its own (bytes; None = a quarter of the device's
+# memory). Larger problems, or a caller-supplied workspace of the plain size, take the two-pass dQ.
+DS_WORKSPACE_BUDGET = None
+
+
+def _ds_budget(device) -> int:
+    if DS_WORKSPACE_BUDGET is not None:
+        return int(DS_WORKSPACE_BUDGET)
+    return torch.cuda.get_device_properties(device).total_memory // 4
+
+
+def default_bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk=None, causal=False, device=None) -> int:
+    """The workspace attn_bwd allocates when given none: the stored-dS size where that path applies
+    and fits DS_WORKSPACE_BUDGET, else the plain size."""
+    plain = bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk)
+    ds = bwd_ds_workspace_bytes(B, Hq, Hkv, N, d, Nk, causal)
+    dev = torch.cuda.current_device() if device is None else device
+    return ds if plain < ds <= _ds_budget(dev) else plain
+
+
 HK_BWD_DETERMINISTIC = 1  # include/hk_attn.h
 HK_BWD_ACCUMULATE_F32 = 2
 
@@ -107,9 +133,10 @@ def attn_bwd(q, k, v, o, lse, do, causal: bool = False, workspace=None, dq=None,
     for n, t, ref in (("dq", dq, q), ("dk", dk, k), ("dv", dv, v)):
         _check_tensor(n, t, torch.float32 if accumulate else torch.bfloat16)
         _expect_shape(n, t, ref.shape)
-    nbytes = bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk)
-    ws = torch.empty(nbytes // 4, dtype=torch.float32, device=q.device) if workspace is None else workspace
-    _check_workspace(ws, nbytes)
+    # no workspace given: the stored-dS backward (d = 128) when its workspace fits the budget
+    nbytes = default_bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk, causal, q.device) if workspace is None else 0
+    ws = torch.empty((nbytes + 3) // 4, dtype=torch.float32, device=q.device) if workspace is None else workspace
+    _check_workspace(ws, bwd_workspace_bytes(B, Hq, Hkv, N, d, Nk))
     check(lib().hk_attn_bwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
                                _ptr(dv), _ptr(ws), ws.numel() * ws.element_size(), B, Hq, Hkv, N, Nk, d,
                                int(bool(causal)), (HK_BWD_DETERMINISTIC if deterministic else 0) |

@@ -216,7 +216,29 @@ struct BwdParams {
   SeqGeom g;          // dense / varlen geometry (seq.cuh)
   int B, Hq, Hkv, Np, Npk;  // Npk = Nk (varlen: max_seqlen_k) rounded up to 128
   bool acc32;         // HK_BWD_ACCUMULATE_F32: dq / dk / dv are fp32 accumulators the results add into
+  // Stored-dS backward (d = 128, dense; ds_block_index): the dK/dV pass also writes each block's bf16
+  // dS^T tile here, 32 KB in the shared-memory image of the MN-major SW128 A operand of dQ = dS K, and
+  // the dQ pass (bwd_dqds_kernel) is one GEMM per block reading it back. nullptr: the two-pass dQ.
+  __nv_bfloat16* ds;
+  int ds_tri;  // 1: causal with Nq == Nk, blocks (qi, jt <= qi) packed per head as a triangle
 };
+
+// 32-byte streaming store (sm_100: STG.256)
+__device__ __forceinline__ void st_global_cs_v8(void* p, const uint32_t (&v)[8]) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
+// Block (b, h, qi, jt) of the stored dS: per (b, h) either the triangle jt <= qi (causal, Nq == Nk:
+// the only blocks the dK/dV pass visits) or the whole Tq x Tk rectangle.
+__device__ __forceinline__ size_t ds_block_index(const BwdParams& p, int b, int h, int qi, int jt) {
+  const int Tq = p.Np / 128, Tk = p.Npk / 128;
+  const size_t per_head = p.ds_tri ? (size_t)Tq * (Tq + 1) / 2 : (size_t)Tq * Tk;
+  const size_t in_head = p.ds_tri ? (size_t)qi * (qi + 1) / 2 + jt : (size_t)qi * Tk + jt;
+  return ((size_t)b * p.Hq + h) * per_head + in_head;
+}
+constexpr uint32_t DS_BLOCK_ELEMS = 128 * 128;  // one bf16 dS tile: [2 panels of 64 queries][128 keys][64]
 
 
 // 128 x 128 tiles throughout: tcgen05.mma with N=64 paces at 48 cycles per
@@ -228,7 +250,10 @@ template <int D>
 struct BwdCfg {
   static constexpr int PANELS = D / 64;
   static constexpr uint32_t T128 = 128 * D * 2;  // a 128-row [rows][D] bf16 tile
-  static constexpr int NSA = (D == 128) ? 3 : 4;  // ring A depth
+#ifndef HK_DKDV_NSA128
+#define HK_DKDV_NSA128 3
+#endif
+  static constexpr int NSA = (D == 128) ? HK_DKDV_NSA128 : 4;  // ring A depth
   static constexpr int NSB = (D == 128) ? 2 : 4;  // ring B depth
   // B1: K_j, V_j resident; ring A = {Q_i}, ring B = {dO_i, lse2_i, D_i} (both freed after dK).
   // At D=128 this is 224 KB + barriers: no room for alignment slack, so the
@@ -404,14 +429,16 @@ __device__ __forceinline__ KvItem kv_decode(const BwdParams& p, int item) {
   return it;
 }
 
-template <int D, bool CAUSAL, bool FQ>
+template <int D, bool CAUSAL, bool FQ, bool DS = false>
 __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS1, 1)
     bwd_dkdv_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapdO,
                     const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                     const __grid_constant__ CUtensorMap mapDQ, const BwdParams p) {
   using C = BwdCfg<D>;
+  static_assert(!DS || (D == 128 && !FQ), "stored-dS dK/dV pass: d = 128, two-pass");
   constexpr bool FQ128 = FQ && D == 128;  // fused, d = 128: dQ_partial in the S^T columns (BwdCfg)
-  constexpr int NSA = FQ ? C::NSA_F : C::NSA, NSB = FQ ? C::NSB_F : C::NSB;
+  // DS: ring A one slot shallower, its 32 KB the staging tile of the dS^T stores
+  constexpr int NSA = FQ ? C::NSA_F : (DS ? C::NSA - 1 : C::NSA), NSB = FQ ? C::NSB_F : C::NSB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   if ((FQ ? C::SLACK_F : C::SLACK1) == 0 && smem != smem_raw) __trap();  // layouts without alignment slack
@@ -419,9 +446,9 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
   uint8_t* sV = smem + C::T128;
   uint8_t* sA = smem + 2 * C::T128;   // ring A slot s: Q [T128]
   uint8_t* sB = sA + NSA * C::T128;   // ring B slot s: dO [T128] lse2 [512 B] D [512 B]
-  uint8_t* sDS = sB + NSB * C::SLOT_B1;                 // FQ: dS tile (MN-major A of dQ_partial = dS K)
+  uint8_t* sDS = sB + NSB * C::SLOT_B1;                 // FQ: dS tile (MN-major A of dQ_partial = dS K); DS: staging
   uint8_t* sDQ = FQ128 ? sDS : sDS + (FQ ? C::DS_TILE : 0);  // FQ: dQ_partial staging (d=128: the dS tile)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + (FQ ? C::DS_TILE + C::DQ_STAGE : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + (FQ ? C::DS_TILE + C::DQ_STAGE : (DS ? C::T128 : 0)));
   uint64_t* fullA = bars;             // [NSA]
   uint64_t* emptyA = bars + NSA;      // [NSA]
   uint64_t* fullB = bars + 2 * NSA;   // [NSB]
@@ -877,6 +904,7 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
         tc_fence_after();
         if (threadIdx.x == 0) hk_trace(4, u, 0);
         float dp[CW];
+        uint32_t dsk[DS ? 32 : 1];  // stored-dS (DS): this row's packed bf16 dS^T
         tmem_ld_cols<CW>(tmem_addr(cP, lb, 0), dp);
         tmem_wait_ld();
 #if HK_DKDV_SHFL
@@ -927,6 +955,12 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
           for (int k = 0; k < CW / 8; ++k)
             sts_v4(rowp + (((c0 + k) ^ (r & 7)) << 4), pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
           fence_proxy_async_smem();  // generic-proxy stores visible to the tensor core
+        } else if constexpr (DS) {
+          // stored-dS backward: the same bf16 dS^T into TMEM (dK) and — after bar_ds is published,
+          // off the MMA's critical path — to the workspace for the dQ pass (below)
+#pragma unroll
+          for (int c2 = 0; c2 < 32; ++c2) dsk[c2] = pack_bf16(dp[2 * c2], dp[2 * c2 + 1]);
+          tmem_st32(tmem_addr(cP, lb, 0), dsk);
         } else {
           tmem_st_packed_cols<CW>(tmem_addr(cP, lb, 0), dp);
         }
@@ -935,6 +969,33 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_ds);
         if (threadIdx.x == 0) hk_trace(5, u, 0);
+        if constexpr (DS) {
+          {
+          // key row r of panel wg of the block's MN-major SW128 A-operand image (16-B chunk c at
+          // c ^ (r % 8)) in 32-byte streaming stores (whole sectors): chunks 2m, 2m + 1 sit at positions
+          // (2m) ^ x, (2m + 1) ^ x, x = r % 8, i.e. in the 32-B slot m ^ (x / 2), swapped when x is odd
+          // through this warpgroup's 16 KB panel of the staging tile and one bulk copy (whole 128-B
+          // lines, issued by the TMA engine: global stores from 256 threads would queue in the
+          // load/store unit ahead of the LSE2/D broadcasts the next block's phases need)
+          const bool leader = (warp & 3) == 0 && lane == 0;
+          const uint32_t stg = smem_u32(sDS) + wg * (C::T128 / 2);
+          if (leader) tma_store_wait_read0();  // the previous block's copy has read the panel
+          named_bar_sync(1 + wg, 128);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            sts_v4(stg + r * 128 + ((k ^ (r & 7)) << 4), dsk[4 * k], dsk[4 * k + 1], dsk[4 * k + 2], dsk[4 * k + 3]);
+          fence_proxy_async_smem();
+          named_bar_sync(1 + wg, 128);
+#ifndef HK_DS_NOSTORE
+#define HK_DS_NOSTORE 0  // experiment: stage but skip the copy to HBM (the cost of the staging alone)
+#endif
+          if (leader && !HK_DS_NOSTORE) {
+            bulk_store_hint(p.ds + ds_block_index(p, w.b, hq, qi, w.jt) * DS_BLOCK_ELEMS + wg * (DS_BLOCK_ELEMS / 2),
+                            sDS + wg * (C::T128 / 2), C::T128 / 2, policy_evict_first());
+            tma_store_commit();
+          }
+          }
+        }
         if (++qi == w.nqt) {
           qi = w.i0;
           ++hq;
@@ -972,6 +1033,9 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
           for (int k = 0; k < 4; ++k) dst[k] = o4[k];
         }
       }
+    }
+    if constexpr (DS) {
+      if ((warp & 3) == 0 && lane == 0) tma_store_wait0();  // this warpgroup's dS copies complete
     }
   } else if constexpr (FQ) {
     reg_dealloc<96>();  // the two idle warps (10, 11) give their share to the elementwise warps
@@ -1336,6 +1400,162 @@ __global__ void __launch_bounds__(BwdCfg<D>::THREADS2, 1)
   if (threadIdx.x == 0) sched_exit(ctr);
 }
 
+// ---------------------------------------------------------------- B2 from the stored dS
+// dQ(qi) = (1/sqrt d) sum_j dS(qi, j) K_j with dS read back from the workspace (written by the dK/dV
+// pass, bwd_dkdv_kernel with p.ds): one 128 x 128 x 128 GEMM per block instead of the three of
+// bwd_dq_kernel (S and dP recomputed there). The pass is HBM-bound (32 KB of dS per 512 tensor
+// cycles). Persistent, dynamic schedule (items as dq_decode: heaviest first). Roles: warp 0 producer
+// (1-D bulk copy of the 32 KB dS image + TMA of K_j into a 3-stage ring), warp 1 MMA (dQ += dS K_j into
+// one of two TMEM accumulators), warps 2-5 epilogue (TMEM -> bf16 rows, or added into fp32 dQ).
+struct DqdsCfg {
+  static constexpr int NS = 3;
+  static constexpr uint32_t TILE = 128 * 128 * 2;  // 32 KB
+  static constexpr uint32_t STAGE = 2 * TILE;      // dS block | K_j
+  static constexpr uint32_t SMEM = NS * STAGE + 1024;
+  static constexpr int THREADS = 192;
+};
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(DqdsCfg::THREADS, 1)
+    bwd_dqds_kernel(const __grid_constant__ CUtensorMap mapK, const BwdParams p) {
+  using C = DqdsCfg;
+  constexpr int D = 128, NS = C::NS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[NS], empty[NS], tfull[2], tempty[2];
+  __shared__ Sched sched;
+  __shared__ uint32_t tmem_base_s;
+  const int warp = warp_id(), lane = lane_id();
+  const int num_items = p.B * p.Hq * (p.Np / 128);
+  unsigned* const ctr = p.sched + 2;
+  if (threadIdx.x == 0) {
+    sched_init(sched, 5);  // MMA warp + 4 epilogue warps
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tma_prefetch(&mapK);
+  if (warp == 1) tmem_alloc<256>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base_s, 0);
+
+  if (warp == 0) {
+    // ================= producer =================
+    if (lane == 0) {
+      const uint64_t pol_k = policy_evict_last();
+      const uint64_t pol_ds = policy_evict_first();  // each dS tile is read once
+      int u = 0;
+      for (int r = 0;; ++r) {
+        const int item = sched_publish(sched, ctr, r);
+        if (item >= num_items) break;
+        const DqItem w = dq_decode<CAUSAL>(p, item);
+        for (int j = 0; j < w.n_it; ++j, ++u) {
+          const int s = u % NS;
+          mbar_wait(&empty[s], ((u / NS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], C::STAGE);
+          uint8_t* st = smem + s * C::STAGE;
+          bulk_load_hint(st, p.ds + ds_block_index(p, w.b, w.h, w.iq, j) * DS_BLOCK_ELEMS, C::TILE, &full[s], pol_ds);
+          for (int pn = 0; pn < 2; ++pn)
+            tma_load_4d(&mapK, &full[s], st + C::TILE + pn * 128 * 128, pn * 64, w.kvh, w.sq.k0 + j * 128, w.sq.tb,
+                        pol_k);
+        }
+      }
+      drain_ring(empty, NS, u);
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    constexpr uint32_t idesc = idesc_bf16(128, D, 1, 1);  // M = 128 queries, A = dS and B = K MN-major
+    constexpr uint64_t MNMAJ = sdesc_sw128_const(128 * 128, 1024);
+    const uint32_t a0 = smem_u32(smem);
+    int u = 0, n_items = 0;
+    for (int r = 0;; ++r) {
+      const int item = sched_take(sched, r);
+      if (item >= num_items) break;
+      const DqItem w = dq_decode<CAUSAL>(p, item);
+      const int a = n_items & 1;
+      // every item takes a turn of its accumulator (an item without keys commits no MMA: its tfull
+      // completes at once and the epilogue writes zeros), so both sides count phases per item
+      mbar_wait(&tempty[a], ((n_items >> 1) & 1) ^ 1);  // the epilogue has read this accumulator out
+      for (int j = 0; j < w.n_it; ++j, ++u) {
+        const int s = u % NS;
+        mbar_wait(&full[s], (u / NS) & 1);
+        tc_fence_after();
+        const uint32_t st = a0 + s * C::STAGE;
+        gemm_ss_mnmn(tb + 128 * a, MNMAJ | (st >> 4), MNMAJ | ((st + C::TILE) >> 4), idesc, j > 0 ? 1u : 0u);
+        tc_commit_w(&empty[s]);
+      }
+      tc_commit_w(&tfull[a]);
+      ++n_items;
+    }
+  } else {
+    // ================= epilogue (warps 2-5: TMEM lane quadrant warp % 4) =================
+    const uint32_t lb = (warp & 3) * 32;
+    const int r = (warp & 3) * 32 + lane;  // query row within the tile
+    const float scale = rsqrtf((float)D);
+    int n_items = 0;
+    for (int rr = 0;; ++rr) {
+      const int item = sched_take(sched, rr);
+      if (item >= num_items) break;
+      const DqItem w = dq_decode<CAUSAL>(p, item);
+      const int a = n_items & 1;
+      const int row = w.iq * 128 + r;
+      const bool row_ok = row < w.sq.lq;
+      const size_t base = ((size_t)(w.sq.gq0 + (row_ok ? row : 0)) * p.Hq + w.h) * D;
+      mbar_wait(&tfull[a], (n_items >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t o[32];
+        if (w.n_it > 0) {
+          tmem_ld32(tmem_addr(tb + 128 * a, lb, c0), o);
+          tmem_wait_ld();
+          if (c0 + 32 == D) {  // accumulator read out: the item after next may overwrite it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);
+          }
+        } else {  // no key visible to this tile: dQ = 0
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] = 0u;
+          if (c0 + 32 == D) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);
+          }
+        }
+        if (p.acc32 && w.n_it == 0) continue;  // accumulate mode: nothing to add
+        if (!row_ok) continue;
+        if (p.acc32) {
+          float* dst = reinterpret_cast<float*>(p.dq) + base + c0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) add8_f32(dst + 8 * k, o + 8 * k, scale);
+        } else {
+          uint4 v[4];
+          uint32_t* vp = reinterpret_cast<uint32_t*>(v);
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            vp[k] = pack_bf16(__uint_as_float(o[2 * k]) * scale, __uint_as_float(o[2 * k + 1]) * scale);
+          uint4* dst = reinterpret_cast<uint4*>(p.dq + base + c0);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) dst[k] = v[k];
+        }
+      }
+      ++n_items;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tb);
+  if (threadIdx.x == 0) sched_exit(ctr);
+}
+
 // ---------------------------------------------------------------- host launch
 #ifndef HK_BWD_FORK
 #define HK_BWD_FORK 1
@@ -1381,6 +1601,7 @@ struct BwdShape {
   int total_q, total_k;    // varlen only
   bool fused;              // d = 64: single-pass dQ (bulk reduce-add into the fp32 accumulator) — not bitwise
   bool acc32;              // HK_BWD_ACCUMULATE_F32: dQ, dK, dV are fp32 accumulators
+  bool ds;                 // stored-dS backward (bwd_ds_bytes > 0 and the workspace holds it)
 };
 
 // Workspace layout of one backward call (hk_attn.h): D and LSE2 [B][Hq][Np] fp32, 256 bytes of work
@@ -1394,6 +1615,16 @@ struct BwdShape {
 #define HK_FUSED128 0
 #endif
 constexpr bool bwd_fused_default(int d) { return d == 64 || HK_FUSED128; }
+
+// Stored-dS backward (d = 128, dense, not the fused pass): bf16 dS tiles of every visited block after
+// the workspace's first part, at a 1024-byte aligned offset; 0 where the path does not apply.
+inline size_t bwd_ds_bytes(int B, int Hq, int Nq, int Nk, int d, bool causal, bool varlen) {
+  if (d != 128 || varlen || bwd_fused_default(d) || B <= 0 || Hq <= 0 || Nq <= 0 || Nk <= 0) return 0;
+  const size_t Tq = ((size_t)Nq + 127) / 128, Tk = ((size_t)Nk + 127) / 128;
+  const size_t per_head = (causal && Nq == Nk) ? Tq * (Tq + 1) / 2 : Tq * Tk;
+  return (size_t)B * Hq * per_head * DS_BLOCK_ELEMS * 2;
+}
+inline size_t bwd_ds_offset(size_t ws) { return (ws + 1023) / 1024 * 1024; }
 
 inline size_t bwd_ws_bytes(int B, int Hq, int Nq, int d) {
   if (B <= 0 || Hq <= 0 || Nq <= 0) return 0;
@@ -1431,6 +1662,9 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     if (!done.count(dev)) {
       bool ok2 = set_smem(bwd_dkdv_kernel<D, CAUSAL, false>, C::SMEM1) && set_smem(bwd_dq_kernel<D, CAUSAL>, C::SMEM2);
       ok2 = ok2 && set_smem(bwd_dkdv_kernel<D, CAUSAL, true>, C::SMEM1F);
+      if (D == 128)
+        ok2 = ok2 && set_smem(bwd_dqds_kernel<CAUSAL>, DqdsCfg::SMEM) &&
+              set_smem(bwd_dkdv_kernel<D, CAUSAL, false, D == 128>, C::SMEM1);
       if (!ok2) {
         snprintf(err, errlen, "cudaFuncSetAttribute(max dynamic smem) failed");
         return HK_ERR_DEVICE;
@@ -1459,7 +1693,11 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
               Hkv,
               Np,
               Npk,
-              sh.acc32};
+              sh.acc32,
+              sh.ds ? reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(ws) +
+                                                      bwd_ds_offset(bwd_ws_bytes(B, Hq, sh.Nq, D)))
+                    : nullptr,
+              CAUSAL && sh.Nq == sh.Nk ? 1 : 0};
   // B0: grid (x, b), x sized for the longest sequence and capped at ~16 blocks per SM overall
   const size_t rows = (size_t)sh.Nq * Hq;
   constexpr int RPW0 = 32 / (D / (8 * pre_vpl(D)));  // rows per warp pass of the preprocess
@@ -1478,7 +1716,7 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
   // CTAs take the SMs the dK/dV pass's last CTAs free instead of waiting for the whole pass.
   cudaStream_t s2 = stream;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (HK_BWD_FORK && phase < 0 && !fq) {
+  if (HK_BWD_FORK && phase < 0 && !fq && !sh.ds) {  // (the stored-dS dQ pass reads the dK/dV pass's dS)
     s2 = side_stream(stream);
     if (s2 && cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) == cudaSuccess &&
         cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) == cudaSuccess &&
@@ -1493,6 +1731,8 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     const int grid = items < num_sms ? items : num_sms;
     if (fq)
       bwd_dkdv_kernel<D, CAUSAL, true><<<grid, C::THREADS1F, C::SMEM1F, stream>>>(mQ, mdO, mK, mV, mDQ, p);
+    else if (D == 128 && sh.ds)
+      bwd_dkdv_kernel<D, CAUSAL, false, D == 128><<<grid, C::THREADS1, C::SMEM1, stream>>>(mQ, mdO, mK, mV, mDQ, p);
     else
       bwd_dkdv_kernel<D, CAUSAL, false><<<grid, C::THREADS1, C::SMEM1, stream>>>(mQ, mdO, mK, mV, mDQ, p);
   }
@@ -1500,7 +1740,10 @@ hk_status launch_bwd_t(const void* Q, const void* K, const void* V, const void* 
     dq_convert_kernel<D><<<dim3((unsigned)bx, (unsigned)B), 256, 0, stream>>>(
         dq_acc, reinterpret_cast<__nv_bfloat16*>(dQ), g, Hq, rsqrtf((float)D), sh.acc32);
   }
-  if (!fq && (phase < 0 || phase == 2)) {
+  if (D == 128 && sh.ds && (phase < 0 || phase == 2)) {
+    const int items = B * Hq * (Np / 128);
+    bwd_dqds_kernel<CAUSAL><<<items < num_sms ? items : num_sms, DqdsCfg::THREADS, DqdsCfg::SMEM, stream>>>(mK, p);
+  } else if (!fq && (phase < 0 || phase == 2)) {
     const int items = B * Hq * (Np / 128);  // persistent: one CTA per SM
     bwd_dq_kernel<D, CAUSAL><<<items < num_sms ? items : num_sms, C::THREADS2, C::SMEM2, s2>>>(mQ, mdO, mK, mV,
                                                                                              p);

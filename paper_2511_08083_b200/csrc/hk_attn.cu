@@ -68,8 +68,9 @@ const char* hk_status_string(hk_status s) {
   return "HK_ERR_UNKNOWN";
 }
 
-int hk_attn_abi_version(void) { return 5; }  // 2: + Nq != Nk and varlen; 4: + _ex (flags), fused d=64 bwd, rope;
+int hk_attn_abi_version(void) { return 6; }  // 2: + Nq != Nk and varlen; 4: + _ex (flags), fused d=64 bwd, rope;
                                               // 5: + hk_set_max_ctas / hk_get_max_ctas, hk_accum_f32
+                                              // 6: + stored-dS backward (hk_attn_bwd_ds_workspace_bytes)
 void hk_set_max_ctas(int max_ctas) { g_max_ctas.store(max_ctas > 0 ? max_ctas : 0); }
 int hk_get_max_ctas(void) { return g_max_ctas.load(); }
 
@@ -84,6 +85,12 @@ hk_status hk_attn_fwd(const void* Q, const void* K, const void* V, void* O, floa
 size_t hk_attn_bwd_workspace_bytes(int B, int Hq, int Hkv, int N, int d) {
   (void)Hkv;
   return ws_bytes(B, Hq, N, d);
+}
+size_t hk_attn_bwd_ds_workspace_bytes(int B, int Hq, int Hkv, int Nq, int Nk, int d, int causal) {
+  (void)Hkv;
+  const size_t ws = ws_bytes(B, Hq, Nq, d);
+  const size_t ds = hk::bwd_ds_bytes(B, Hq, Nq, Nk, d, causal != 0, false);
+  return ds ? hk::bwd_ds_offset(ws) + ds : ws;
 }
 hk_status hk_attn_bwd(const void* Q, const void* K, const void* V, const void* O, const float* LSE, const void* dO,
                       void* dQ, void* dK, void* dV, void* workspace, size_t workspace_bytes, int B, int Hq, int Hkv,

@@ -177,7 +177,12 @@ static hk_status bwd_impl(int phase, const void* Q, const void* K, const void* V
   if (s != HK_OK) return s;
   // NEXT #1 single pass: d = 64 (d = 128 only in -DHK_FUSED128=1 builds, bwd.cuh)
   const bool fused = hk::bwd_fused_default(d) && !(flags & HK_BWD_DETERMINISTIC);
-  const hk::BwdShape bs{sh.cu_q, sh.cu_k, sh.B, sh.Hq, sh.Hkv, sh.Nq, sh.Nk, sh.total_q, sh.total_k, fused, acc32};
+  // stored-dS backward: whenever the caller's workspace has room for the dS tiles
+  // (hk_attn_bwd_ds_workspace_bytes)
+  const size_t ds_need = hk::bwd_ds_bytes(sh.B, sh.Hq, sh.Nq, sh.Nk, d, causal != 0, sh.cu_q != nullptr);
+  const bool ds = !fused && ds_need > 0 && workspace_bytes >= hk::bwd_ds_offset(need) + ds_need;
+  const hk::BwdShape bs{sh.cu_q, sh.cu_k, sh.B,        sh.Hq, sh.Hkv, sh.Nq, sh.Nk,
+                        sh.total_q, sh.total_k, fused, acc32, ds};
   return hk::launch_bwd(Q, K, V, O, LSE, dO, dQ, dK, dV, reinterpret_cast<float*>(workspace), bs, d, causal != 0,
                         stream, g_err, sizeof(g_err), phase, num_sms);
 }

@@ -56,7 +56,7 @@ def test_host_only_validation(lib):
     size, and argument validation that fails before any CUDA call."""
     from paper_2511_08083_b200 import _lib
     L = _lib.lib()
-    assert L.hk_attn_abi_version() == 5
+    assert L.hk_attn_abi_version() == 6
     assert L.hk_status_string(2) == b"HK_ERR_UNSUPPORTED"
     assert L.hk_attn_bwd_workspace_bytes(2, 4, 2, 256, 128) == 2 * 2 * 4 * 256 * 4 + 256
     # d = 64 adds the fused backward's fp32 dQ accumulator, B * Np * Hq * 64 floats
