@@ -114,7 +114,11 @@ def test_varlen_uniform_equals_dense_bitwise(N, d, causal):
     B, Hq, Hkv = 3, 4, 2
     x = make_inputs(B, N, Hq, Hkv, d, seed=9, device="cuda")
     o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
-    dq, dk, dv = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, deterministic=True)
+    # the plain workspace: the two-pass backward the varlen entry runs (without one, a dense d = 128
+    # call takes the stored-dS path, whose dQ rounds dS from S^T: reading #29)
+    from paper_2511_08083_b200 import bwd_workspace_bytes
+    ws = torch.empty(bwd_workspace_bytes(B, Hq, Hkv, N, d) // 4, dtype=torch.float32, device="cuda")
+    dq, dk, dv = attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, deterministic=True, workspace=ws)
     cu = torch.arange(0, (B + 1) * N, N, dtype=torch.int32, device="cuda")
     flat = lambda t: t.reshape(B * N, t.shape[2], d)
     ov, lv = attn_fwd_varlen(flat(x["Q"]), flat(x["K"]), flat(x["V"]), cu, cu, N, N, causal)
