@@ -974,24 +974,25 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
           // key row r of panel wg of the block's MN-major SW128 A-operand image (16-B chunk c at
           // c ^ (r % 8)) in 32-byte streaming stores (whole sectors): chunks 2m, 2m + 1 sit at positions
           // (2m) ^ x, (2m + 1) ^ x, x = r % 8, i.e. in the 32-B slot m ^ (x / 2), swapped when x is odd
-          // through this warpgroup's 16 KB panel of the staging tile and one bulk copy (whole 128-B
-          // lines, issued by the TMA engine: global stores from 256 threads would queue in the
-          // load/store unit ahead of the LSE2/D broadcasts the next block's phases need)
-          const bool leader = (warp & 3) == 0 && lane == 0;
-          const uint32_t stg = smem_u32(sDS) + wg * (C::T128 / 2);
-          if (leader) tma_store_wait_read0();  // the previous block's copy has read the panel
-          named_bar_sync(1 + wg, 128);
+          // through this warp's 4 KB of the staging tile (its 32 key rows of panel wg, contiguous in
+          // the block image too) and one bulk copy by lane 0: whole 128-B lines issued by the TMA
+          // engine (global stores from 256 threads would queue in the load/store unit ahead of the
+          // LSE2/D broadcasts the next phases need), and no barrier wider than the warp
+          const uint32_t stg = smem_u32(sDS) + wg * (C::T128 / 2) + lb * 128;
+          if (lane == 0) tma_store_wait_read0();  // this warp's previous copy has read its rows
+          __syncwarp();
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            sts_v4(stg + r * 128 + ((k ^ (r & 7)) << 4), dsk[4 * k], dsk[4 * k + 1], dsk[4 * k + 2], dsk[4 * k + 3]);
+            sts_v4(stg + lane * 128 + ((k ^ (r & 7)) << 4), dsk[4 * k], dsk[4 * k + 1], dsk[4 * k + 2], dsk[4 * k + 3]);
           fence_proxy_async_smem();
-          named_bar_sync(1 + wg, 128);
+          __syncwarp();
 #ifndef HK_DS_NOSTORE
 #define HK_DS_NOSTORE 0  // experiment: stage but skip the copy to HBM (the cost of the staging alone)
 #endif
-          if (leader && !HK_DS_NOSTORE) {
-            bulk_store_hint(p.ds + ds_block_index(p, w.b, hq, qi, w.jt) * DS_BLOCK_ELEMS + wg * (DS_BLOCK_ELEMS / 2),
-                            sDS + wg * (C::T128 / 2), C::T128 / 2, policy_evict_first());
+          if (lane == 0 && !HK_DS_NOSTORE) {
+            bulk_store_hint(p.ds + ds_block_index(p, w.b, hq, qi, w.jt) * DS_BLOCK_ELEMS + wg * (DS_BLOCK_ELEMS / 2) +
+                                lb * 64,
+                            sDS + wg * (C::T128 / 2) + lb * 128, 32 * 128, policy_evict_first());
             tma_store_commit();
           }
           }
@@ -1035,7 +1036,7 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
       }
     }
     if constexpr (DS) {
-      if ((warp & 3) == 0 && lane == 0) tma_store_wait0();  // this warpgroup's dS copies complete
+      if (lane == 0) tma_store_wait0();  // this warp's dS copies complete
     }
   } else if constexpr (FQ) {
     reg_dealloc<96>();  // the two idle warps (10, 11) give their share to the elementwise warps
