@@ -30,7 +30,22 @@ METRICS = {
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ms": 1e6, "us": 1e3, "ns": 1,
               "usecond": 1e3, "msecond": 1e6, "nsecond": 1, "Ghz": 1, "Mhz": 1e-3, "hz": 1e-9}
-NAMES = {"fwd_kernel": "fwd", "bwd_pre_kernel": "bwd_pre", "bwd_dkdv_kernel": "bwd_dkdv", "bwd_dq_kernel": "bwd_dq"}
+NAMES = {"fwd_kernel": "fwd", "bwd_pre_kernel": "bwd_pre", "bwd_dkdv_kernel": "bwd_dkdv", "bwd_dq_kernel": "bwd_dq",
+         "bwd_dqds_kernel": "bwd_dq_ds", "dq_convert_kernel": "dq_convert"}
+
+
+def short_name(name):
+    """bench.py's kernel names: bwd_dkdv_kernel<D, CAUSAL, FQ, DS> is bwd_dkdv_dq when fused (d = 64),
+    bwd_dkdv_ds when it stores dS, bwd_dkdv otherwise."""
+    short = next((v for k, v in NAMES.items() if k in name), None)
+    if short == "bwd_dkdv":
+        args = [a.strip() for a in name.split("<", 1)[1].split(">", 1)[0].split(",")]
+        flags = [a.endswith("1") or a.endswith("true") for a in args[2:]]
+        if flags and flags[0]:
+            return "bwd_dkdv_dq"
+        if len(flags) > 1 and flags[1]:
+            return "bwd_dkdv_ds"
+    return short
 
 
 def main(rep, config, tag):
@@ -41,7 +56,7 @@ def main(rep, config, tag):
     out = []
     for r in data:
         name = r[idx["Kernel Name"]]
-        short = next((v for k, v in NAMES.items() if k in name), None)
+        short = short_name(name)
         if short is None:
             continue
         rec = {"kernel": short, "signature": name}
@@ -96,7 +111,7 @@ def launches(csv_path, out_md):
             continue
         v = float(r["Metric Value"].replace(",", "")) * UNIT_SCALE.get(r["Metric Unit"], 1) / 1e6
         k = r["Kernel Name"]
-        short = next((s for key, s in NAMES.items() if key in k), re.sub(r"\(.*", "", k)[:60])
+        short = short_name(k) or re.sub(r"\(.*", "", k)[:60]
         per.setdefault(short, [0, 0.0])
         per[short][0] += 1
         per[short][1] += v

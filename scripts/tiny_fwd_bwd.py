@@ -7,7 +7,8 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
-from paper_2511_08083_b200 import attn_bwd, attn_bwd_varlen, attn_fwd, attn_fwd_varlen, gemm, ring  # noqa: E402
+from paper_2511_08083_b200 import (attn_bwd, attn_bwd_varlen, attn_fwd, attn_fwd_varlen, bwd_workspace_bytes,  # noqa: E402
+                                   gemm, ring)
 from paper_2511_08083_b200.inputs import make_gemm_inputs, make_inputs, make_qk_inputs, make_varlen_inputs  # noqa: E402
 
 # (B, N, Hq, Hkv, d, causal): fwd 512 items, dQ 1024 items (> 148 SMs), dK/dV 256 items (MHA case)
@@ -15,7 +16,9 @@ for B, N, Hq, Hkv, d, causal in ((2, 1024, 64, 8, 128, True), (2, 1024, 16, 16, 
                                  (1, 200, 2, 1, 128, True)):
     x = make_inputs(B, N, Hq, Hkv, d, seed=1, device="cuda")
     o, lse = attn_fwd(x["Q"], x["K"], x["V"], causal)
-    attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal)
+    attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal)  # d = 128: the stored-dS backward
+    ws = torch.empty(bwd_workspace_bytes(B, Hq, Hkv, N, d) // 4, dtype=torch.float32, device="cuda")
+    attn_bwd(x["Q"], x["K"], x["V"], o, lse, x["dO"], causal, workspace=ws)  # the two-pass backward
 for M, N, K in ((4096, 4096, 128), (2048, 4096, 192)):  # 128 pair tiles (wide), 128 narrow-able
     g = make_gemm_inputs(M, N, K, seed=2, device="cuda")
     gemm(g["A"], g["B"])
