@@ -979,7 +979,10 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
           // engine (global stores from 256 threads would queue in the load/store unit ahead of the
           // LSE2/D broadcasts the next phases need), and no barrier wider than the warp
           const uint32_t stg = smem_u32(sDS) + wg * (C::T128 / 2) + lb * 128;
-          if (lane == 0) tma_store_wait_read0();  // this warp's previous copy has read its rows
+#ifndef HK_DS_NOWAIT
+#define HK_DS_NOWAIT 0  // timing experiment only (races the previous copy's smem read)
+#endif
+          if (lane == 0 && !HK_DS_NOWAIT) tma_store_wait_read0();  // this warp's previous copy has read its rows
           __syncwarp();
 #pragma unroll
           for (int k = 0; k < 8; ++k)
