@@ -454,6 +454,15 @@ def time_breakdown(pb, steps, warmup, world):
     return {n: statistics.fmean(t) for n, t in per.items()}
 
 
+def bwd_path(pb):
+    """Which backward the public attn_bwd runs for this problem (its default workspace decides)."""
+    if pb.d == 64:
+        return "fused single pass (dQ partials by bulk tensor reduce, NEXT #1)"
+    if pb.ds:
+        return f"stored dS ({pb.ds_bytes / 1e9:.1f} GB workspace): dK/dV pass + one-GEMM dQ pass"
+    return "two-pass (dK/dV pass, dQ pass recomputing S and dP)"
+
+
 def kernel_table(pb, kern_ms, peaks, world, sm_mhz=None):
     """Per-kernel algorithmic / executed rates and the roofline of the dominant kernel."""
     ff = pb.fwd_flops
@@ -531,7 +540,7 @@ def sub_record(name, args, peaks):
            "fwd_tflops": round(ff / (statistics.fmean(fwd_ms) * 1e-3) / 1e12, 1),
            "bwd_tflops": round(2.5 * ff / (statistics.fmean(bwd_ms) * 1e-3) / 1e12, 1),
            "pct_of_burst": round(100 * 3.5 * ff / (ms * 1e-3) / 1e12 / peaks["burst"], 2),
-           "step_ms_stats": step_stats(step_ms), "kernels": table,
+           "step_ms_stats": step_stats(step_ms), "kernels": table, "bwd_path": bwd_path(pb),
            "dominant": {"kernel": dom, "frac_of_burst": roof["frac"], "achieved": roof["achieved"]},
            "clocks": clk}
     del pb
@@ -677,7 +686,8 @@ def main():
            "scaling": args.scaling,
            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (i.i.d. N(0,1) rounded to bf16, P:538)",
            "config": {"workload": args.config, "label": label, "global_batch": pb.B_global, "B_per_gpu": pb.B,
-                      "N": N, "Hq": Hq, "Hkv": Hkv, "d": d, "causal": causal, "parallelism": par, "l2": pb.l2_note},
+                      "N": N, "Hq": Hq, "Hkv": Hkv, "d": d, "causal": causal, "parallelism": par, "l2": pb.l2_note,
+                      "bwd_path": bwd_path(pb)},
            "per_gpu_tflops": round(value / world, 2),
            "pct_of_peak": {"burst": round(100 * value / world / peaks["burst"], 2),
                            "sustained": round(100 * value / world / peaks["sustained"], 2),
