@@ -59,6 +59,11 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Arrive on another CTA's barrier with the default .release.cta semantics (as CUTLASS's
+// ClusterBarrier::arrive(cta_id)): enough where tcgen05 fences order the work being signalled
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
@@ -233,6 +238,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const int row = mt * 256 + rank * 128 + r;
       __nv_bfloat16* crow = p.c + (size_t)row * p.N + nt * BNP;
+#ifndef HK_GEMM_EPI_EARLY
+#define HK_GEMM_EPI_EARLY 1
+#endif
+      if (HK_GEMM_EPI_EARLY) {
+        // each 256-column half: read all of it out of TMEM (packed to bf16 as it arrives), release it to
+        // the MMA warp, then store — the release no longer waits behind this half's global stores, and
+        // it uses the .release.cta form of the remote arrive (the .release.cluster form compiles to a
+        // full memory barrier, which would wait for the previous half's stores to complete)
+#pragma unroll 1
+        for (int h = 0; h < NB; ++h) {
+          uint32_t pk[128];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint32_t v[32];
+            tmem_ld32(tmem_addr(tbase + acc * 256, lane_base, 256 * h + 32 * c), v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) pk[16 * c + k] = pack_bf16(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(tempty_leader + 8 * (NB == 1 ? acc : h));
+          uint4* dst = reinterpret_cast<uint4*>(crow + 256 * h);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) dst[k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+        }
+      } else {
 #pragma unroll 1
       for (int c0 = 0; c0 < BNP; c0 += 32) {
         uint32_t v[32];
@@ -250,6 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         uint4* dst = reinterpret_cast<uint4*>(crow + c0);
 #pragma unroll
         for (int k = 0; k < 4; ++k) dst[k] = o[k];
+      }
       }
     }
   }
