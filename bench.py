@@ -511,6 +511,13 @@ def kernel_table(pb, kern_ms, peaks, world, sm_mhz=None):
             "frac_of_spec_2250": round(ach / SPEC_PEAK_TFLOPS, 4),
             "algorithmic_flops_per_launch": alg[dom], "executed_flops_per_launch": execd[dom],
             "timing": "mean launch duration from CUDA events between kernels (timed region 2)"}
+    # the backward as a whole: the method's 5 backward GEMMs (2.5 x the forward's FLOPs, reading #14)
+    # over the summed kernel times, whichever path (two-pass / stored dS / fused) ran them
+    bwd_ms = sum(ms for n, ms in kern_ms.items() if n != "fwd")
+    if bwd_ms > 0:
+        b_ach = 2.5 * ff / (bwd_ms * 1e-3) / 1e12
+        roof["backward_path"] = {"kernels": [n for n in kern_ms if n != "fwd"], "ms": round(bwd_ms, 4),
+                                 "algorithmic_tflops": round(b_ach, 1), "frac": round(b_ach / peaks["burst"], 4)}
     return table, roof, dom
 
 
