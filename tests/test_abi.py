@@ -108,3 +108,22 @@ def test_host_only_validation_next4(lib):
     assert L.hk_attn_merge(p, p, p, p, None, 1, 128, 2, 64, 0, None) == 1       # buffers overlap
     assert L.hk_accum_bf16(p, p, None, Z(12), 0, None) == 1                     # n % 8
     assert L.hk_accum_bf16(None, None, p, Z(16), 0, None) == 1                  # nothing to read
+
+
+def test_stored_ds_workspace_size(lib):
+    """hk_attn_bwd_ds_workspace_bytes (host only): the plain workspace rounded up to 1024 bytes plus
+    one 32 KB bf16 dS tile per visited 128 x 128 block — the T(T+1)/2 triangle for causal Nq == Nk,
+    the Tq x Tk rectangle otherwise — and exactly the plain size where the path does not apply (d = 64)."""
+    from paper_2511_08083_b200 import _lib
+    L = _lib.lib()
+    for B, Hq, Hkv, Nq, Nk, causal in ((16, 32, 8, 8192, 8192, 1), (2, 4, 2, 300, 700, 1), (1, 6, 3, 777, 333, 0),
+                                       (3, 2, 1, 128, 128, 1), (1, 1, 1, 1, 1, 0)):
+        plain = L.hk_attn_bwd_qk_workspace_bytes(B, Hq, Hkv, Nq, Nk, 128)
+        Tq, Tk = -(-Nq // 128), -(-Nk // 128)
+        blocks = Tq * (Tq + 1) // 2 if (causal and Nq == Nk) else Tq * Tk
+        want = -(-plain // 1024) * 1024 + B * Hq * blocks * 128 * 128 * 2
+        assert L.hk_attn_bwd_ds_workspace_bytes(B, Hq, Hkv, Nq, Nk, 128, causal) == want
+        assert L.hk_attn_bwd_ds_workspace_bytes(B, Hq, Hkv, Nq, Nk, 64, causal) == \
+            L.hk_attn_bwd_qk_workspace_bytes(B, Hq, Hkv, Nq, Nk, 64)
+    # C3: 34.9 GB of dS tiles (16 x 32 heads x 2080 blocks x 32 KB)
+    assert L.hk_attn_bwd_ds_workspace_bytes(16, 32, 8, 8192, 8192, 128, 1) // 10**8 == 349
