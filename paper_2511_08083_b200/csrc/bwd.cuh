@@ -979,20 +979,14 @@ __global__ void __launch_bounds__(FQ ? BwdCfg<D>::THREADS1F : BwdCfg<D>::THREADS
           // engine (global stores from 256 threads would queue in the load/store unit ahead of the
           // LSE2/D broadcasts the next phases need), and no barrier wider than the warp
           const uint32_t stg = smem_u32(sDS) + wg * (C::T128 / 2) + lb * 128;
-#ifndef HK_DS_NOWAIT
-#define HK_DS_NOWAIT 0  // timing experiment only (races the previous copy's smem read)
-#endif
-          if (lane == 0 && !HK_DS_NOWAIT) tma_store_wait_read0();  // this warp's previous copy has read its rows
+          if (lane == 0) tma_store_wait_read0();  // this warp's previous copy has read its rows
           __syncwarp();
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             sts_v4(stg + lane * 128 + ((k ^ (r & 7)) << 4), dsk[4 * k], dsk[4 * k + 1], dsk[4 * k + 2], dsk[4 * k + 3]);
           fence_proxy_async_smem();
           __syncwarp();
-#ifndef HK_DS_NOSTORE
-#define HK_DS_NOSTORE 0  // experiment: stage but skip the copy to HBM (the cost of the staging alone)
-#endif
-          if (lane == 0 && !HK_DS_NOSTORE) {
+          if (lane == 0) {
             bulk_store_hint(p.ds + ds_block_index(p, w.b, hq, qi, w.jt) * DS_BLOCK_ELEMS + wg * (DS_BLOCK_ELEMS / 2) +
                                 lb * 64,
                             sDS + wg * (C::T128 / 2) + lb * 128, 32 * 128, policy_evict_first());
