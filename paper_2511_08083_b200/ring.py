@@ -162,7 +162,7 @@ class _Fanout:
     n <= 1: everything on the calling stream, in order."""
 
     def __init__(self, n: int):
-        self.main = torch.cuda.current_stream()
+        self.main = torch.cuda.current_stream() if n > 1 else None  # n <= 1 touches no CUDA state
         self.side = [torch.cuda.Stream() for _ in range(n)] if n > 1 else []
         self.i = 0
 

@@ -105,3 +105,123 @@ def test_distring_gloo_rotation(world):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert all(res[r] for r in range(world)), res
+
+
+# ---------------------------------------------------------------- backward schedule on CPU
+def _share_bwd(q, k, v, o, lse, do, causal, workspace=None, dq=None, dk=None, dv=None, deterministic=True,
+               accumulate=True):
+    """Stand-in for the kernel call the ring backward makes (hk_attn_bwd with the final O, LSE, adding into
+    fp32 accumulators): the gradient share of one (query chunk, key chunk) pair, written out from the
+    analytic backward with the GLOBAL O and LSE — P = exp(S - LSE), D = rowsum(dO O), dS = P (dP - D)."""
+    assert accumulate
+    B, c, Hq, d = q.shape
+    Hkv = k.shape[2]
+    G = Hq // Hkv
+    sc = 1.0 / np.sqrt(d)
+    for h in range(Hq):
+        kh = h // G
+        S = torch.einsum("bid,bjd->bij", q[:, :, h], k[:, :, kh]) * sc
+        if causal:
+            S = S.masked_fill(torch.triu(torch.ones(c, c, dtype=torch.bool), 1), float("-inf"))
+        P = torch.exp(S - lse[:, h, :, None])
+        dP = torch.einsum("bid,bjd->bij", do[:, :, h], v[:, :, kh])
+        D = (do[:, :, h] * o[:, :, h]).sum(-1, keepdim=True)
+        dS = P * (dP - D)
+        dq[:, :, h] += (torch.einsum("bij,bjd->bid", dS, k[:, :, kh]) * sc).to(dq.dtype)
+        dk[:, :, kh] += (torch.einsum("bij,bid->bjd", dS, q[:, :, h]) * sc).to(dk.dtype)
+        dv[:, :, kh] += torch.einsum("bij,bid->bjd", P, do[:, :, h]).to(dv.dtype)
+    return dq, dk, dv
+
+
+def _cpu_kernels(monkeypatch):
+    from paper_2511_08083_b200 import api
+    import contextlib
+
+    def accum(acc, x, out=None, init=False):
+        if acc is not None and x is not None:
+            acc.copy_((0 if init else acc) + x.to(acc.dtype))
+        if out is not None:
+            out.copy_(acc)
+
+    monkeypatch.setattr(api, "attn_bwd", _share_bwd)
+    monkeypatch.setattr(api, "accum_f32", lambda acc, x: acc.add_(x))
+    monkeypatch.setattr(api, "sm_budget", lambda n: contextlib.nullcontext())
+    monkeypatch.setattr(ring, "_accum", accum)
+
+
+def _bwd_case(P, causal, seed=4):
+    B, c, Hq, Hkv, d = 1, 4, 4, 2, 8
+    N = 2 * P * c
+    g = np.random.default_rng(seed)
+    Q, K, V, dO = (g.standard_normal((B, N, h, d)) for h in (Hq, Hkv, Hkv, Hq))
+    ref = oracle.attn_fwd_bwd(Q, K, V, dO, causal)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a))
+    O, LSE = t(ref["O"]), t(ref["LSE"])
+    shard = lambda x, r: ring.zigzag_shard(t(x), P, r)
+    lse_sh = lambda r: tuple(x.transpose(1, 2).contiguous() for x in ring.zigzag_shard(LSE.transpose(1, 2), P, r))
+    return ref, shard, lse_sh, Q, K, V, dO, O
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("causal", [False, True])
+def test_backward_schedule_loopback_equals_whole_sequence(P, causal, monkeypatch):
+    """ring_attn_bwd's schedule — K/V one step ahead, the fp32 dK/dV accumulators one step behind the
+    compute (each rank's contributions formed while the previous rank's sums travel, then added and
+    sent on, the last send bringing every chunk home) — with the kernels replaced by the analytic
+    share of each chunk pair: the whole-sequence gradients of the fp64 oracle."""
+    _cpu_kernels(monkeypatch)
+    ref, shard, lse_sh, Q, K, V, dO, O = _bwd_case(P, causal)
+    qs = [shard(Q, r) for r in range(P)]
+    ks = [shard(K, r) for r in range(P)]
+    vs = [shard(V, r) for r in range(P)]
+    dos = [shard(dO, r) for r in range(P)]
+    os_ = [ring.zigzag_shard(O, P, r) for r in range(P)]
+    lses = [lse_sh(r) for r in range(P)]
+    res = ring.ring_attn_bwd(qs, ks, vs, os_, lses, dos, causal, ring.LoopbackRing(P))
+    for i, n in enumerate(("dQ", "dK", "dV")):
+        got = ring.zigzag_unshard([r[i] for r in res]).numpy()
+        np.testing.assert_allclose(got, ref[n], atol=2e-5, rtol=1e-4, err_msg=n)
+
+
+def _bwd_worker(rank, world, port, causal, out):
+    import contextlib
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2511_08083_b200 import api
+
+    def accum(acc, x, out_=None, init=False):
+        if acc is not None and x is not None:
+            acc.copy_((0 if init else acc) + x.to(acc.dtype))
+        if out_ is not None:
+            out_.copy_(acc)
+    api.attn_bwd = _share_bwd
+    api.accum_f32 = lambda acc, x: acc.add_(x)
+    api.sm_budget = lambda n: contextlib.nullcontext()
+    ring._accum = accum
+    ref, shard, lse_sh, Q, K, V, dO, O = _bwd_case(world, causal)
+    (dq, dk, dv), = ring.ring_attn_bwd([shard(Q, rank)], [shard(K, rank)], [shard(V, rank)],
+                                       [ring.zigzag_shard(O, world, rank)], [lse_sh(rank)], [shard(dO, rank)],
+                                       causal, ring.DistRing())
+    ok = True
+    for n, got in (("dQ", dq), ("dK", dk), ("dV", dv)):
+        want = ring.zigzag_shard(torch.from_numpy(np.ascontiguousarray(ref[n])), world, rank)
+        ok = ok and all(np.allclose(a.numpy(), b.numpy(), atol=2e-5, rtol=1e-4) for a, b in zip(got, want))
+    out.put((rank, bool(ok)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_backward_schedule_gloo_two_ranks(causal):
+    """The same backward schedule over torch.distributed (gloo, 2 processes, DistRing)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bwd_worker, args=(r, 2, port, causal, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(res.values()), res
