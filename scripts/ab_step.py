@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--warm-s", type=float, default=1.5)
     ap.add_argument("--steps", type=int, default=15)
     ap.add_argument("--rounds", type=int, default=2)
+    ap.add_argument("--ds", action="store_true", help="size the workspace for the stored-dS backward (d = 128)")
     a = ap.parse_args()
     try:
         import pynvml
@@ -56,7 +57,13 @@ def main():
     dq, dk, dv = torch.empty_like(x["Q"]), torch.empty_like(x["K"]), torch.empty_like(x["V"])
     names = a.libs.split(",")
     libs = {n: load(n) for n in names}
-    wsb = max(L.hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d) for L in libs.values())
+    if a.ds:
+        for L in libs.values():
+            L.hk_attn_bwd_ds_workspace_bytes.restype = ctypes.c_size_t
+            L.hk_attn_bwd_ds_workspace_bytes.argtypes = [ctypes.c_int] * 7
+        wsb = max(L.hk_attn_bwd_ds_workspace_bytes(B, Hq, Hkv, N, N, d, int(causal)) for L in libs.values())
+    else:
+        wsb = max(L.hk_attn_bwd_workspace_bytes(B, Hq, Hkv, N, d) for L in libs.values())
     ws = torch.zeros(wsb // 4 + 64, device="cuda", dtype=torch.float32)
     P = lambda t: ctypes.c_void_p(t.data_ptr())
     sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
