@@ -22,6 +22,9 @@ CASES = [
     (1, 500, 260, 6, 3, True),      # Nq > Nk: key-less query rows
     (1, 777, 333, 6, 3, False),
     (2, 2048, 2048, 16, 4, True),   # 256 query items on 148 CTAs: several items per CTA in both passes
+    (1, 512, 512, 16, 2, True),     # G = 8 (the 70B head geometry)
+    (3, 1000, 1000, 8, 8, True),    # MHA, ragged, 3 sequences
+    (2, 640, 640, 4, 1, False),     # MQA (Hkv = 1), non-causal
 ]
 
 
